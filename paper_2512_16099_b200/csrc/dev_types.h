@@ -1,0 +1,135 @@
+// Device-side record layouts shared by the kernels (engine_core.cuh) and the
+// host runtime (host_runtime.cpp).  Plain PODs, no CUDA types.
+#pragma once
+#include <stdint.h>
+
+namespace msgk {
+
+// Slot states: one slot per (GPU, start index) — instances on a GPU are
+// pairwise slice-disjoint (gpu.cpp:146-156), so a start index names at most
+// one instance.  Instance::busy()/idle()/draining (gpu.hpp:18-29) plus the
+// job's RunJob state (sim.cpp:58-68) folded in:
+enum : uint8_t {
+    ST_EMPTY = 0,  // no instance
+    ST_IDLE = 1,   // instance without job, not draining
+    ST_RUN = 2,    // job bound and Running            (Completion timer)
+    ST_WAIT = 3,   // job bound, WaitingStart          (ServiceStart timer)
+    ST_DRAIN = 4   // draining source replica          (MigrationEnd timer)
+};
+
+// Feature / output flags.
+enum : uint32_t {
+    CF_LB = 1u,      // FeatureFlags::load_balancing
+    CF_DYN = 2u,     // FeatureFlags::dynamic_partitioning
+    CF_MIG = 4u      // FeatureFlags::migration
+};
+enum : uint32_t { OF_JOBS = 1u, OF_EVENTS = 2u, OF_TIMELINE = 4u };
+
+struct DevConfig {
+    double alpha;     // SimConfig::contention_alpha
+    double overlap;   // SimConfig::migration_overlap_s
+    double latency;   // SimConfig::reconfig_latency_s
+    int32_t G;        // SimConfig::gpu_count
+    uint32_t flags;   // CF_*
+    uint32_t lazymask;  // bit pc set iff pc/7.0 < threshold (gpu.cpp:168-177)
+    uint32_t n_init;    // static-layout instances (sim.cpp:86-95)
+    uint32_t init_off;  // offset into the init-slot array
+    uint32_t reserved;
+};
+
+// Packed static-layout instance: slot | profile << 16 (creation order = array order).
+struct DevTrace {
+    uint64_t job_off;   // first job (rank order) in the batch arrays
+    uint64_t ev_off;    // first event record
+    uint64_t tl_off;    // first timeline sample
+    uint32_t n_jobs;
+    uint32_t cfg;
+    uint32_t ev_cap;
+    uint32_t tl_cap;
+    uint32_t has_perm;  // arrival order differs from rank order
+    uint32_t reserved;
+};
+
+// Fixed 32-byte event record written by the kernel (decoded on the host into
+// msg_event, include/migsched_b200.h).
+struct EventRec {
+    double t;
+    uint64_t aux;      // bits of scheduled_s; MigrationStart: 4 x u16 cost numerators over 25200
+    int32_t job;       // job rank (dense id order), -1 none
+    uint16_t gpu;      // gpu / from_gpu
+    uint16_t gpu2;     // to_gpu
+    uint8_t kind;      // msg EventKind
+    uint8_t profile;
+    uint8_t start;     // start / from_start
+    uint8_t start2;    // to_start
+    uint8_t flags;     // EF_*
+    uint8_t pad[3];
+};
+static_assert(sizeof(EventRec) == 32, "EventRec must be 32 bytes");
+enum : uint8_t { EF_REUSED = 1, EF_PLACED = 2, EF_DESTROY = 4, EF_INTER = 8 };
+
+struct JobOut {
+    double sched;      // service start (scheduled_s)
+    double done;       // completion time
+    int32_t gpu;       // final GPU
+    int32_t mig;       // migrations
+};
+
+struct DevSummary {
+    int32_t status;
+    uint32_t reserved;
+    uint64_t handler_events;
+    uint64_t n_events;
+    uint64_t timeline_samples;
+    int64_t migrations;
+    int64_t reconfig_ops;
+    int64_t enqueues;
+    int64_t dequeues;
+    int32_t max_arr;
+    int32_t max_intra;
+    int32_t max_inter;
+    int32_t pending_rank;   // smallest queued job rank when JobsPending
+    double mean_wait;
+    double mean_exec;
+    double mean_turn;
+    double makespan;
+    double tl_sum;
+};
+
+// Read-only lookup tables computed on the host from the exact-rational
+// fragmentation metric (frag.cpp:44-58) and staged into shared memory.
+struct DevTables {
+    uint8_t cost2rank[8 * 256];  // [popc(busy_c)][busy_m] -> rank of the 2-mask cost
+    uint32_t feas[256];          // blocked_m -> 6 x 3-bit feasible counts
+    uint32_t ideal[8 * 9];       // [popc busy_c][popc busy_m] -> 6 x 3-bit ideal counts
+    uint16_t rank2k[32];         // cost rank -> numerator over 25200
+    uint8_t placeable[256];      // blocked_m -> profiles with >= 1 free legal start
+};
+
+// Kernel arguments of the per-trace event loop (engine_core.cuh).
+struct SimArgs {
+    const DevTrace* traces;
+    const DevConfig* configs;
+    const uint32_t* init_slots;
+    const DevTables* tables;
+    const double* arrival;   // rank order
+    const double* service;
+    const uint8_t* profile;
+    const uint32_t* perm;    // arrival order -> rank (only traces with has_perm)
+    int32_t* queue;          // FCFS queue storage, n_jobs per trace
+    JobOut* jobs;
+    EventRec* events;
+    double* timeline;        // (t, mean) pairs
+    DevSummary* summary;
+    uint32_t n_traces;
+    uint32_t out_flags;
+};
+
+// Constant geometry (profiles.cpp:8-15), packed per profile id.
+constexpr uint32_t kCsPack = 0x112347u;               // nibble p: compute slices
+constexpr uint32_t kMsPack = 0x122448u;               // nibble p: memory slices
+constexpr uint64_t kStartMask = 0x00007F5515110101ull;  // byte p: legal starts
+constexpr uint32_t kStridePack = 0x122488u;           // nibble p: start stride
+constexpr uint32_t kCountPack = 0x743211u;            // nibble p: number of starts
+
+}  // namespace msgk

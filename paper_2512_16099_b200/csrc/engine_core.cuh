@@ -1,0 +1,895 @@
+// engine_core.cuh — one warp replays one trace of the reference's
+// discrete-event MIG scheduler (proj/src/sim.cpp:71-410) bit-exactly.
+//
+// Layout (per warp, in shared memory, WarpSmem<SPL>): one slot per
+// (GPU g, start s) — slot = 8g + s — holding the instance that starts at s
+// (profile, state, creation sequence) and, when a job is bound, that job's
+// runtime state (remaining work, last update, timer time, migrations).
+// Lane L owns slots L, L+32, ... (SPL = slots per lane), so the 8 slots of
+// one GPU sit in 8 consecutive lanes.  A per-GPU word caches the busy
+// compute / busy memory / blocked memory masks and the running-job count.
+//
+// Every timer of the reference's heap (sim.cpp:37-56) lives in a slot:
+//   ST_RUN   -> Completion   (kind 0) at the latest prediction
+//   ST_DRAIN -> MigrationEnd (kind 1) of the draining source replica
+//   ST_WAIT  -> ServiceStart (kind 2)
+// plus the next Arrival (kind 3) prefetched from HBM.  The next event is a
+// warp-wide lexicographic argmin over (time, kind, job id, push seq) done
+// with three REDUX.MIN steps — the same order TimerLater imposes, minus the
+// stale completions the reference pops and ignores (sim.cpp:271-273).
+//
+// All placement / planner scoring is integer: the fragmentation cost of a
+// post-placement mask pair is a rank (0..30) looked up in a 2 KiB table
+// computed from the exact rational metric (frag.cpp:44-58); ranks are
+// order-isomorphic to Frac comparisons, so packed u32 keys
+// [pass|cost|!reused|gpu|start] reduce with a single REDUX.MIN.
+//
+// FP64 arithmetic uses the _rn intrinsics only (no contraction), replaying
+// the reference's exact operation sequence.
+#pragma once
+#include "dev_types.h"
+#include "warp_prims.cuh"
+
+namespace msgk {
+
+constexpr unsigned NONE = 0xFFFFFFFFu;
+constexpr int MAX_JOB_BITS = 22;  // job ranks < 2^22 (inter key layout)
+
+// EventKind (sim.hpp:20-28)
+enum : uint8_t {
+    EV_ARRIVAL = 0,
+    EV_COMPLETION = 1,
+    EV_MIGRATION_START = 2,
+    EV_MIGRATION_END = 3,
+    EV_RECONFIG = 4,
+    EV_ENQUEUE = 5,
+    EV_DEQUEUE = 6
+};
+enum : int32_t { STATUS_OK = 0, STATUS_JOBS_PENDING = 12 };
+
+// ---- MIG geometry (profiles.cpp:8-15, 43-57) ------------------------------
+MSG_DI unsigned cs_of(int p) { return (kCsPack >> (4 * p)) & 0xFu; }
+MSG_DI unsigned ms_of(int p) { return (kMsPack >> (4 * p)) & 0xFu; }
+MSG_DI unsigned startmask_of(int p) { return (unsigned)(kStartMask >> (8 * p)) & 0xFFu; }
+MSG_DI unsigned stride_of(int p) { return (kStridePack >> (4 * p)) & 0xFu; }
+MSG_DI unsigned count_of(int p) { return (kCountPack >> (4 * p)) & 0xFu; }
+// slice_footprint: compute bits [s, s+cs), memory bits [s, s+ms).
+MSG_DI unsigned fpc(int p, int s) { return ((1u << cs_of(p)) - 1u) << s; }
+MSG_DI unsigned fpm(int p, int s) { return ((1u << ms_of(p)) - 1u) << s; }
+
+// ---- per-GPU word: busy_c | busy_m<<8 | blocked_m<<16 | running<<24 --------
+MSG_DI unsigned w_bc(unsigned w) { return w & 0x7Fu; }
+MSG_DI unsigned w_bm(unsigned w) { return (w >> 8) & 0xFFu; }
+MSG_DI unsigned w_km(unsigned w) { return (w >> 16) & 0xFFu; }
+MSG_DI unsigned w_k(unsigned w) { return (w >> 24) & 0xFu; }
+
+// Order-preserving u64 image of a double (-0 canonicalised to +0, which the
+// reference's `a.time != b.time` also treats as equal).
+MSG_DI uint64_t time_key(double t) {
+    const uint64_t b = wp::dbits(wp::dadd(t, 0.0));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+MSG_DI unsigned q420(unsigned id) {  // 420 / ideal, ideal in 1..7 (frag.cpp:10,55)
+    return id == 1 ? 420u : id == 2 ? 210u : id == 3 ? 140u : id == 4 ? 105u : id == 5 ? 84u
+           : id == 6 ? 70u : 60u;
+}
+MSG_DI unsigned q60(unsigned c) {  // 60 / counted, counted in 1..6
+    return c == 1 ? 60u : c == 2 ? 30u : c == 3 ? 20u : c == 4 ? 15u : c == 5 ? 12u : 10u;
+}
+
+template <int SPL>
+struct WarpSmem {
+    static constexpr int NS = 32 * SPL;  // slots
+    static constexpr int NG = 4 * SPL;   // GPUs
+    double rem[NS];    // RunJob::remaining_work (WAIT: service demand)
+    double last[NS];   // RunJob::last_update
+    double tkey[NS];   // timer time of the slot
+    double gcost[NG];  // frag_cost(gpu) for the timeline (4-mask form)
+    int32_t job[NS];   // bound job rank (RUN/WAIT) or migrating job (DRAIN)
+    uint32_t cseq[NS]; // instance creation order (vector order, gpu.cpp:88-111)
+    uint32_t mseq[NS]; // MigrationEnd push sequence
+    uint32_t gw[NG];   // per-GPU mask word
+    uint16_t mig[NS];  // migrations of the bound job
+    uint8_t prof[NS];  // instance profile
+    uint8_t st[NS];    // ST_*
+};
+
+
+struct CreateRes {
+    bool reused;
+    unsigned dmask;  // destroyed slots (bit = start) on the GPU
+    unsigned dprof;  // lane-local (lanes 0..7): profile of the slot before
+    unsigned dseq;   // lane-local: creation sequence of the slot before
+};
+
+struct Decision {
+    bool placed;
+    bool reused;
+    int g;
+    int s;
+    unsigned evals;
+};
+
+template <int SPL>
+struct TraceSim {
+    using WS = WarpSmem<SPL>;
+    WS* sm;
+    const DevTables* tb;
+    const double* arr;
+    const double* svc;
+    const uint8_t* prf;
+    const uint32_t* perm;
+    int32_t* queue;
+    JobOut* jobs;
+    EventRec* evs;
+    double* tl;
+    uint32_t N, ev_cap, tl_cap, oflags;
+    // SimConfig
+    int G;
+    uint32_t cflags, lazymask;
+    double alpha, overlap, latency;
+    // warp-uniform engine state
+    unsigned L;
+    double now;
+    uint32_t a_idx, a_rank;
+    int a_prof;
+    double a_t, a_svc;
+    uint32_t q_head, q_tail;
+    uint32_t cseq_ctr, mseq_ctr;
+    uint64_t n_ev, n_handler, n_tl;
+    int64_t n_mig, n_reconf, n_enq, n_deq;
+    int max_arr, max_intra, max_inter;
+    double tl_sum, tl_mean;
+    bool tl_dirty;
+
+    // ---------------------------------------------------------------- tables
+    MSG_DI unsigned rank2(unsigned bc, unsigned bm) const {
+        return tb->cost2rank[wp::popc(bc) * 256 + bm];
+    }
+    MSG_DI unsigned k2w(unsigned w) const { return tb->rank2k[rank2(w_bc(w), w_bm(w))]; }
+    // 4-mask cost numerator over 25200: busy drives ideal, blocked drives
+    // feasibility (frag.cpp:44-58 via frag_cost_exact, :60-63).
+    MSG_DI unsigned k4w(unsigned w) const {
+        const unsigned ideal = tb->ideal[wp::popc(w_bc(w)) * 9 + wp::popc(w_bm(w))];
+        const unsigned feas = tb->feas[w_km(w)];
+        unsigned ratio = 0, counted = 0;
+#pragma unroll
+        for (int p = 0; p < 6; ++p) {
+            const unsigned id = (ideal >> (3 * p)) & 7u;
+            if (id) {
+                ratio += ((feas >> (3 * p)) & 7u) * q420(id);
+                ++counted;
+            }
+        }
+        if (!counted) return 0;
+        return (420u * counted - ratio) * q60(counted);
+    }
+
+    // --------------------------------------------------------------- events
+    MSG_DI void emit(uint8_t kind, int32_t job, unsigned gpu, unsigned gpu2, unsigned prof,
+                     unsigned start, unsigned start2, unsigned flags, uint64_t aux) {
+        if ((oflags & OF_EVENTS) && n_ev < ev_cap && L == 0) {
+            EventRec r;
+            r.t = now;
+            r.aux = aux;
+            r.job = job;
+            r.gpu = (uint16_t)gpu;
+            r.gpu2 = (uint16_t)gpu2;
+            r.kind = kind;
+            r.profile = (uint8_t)prof;
+            r.start = (uint8_t)start;
+            r.start2 = (uint8_t)start2;
+            r.flags = (uint8_t)flags;
+            r.pad[0] = r.pad[1] = r.pad[2] = 0;
+            evs[n_ev] = r;
+        }
+        ++n_ev;
+    }
+
+    // ---------------------------------------------------------------- setup
+    MSG_DI void setup(const SimArgs& a, const DevTables* tables, WS* ws, uint32_t t) {
+        L = wp::lane();
+        sm = ws;
+        tb = tables;
+        const DevTrace tr = a.traces[t];
+        const DevConfig c = a.configs[tr.cfg];
+        N = tr.n_jobs;
+        arr = a.arrival + tr.job_off;
+        svc = a.service + tr.job_off;
+        prf = a.profile + tr.job_off;
+        perm = tr.has_perm ? a.perm + tr.job_off : nullptr;
+        queue = a.queue + tr.job_off;
+        jobs = a.jobs + tr.job_off;
+        evs = a.events ? a.events + tr.ev_off : nullptr;
+        tl = a.timeline ? a.timeline + 2 * tr.tl_off : nullptr;
+        ev_cap = tr.ev_cap;
+        tl_cap = tr.tl_cap;
+        oflags = a.out_flags;
+        if (!evs) oflags &= ~OF_EVENTS;
+        if (!tl) oflags &= ~OF_TIMELINE;
+        G = c.G;
+        cflags = c.flags;
+        lazymask = c.lazymask;
+        alpha = c.alpha;
+        overlap = c.overlap;
+        latency = c.latency;
+        now = 0.0;
+        a_idx = 0;
+        q_head = q_tail = 0;
+        mseq_ctr = 0;
+        n_ev = n_handler = n_tl = 0;
+        n_mig = n_reconf = n_enq = n_deq = 0;
+        max_arr = max_intra = max_inter = 0;
+        tl_sum = 0.0;
+        tl_mean = 0.0;
+        tl_dirty = true;
+#pragma unroll
+        for (int i = 0; i < SPL; ++i) {
+            const int slot = L + 32 * i;
+            sm->st[slot] = ST_EMPTY;
+            sm->mig[slot] = 0;
+        }
+        if (L < (unsigned)WS::NG) {
+            sm->gw[L] = 0;
+            sm->gcost[L] = 0.0;  // empty GPU: cost 0 (every ratio is 1)
+        }
+        wp::sync();
+        // Static layout: pre-provisioned idle instances (sim.cpp:86-95).
+        if (L == 0) {
+            for (uint32_t k = 0; k < c.n_init; ++k) {
+                const uint32_t v = a.init_slots[c.init_off + k];
+                const int slot = (int)(v & 0xFFFFu);
+                sm->st[slot] = ST_IDLE;
+                sm->prof[slot] = (uint8_t)(v >> 16);
+                sm->cseq[slot] = k;
+            }
+        }
+        cseq_ctr = c.n_init;
+        if (c.n_init) {
+            for (int g = 0; g < G; ++g) refresh_gpu(g);
+        }
+        load_arrival();
+        wp::sync();
+    }
+
+    // Prefetch the next arrival timer (pushed in trace order, popped in
+    // (time, job id) order: sim.cpp:118-120 with TimerLater).
+    MSG_DI void load_arrival() {
+        if (a_idx < N) {
+            const uint32_t r = perm ? perm[a_idx] : a_idx;
+            a_rank = r;
+            a_t = arr[r];
+            a_prof = prf[r];
+            a_svc = svc[r];
+        }
+    }
+
+    // ---------------------------------------------------------- GPU masks
+    // Recompute GPU g's word from its 8 slots: busy/blocked masks
+    // (gpu.cpp:10-48) and the running count running_on_ (sim.cpp:405).
+    MSG_DI unsigned refresh_gpu(int g) {
+        wp::sync();
+        unsigned c = 0, r = 0;
+        if (L < 8) {
+            const int sl = g * 8 + (int)L;
+            const uint8_t s = sm->st[sl];
+            if (s >= ST_RUN) {
+                const int p = sm->prof[sl];
+                const unsigned m = fpm(p, (int)L);
+                c = (s == ST_DRAIN) ? (m << 16) : (fpc(p, (int)L) | (m << 8) | (m << 16));
+                r = (s == ST_RUN) ? 1u : 0u;
+            }
+        }
+        const unsigned w = wp::ror(c) | (wp::radd(r) << 24);
+        if (L == 0) {
+            sm->gw[g] = w;
+            sm->gcost[g] = wp::ddiv((double)k4w(w), 25200.0);
+        }
+        tl_dirty = true;
+        wp::sync();
+        return w;
+    }
+
+    // ------------------------------------------------- contention model
+    // slowdown(k) = 1 + alpha*(k-1) (sim.cpp:26-31): DMUL then DADD.
+    MSG_DI double factor(unsigned k) const {
+        return wp::dadd(1.0, wp::dmul(alpha, (double)((int)k - 1)));
+    }
+
+    // advance_all (sim.cpp:153-165)
+    MSG_DI void advance_all() {
+        wp::sync();
+#pragma unroll
+        for (int i = 0; i < SPL; ++i) {
+            const int slot = L + 32 * i;
+            if (sm->st[slot] == ST_RUN) {
+                const double dt = wp::dsub(now, sm->last[slot]);
+                if (dt > 0.0) {
+                    const double f = factor(w_k(sm->gw[slot >> 3]));
+                    sm->rem[slot] = wp::dsub(sm->rem[slot], wp::ddiv(dt, f));
+                }
+                sm->last[slot] = now;
+            }
+        }
+    }
+
+    // reschedule_completions (sim.cpp:167-175): prediction now + max(rem,0)*f.
+    MSG_DI void reschedule() {
+        wp::sync();
+#pragma unroll
+        for (int i = 0; i < SPL; ++i) {
+            const int slot = L + 32 * i;
+            if (sm->st[slot] == ST_RUN) {
+                const double f = factor(w_k(sm->gw[slot >> 3]));
+                double r = sm->rem[slot];
+                if (r < 0.0) r = 0.0;  // std::max(rem, 0.0)
+                sm->tkey[slot] = wp::dadd(now, wp::dmul(r, f));
+            }
+        }
+    }
+
+    // sample_timeline (sim.cpp:177-181): sequential sum in GPU order / G.
+    MSG_DI void sample() {
+        if (tl_dirty) {
+            wp::sync();
+            double tot = 0.0;
+            for (int g = 0; g < G; ++g) tot = wp::dadd(tot, sm->gcost[g]);
+            tl_mean = wp::ddiv(tot, (double)G);
+            tl_dirty = false;
+        }
+        if ((oflags & OF_TIMELINE) && n_tl < tl_cap && L == 0) {
+            tl[2 * n_tl] = now;
+            tl[2 * n_tl + 1] = tl_mean;
+        }
+        ++n_tl;
+        tl_sum = wp::dadd(tl_sum, tl_mean);
+    }
+
+    // -------------------------------------------------------------- events
+    // Next timer pop; returns -1 none, 0 completion, 1 migration end,
+    // 2 service start, 3 arrival.
+    MSG_DI int next_event(int& ev_slot) {
+        wp::sync();
+        unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
+        int bsl = -1;
+#pragma unroll
+        for (int i = 0; i < SPL; ++i) {
+            const int slot = L + 32 * i;
+            const uint8_t s = sm->st[slot];
+            if (s >= ST_RUN) {
+                const uint64_t tk = time_key(sm->tkey[slot]);
+                const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;
+                const unsigned kind = s == ST_RUN ? 0u : (s == ST_DRAIN ? 1u : 2u);
+                const unsigned tie = (kind << 28) | (unsigned)sm->job[slot];
+                const unsigned ms = s == ST_DRAIN ? sm->mseq[slot] : 0u;
+                const bool better =
+                    hi < bhi ||
+                    (hi == bhi && (lo < blo || (lo == blo && (tie < btie || (tie == btie && ms < bms)))));
+                if (better) {
+                    bhi = hi;
+                    blo = lo;
+                    btie = tie;
+                    bms = ms;
+                    bsl = slot;
+                }
+            }
+        }
+        const unsigned mhi = wp::rmin(bhi);
+        const bool have_arrival = a_idx < N;
+        if (mhi == NONE) {
+            if (!have_arrival) return -1;
+            now = a_t;
+            return 3;
+        }
+        const unsigned mlo = wp::rmin(bhi == mhi ? blo : NONE);
+        const unsigned mtie = wp::rmin((bhi == mhi && blo == mlo) ? btie : NONE);
+        bool match = bhi == mhi && blo == mlo && btie == mtie;
+        if ((mtie >> 28) == 1u) {  // same job, same time MigrationEnds: push order
+            const unsigned mms = wp::rmin(match ? bms : NONE);
+            match = match && bms == mms;
+        }
+        if (have_arrival) {
+            const uint64_t sk = ((uint64_t)mhi << 32) | mlo;
+            if (time_key(a_t) < sk) {  // arrivals rank last on equal time
+                now = a_t;
+                return 3;
+            }
+        }
+        const int wl = wp::ffs(wp::ballot(match)) - 1;
+        ev_slot = wp::shfl(bsl, wl);
+        now = sm->tkey[ev_slot];
+        return (int)(mtie >> 28);
+    }
+
+    // ------------------------------------------------------------ schedule
+    // schedule() (scheduler.cpp:47-81) / first_fit_schedule() (:83-98) /
+    // dispatch_schedule() (:100-104) on the warp's cluster.
+    MSG_DI Decision dispatch(int p) {
+        wp::sync();
+        Decision d;
+        const unsigned smask = startmask_of(p);
+        const bool dyn = (cflags & CF_DYN) != 0;
+        if (cflags & CF_LB) {
+            unsigned kmin = NONE, nl = 0, nb = 0;
+#pragma unroll
+            for (int i = 0; i < SPL; ++i) {
+                const int slot = L + 32 * i;
+                const int g = slot >> 3, s = slot & 7;
+                if (g < G && ((smask >> s) & 1u)) {
+                    const unsigned w = sm->gw[g];
+                    const bool exact = sm->st[slot] == ST_IDLE && sm->prof[slot] == p;
+                    if ((dyn || exact) && !(fpm(p, s) & w_km(w))) {  // candidate_starts + avail
+                        const unsigned rk = rank2(w_bc(w) | fpc(p, s), w_bm(w) | fpm(p, s));
+                        const unsigned lazy = (lazymask >> wp::popc(w_bc(w))) & 1u;
+                        const unsigned key = ((lazy ^ 1u) << 31) | (rk << 26) | ((exact ? 0u : 1u) << 25) |
+                                             ((unsigned)g << 3) | (unsigned)s;
+                        kmin = key < kmin ? key : kmin;
+                        nl += lazy;
+                        nb += lazy ^ 1u;
+                    }
+                }
+            }
+            const unsigned k = wp::rmin(kmin);
+            const unsigned NL = wp::radd(nl), NB = wp::radd(nb);
+            d.evals = NL + (NL == 0 ? NB : 0u);  // Busy pass only if Lazy found nothing
+            d.placed = k != NONE;
+            d.g = (int)((k >> 3) & 0x3FFFFFu);
+            d.s = (int)(k & 7u);
+            d.reused = ((k >> 25) & 1u) == 0;
+        } else {
+            unsigned kmin = NONE;
+#pragma unroll
+            for (int i = 0; i < SPL; ++i) {
+                const int slot = L + 32 * i;
+                const int g = slot >> 3, s = slot & 7;
+                if (g < G && ((smask >> s) & 1u)) {
+                    const unsigned w = sm->gw[g];
+                    const bool exact = sm->st[slot] == ST_IDLE && sm->prof[slot] == p;
+                    if ((dyn || exact) && !(fpm(p, s) & w_km(w))) {
+                        const unsigned key = ((unsigned)g << 3) | (unsigned)s;
+                        kmin = key < kmin ? key : kmin;
+                    }
+                }
+            }
+            const unsigned k = wp::rmin(kmin);
+            d.evals = 0;  // first_fit_schedule reports no evaluations
+            d.placed = k != NONE;
+            d.g = (int)(k >> 3);
+            d.s = (int)(k & 7u);
+            d.reused = false;
+            if (d.placed) {
+                const int slot = (int)k;
+                d.reused = sm->st[slot] == ST_IDLE && sm->prof[slot] == p;
+            }
+        }
+        return d;
+    }
+
+    // ------------------------------------------------------ create_instance
+    // gpu.cpp:71-101: reuse an exact idle instance (0 ops) or destroy every
+    // idle instance overlapping the footprint (creation order) and create.
+    // Leaves the destination slot ST_RUN as a placeholder; the caller binds
+    // the job state.
+    MSG_DI CreateRes create(int g, int p, int s) {
+        wp::sync();
+        CreateRes cr;
+        const int sl = g * 8 + (int)(L & 7u);
+        const uint8_t mst = L < 8 ? sm->st[sl] : ST_EMPTY;
+        const unsigned mpr = L < 8 ? sm->prof[sl] : 0u;
+        const unsigned mseq = L < 8 ? sm->cseq[sl] : 0u;
+        cr.reused = wp::ballot(L == (unsigned)s && mst == ST_IDLE && mpr == (unsigned)p) != 0;
+        cr.dprof = mpr;
+        cr.dseq = mseq;
+        cr.dmask = 0;
+        if (!cr.reused) {
+            const bool d = L < 8 && mst == ST_IDLE && (fpm((int)mpr, (int)L) & fpm(p, s)) != 0;
+            cr.dmask = wp::ballot(d);
+            if (d) sm->st[sl] = ST_EMPTY;
+        }
+        wp::sync();
+        if (L == 0) {
+            const int dst = g * 8 + s;
+            sm->st[dst] = ST_RUN;
+            if (!cr.reused) {
+                sm->prof[dst] = (uint8_t)p;
+                sm->cseq[dst] = cseq_ctr;
+            }
+        }
+        if (!cr.reused) ++cseq_ctr;
+        wp::sync();
+        return cr;
+    }
+
+    // Reconfig events of one create_instance: destroys in instance-vector
+    // (creation) order, then the create (gpu.cpp:88-98, sim.cpp:183-195).
+    MSG_DI void emit_reconfig(int g, int p, int s, const CreateRes& cr) {
+        unsigned m = cr.dmask;
+        while (m) {
+            int lw;
+            if ((m & (m - 1u)) == 0) {
+                lw = wp::ffs(m) - 1;
+            } else {
+                const unsigned c = (L < 8 && ((m >> L) & 1u)) ? cr.dseq : NONE;
+                const unsigned mn = wp::rmin(c);
+                lw = wp::ffs(wp::ballot(c == mn && c != NONE)) - 1;
+            }
+            const int pr = wp::shfl((int)cr.dprof, lw);
+            emit(EV_RECONFIG, -1, (unsigned)g, 0, (unsigned)pr, (unsigned)lw, 0, EF_DESTROY, 0);
+            ++n_reconf;
+            m &= ~(1u << lw);
+        }
+        if (!cr.reused) {
+            emit(EV_RECONFIG, -1, (unsigned)g, 0, (unsigned)p, (unsigned)s, 0, 0, 0);
+            ++n_reconf;
+        }
+    }
+
+    // apply_placement + start_service (sim.cpp:199-218).
+    MSG_DI double apply_placement(int g, int s, int32_t r, double sv, unsigned nops) {
+        const double delay = wp::dmul((double)nops, latency);
+        const double ss = wp::dadd(now, delay);
+        const int slot = g * 8 + s;
+        if (L == 0) {
+            sm->job[slot] = r;
+            sm->mig[slot] = 0;
+            sm->rem[slot] = sv;
+            if (delay > 0.0) {
+                sm->st[slot] = ST_WAIT;
+                sm->tkey[slot] = ss;
+            } else {
+                sm->st[slot] = ST_RUN;
+                sm->last[slot] = now;
+            }
+            jobs[r].sched = ss;
+        }
+        refresh_gpu(g);
+        return ss;
+    }
+
+    // Place job r (profile p) per decision d; emits the placement event
+    // (Arrival or Dequeue) followed by its reconfig ops.
+    MSG_DI void place(const Decision& d, int32_t r, int p, double sv, uint8_t kind) {
+        const CreateRes cr = create(d.g, p, d.s);
+        const unsigned nops = (unsigned)wp::popc(cr.dmask) + (cr.reused ? 0u : 1u);
+        const double ss = apply_placement(d.g, d.s, r, sv, nops);
+        emit(kind, r, (unsigned)d.g, 0, (unsigned)p, (unsigned)d.s, 0, EF_PLACED | (cr.reused ? EF_REUSED : 0),
+             wp::dbits(ss));
+        emit_reconfig(d.g, p, d.s, cr);
+    }
+
+    // dequeue_pass / try_dequeue: strict FCFS, stop at the first head that
+    // cannot be placed (sim.cpp:325-344, scheduler.cpp:106-121).
+    MSG_DI void dequeue_pass() {
+        while (q_head < q_tail) {
+            wp::sync();
+            const int32_t h = queue[q_head];
+            const int p = prf[h];
+            const double sv = svc[h];
+            const Decision d = dispatch(p);
+            if (!d.placed) break;
+            max_arr = max_arr > (int)d.evals ? max_arr : (int)d.evals;
+            ++q_head;
+            place(d, h, p, sv, EV_DEQUEUE);
+            ++n_deq;
+        }
+    }
+
+    // ----------------------------------------------------------- migration
+    // apply_move (migration.cpp:35-69) + record_plan bookkeeping
+    // (sim.cpp:346-396): replica-first move of the job in from_slot to
+    // (tg, ts); costs are the end-state (busy-mask) costs before/after.
+    MSG_DI void apply_move(int from_slot, int tg, int ts, bool inter) {
+        wp::sync();
+        const int fg = from_slot >> 3, fs = from_slot & 7;
+        const int q = sm->prof[from_slot];
+        const int32_t r = sm->job[from_slot];
+        const uint8_t jst = sm->st[from_slot];
+        const double jrem = sm->rem[from_slot], jlast = sm->last[from_slot], jtk = sm->tkey[from_slot];
+        const unsigned jmig = sm->mig[from_slot];
+        const unsigned fcb = k2w(sm->gw[fg]);
+        const unsigned tcb = k2w(sm->gw[tg]);
+        wp::sync();
+        if (L == 0) sm->st[from_slot] = ST_DRAIN;  // start_draining
+        const CreateRes cr = create(tg, q, ts);
+        if (L == 0) {
+            const int dst = tg * 8 + ts;
+            sm->st[dst] = jst;
+            sm->job[dst] = r;
+            sm->mig[dst] = (uint16_t)(jmig + 1u);
+            sm->rem[dst] = jrem;
+            sm->last[dst] = jlast;
+            sm->tkey[dst] = jtk;
+            if (overlap <= 0.0) {
+                sm->st[from_slot] = ST_IDLE;  // finish_draining at once
+            } else {
+                sm->tkey[from_slot] = wp::dadd(now, overlap);
+                sm->mseq[from_slot] = mseq_ctr;
+            }
+        }
+        if (overlap > 0.0) ++mseq_ctr;
+        const unsigned nwf = refresh_gpu(fg);
+        const unsigned nwt = tg != fg ? refresh_gpu(tg) : nwf;
+        const uint64_t costs = (uint64_t)fcb | ((uint64_t)k2w(nwf) << 16) | ((uint64_t)tcb << 32) |
+                               ((uint64_t)k2w(nwt) << 48);
+        emit(EV_MIGRATION_START, r, (unsigned)fg, (unsigned)tg, (unsigned)q, (unsigned)fs, (unsigned)ts,
+             inter ? EF_INTER : 0, costs);
+        ++n_mig;
+        emit_reconfig(tg, q, ts, cr);
+        if (overlap <= 0.0) emit(EV_MIGRATION_END, r, (unsigned)fg, 0, 0, 0, 0, 0, 0);
+    }
+
+    // plan_intra (migration.cpp:71-123): greedy, strictly improving moves of
+    // one busy job to another legal start on the same GPU; key
+    // (cost, job id, start).
+    MSG_DI void plan_intra(int g) {
+        for (;;) {
+            wp::sync();
+            const unsigned w = sm->gw[g];
+            const unsigned bc = w_bc(w), bm = w_bm(w), km = w_km(w);
+            const unsigned cur = rank2(bc, bm);
+            const int own = (int)(L & 7u);
+            const int sl = g * 8 + own;
+            const uint8_t s = sm->st[sl];
+            unsigned kmin = NONE, cnt = 0;
+            if (s == ST_RUN || s == ST_WAIT) {
+                const int q = sm->prof[sl];
+                const unsigned r = (unsigned)sm->job[sl];
+                const unsigned ofc = fpc(q, own), ofm = fpm(q, own);
+                const unsigned n = count_of(q), stride = stride_of(q);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const unsigned j = (L >> 3) + 4u * (unsigned)h;
+                    if (j < n) {
+                        const int t = (int)(j * stride);
+                        if (t != own && !(fpm(q, t) & km)) {
+                            const unsigned rk = rank2((bc & ~ofc) | fpc(q, t), (bm & ~ofm) | fpm(q, t));
+                            const unsigned key = (rk << 27) | (r << 3) | (unsigned)t;
+                            kmin = key < kmin ? key : kmin;
+                            ++cnt;
+                        }
+                    }
+                }
+            }
+            const unsigned best = wp::rmin(kmin);
+            const int evals = (int)wp::radd(cnt);
+            max_intra = max_intra > evals ? max_intra : evals;
+            if (best == NONE || (best >> 27) >= cur) break;  // strict improvement only
+            const int wl = wp::ffs(wp::ballot(kmin == best)) - 1;
+            apply_move(g * 8 + (wl & 7), g, (int)(best & 7u), false);
+        }
+    }
+
+    // plan_inter (migration.cpp:125-210): move jobs from Busy GPUs to the
+    // Lazy GPU g0 while the move leaves g0 less loaded than the source;
+    // source key (cost without the job, gpu, job id), destination key
+    // (cost with the job, start).  Lazy-ness of g0 is not re-checked.
+    MSG_DI void plan_inter(int g0) {
+        for (;;) {
+            wp::sync();
+            const unsigned w0 = sm->gw[g0];
+            const unsigned lazy_cs = (unsigned)wp::popc(w_bc(w0));
+            const unsigned km0 = w_km(w0);
+            const unsigned pl = tb->placeable[km0];
+            unsigned kmin = NONE, cnt = 0;
+            int bsl = -1;
+#pragma unroll
+            for (int i = 0; i < SPL; ++i) {
+                const int slot = L + 32 * i;
+                const int g = slot >> 3, s = slot & 7;
+                if (g < G && g != g0) {
+                    const uint8_t st = sm->st[slot];
+                    if (st == ST_RUN || st == ST_WAIT) {
+                        const unsigned w = sm->gw[g];
+                        const unsigned src_cs = (unsigned)wp::popc(w_bc(w));
+                        const int q = sm->prof[slot];
+                        const unsigned cs = cs_of(q);
+                        if (!((lazymask >> src_cs) & 1u) && lazy_cs + cs < src_cs - cs && ((pl >> q) & 1u)) {
+                            const unsigned rk = rank2(w_bc(w) & ~fpc(q, s), w_bm(w) & ~fpm(q, s));
+                            const unsigned key = (rk << 27) | ((unsigned)g << 22) | (unsigned)sm->job[slot];
+                            if (key < kmin) {
+                                kmin = key;
+                                bsl = slot;
+                            }
+                            ++cnt;
+                        }
+                    }
+                }
+            }
+            const unsigned best = wp::rmin(kmin);
+            int evals = (int)wp::radd(cnt);
+            if (best == NONE) {
+                max_inter = max_inter > evals ? max_inter : evals;
+                break;
+            }
+            const int wl = wp::ffs(wp::ballot(kmin == best)) - 1;
+            const int from_slot = wp::shfl(bsl, wl);
+            const int q = sm->prof[from_slot];
+            // Destination: minimum (cost, start) on g0; lane L < 8 = start L.
+            const bool cand = L < 8 && ((startmask_of(q) >> L) & 1u) && !(fpm(q, (int)L) & km0);
+            const unsigned dk = cand ? ((rank2(w_bc(w0) | fpc(q, (int)L), w_bm(w0) | fpm(q, (int)L)) << 3) | L)
+                                     : NONE;
+            const unsigned dbest = wp::rmin(dk);
+            evals += (int)wp::radd(cand ? 1u : 0u);
+            max_inter = max_inter > evals ? max_inter : evals;
+            apply_move(from_slot, g0, (int)(dbest & 7u), true);
+        }
+    }
+
+    // on_departure (migration.cpp:212-220): Busy -> intra, Lazy -> inter.
+    MSG_DI void on_departure(int g) {
+        wp::sync();
+        const unsigned w = sm->gw[g];
+        if ((lazymask >> wp::popc(w_bc(w))) & 1u) plan_inter(g);
+        else plan_intra(g);
+    }
+
+    // ------------------------------------------------------------ handlers
+    MSG_DI void handle_arrival() {  // sim.cpp:220-267
+        const int32_t r = (int32_t)a_rank;
+        const int p = a_prof;
+        const double sv = a_svc;
+        ++a_idx;
+        load_arrival();
+        advance_all();
+        bool enq = q_head < q_tail;  // never overtake a non-empty queue
+        if (!enq) {
+            const Decision d = dispatch(p);
+            max_arr = max_arr > (int)d.evals ? max_arr : (int)d.evals;
+            if (d.placed) place(d, r, p, sv, EV_ARRIVAL);
+            else enq = true;
+        }
+        if (enq) {
+            emit(EV_ARRIVAL, r, 0, 0, (unsigned)p, 0, 0, 0, 0);
+            if (L == 0) queue[q_tail] = r;
+            ++q_tail;
+            emit(EV_ENQUEUE, r, 0, 0, 0, 0, 0, 0, 0);
+            ++n_enq;
+        }
+        reschedule();
+        sample();
+    }
+
+    MSG_DI void handle_completion(int slot) {  // sim.cpp:269-301
+        advance_all();
+        wp::sync();
+        const int g = slot >> 3;
+        const int32_t r = sm->job[slot];
+        const int m = sm->mig[slot];
+        wp::sync();
+        if (L == 0) {
+            sm->st[slot] = ST_IDLE;  // release_job: the instance stays, idle
+            jobs[r].done = now;
+            jobs[r].gpu = g;
+            jobs[r].mig = m;
+        }
+        refresh_gpu(g);
+        emit(EV_COMPLETION, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
+        sample();  // post-departure level
+        dequeue_pass();
+        if (cflags & CF_MIG) {
+            on_departure(g);
+            dequeue_pass();
+        }
+        reschedule();
+        sample();
+    }
+
+    MSG_DI void handle_migration_end(int slot) {  // sim.cpp:303-315
+        advance_all();
+        wp::sync();
+        const int g = slot >> 3;
+        const int32_t r = sm->job[slot];
+        wp::sync();
+        if (L == 0) sm->st[slot] = ST_IDLE;  // finish_draining
+        refresh_gpu(g);
+        emit(EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
+        dequeue_pass();
+        reschedule();
+        sample();
+    }
+
+    MSG_DI void handle_service_start(int slot) {  // sim.cpp:317-323
+        advance_all();
+        wp::sync();
+        if (L == 0) {
+            sm->st[slot] = ST_RUN;  // start_service: rem already holds service_s
+            sm->last[slot] = now;
+        }
+        refresh_gpu(slot >> 3);
+        reschedule();
+        sample();
+    }
+
+    MSG_DI void run() {  // Engine::execute (sim.cpp:123-141)
+        for (;;) {
+            int slot = -1;
+            const int kind = next_event(slot);
+            if (kind < 0) break;
+            ++n_handler;
+            if (kind == 3) handle_arrival();
+            else if (kind == 0) handle_completion(slot);
+            else if (kind == 1) handle_migration_end(slot);
+            else handle_service_start(slot);
+        }
+    }
+
+    // metrics (sim.cpp:414-502): sums in job-id order, then divide.
+    MSG_DI void finish(DevSummary* out) {
+        wp::sync();
+        DevSummary s;
+        s.status = q_head < q_tail ? STATUS_JOBS_PENDING : STATUS_OK;
+        s.reserved = 0;
+        s.pending_rank = -1;
+        double sw = 0.0, se = 0.0, st = 0.0, first = 0.0, lastc = 0.0;
+        if (s.status == STATUS_OK) {
+            for (uint32_t base = 0; base < N; base += 32) {
+                const uint32_t j = base + L;
+                double w = 0.0, e = 0.0, t = 0.0, a = 0.0, d = 0.0;
+                if (j < N) {
+                    a = arr[j];
+                    const double sc = jobs[j].sched;
+                    d = jobs[j].done;
+                    w = wp::dsub(sc, a);
+                    e = wp::dsub(d, sc);
+                    t = wp::dadd(w, e);
+                }
+                const uint32_t n = N - base < 32 ? N - base : 32;
+                for (uint32_t k = 0; k < n; ++k) {
+                    const double wk = wp::shfl(w, (int)k), ek = wp::shfl(e, (int)k), tk = wp::shfl(t, (int)k);
+                    const double ak = wp::shfl(a, (int)k), dk = wp::shfl(d, (int)k);
+                    sw = wp::dadd(sw, wk);
+                    se = wp::dadd(se, ek);
+                    st = wp::dadd(st, tk);
+                    if (base + k == 0) {
+                        first = ak;
+                        lastc = dk;
+                    } else {
+                        first = ak < first ? ak : first;  // std::min(first, a)
+                        lastc = lastc < dk ? dk : lastc;  // std::max(last, c)
+                    }
+                }
+            }
+        } else {
+            unsigned mn = NONE;
+            for (uint32_t i = q_head + L; i < q_tail; i += 32) {
+                const unsigned r = (unsigned)queue[i];
+                mn = r < mn ? r : mn;
+            }
+            s.pending_rank = (int32_t)wp::rmin(mn);
+        }
+        if (N > 0 && s.status == STATUS_OK) {
+            const double n = (double)N;
+            s.mean_wait = wp::ddiv(sw, n);
+            s.mean_exec = wp::ddiv(se, n);
+            s.mean_turn = wp::ddiv(st, n);
+            s.makespan = wp::dsub(lastc, first);
+        } else {
+            s.mean_wait = s.mean_exec = s.mean_turn = s.makespan = 0.0;
+        }
+        s.handler_events = n_handler;
+        s.n_events = n_ev;
+        s.timeline_samples = n_tl;
+        s.migrations = n_mig;
+        s.reconfig_ops = n_reconf;
+        s.enqueues = n_enq;
+        s.dequeues = n_deq;
+        s.max_arr = max_arr;
+        s.max_intra = max_intra;
+        s.max_inter = max_inter;
+        s.tl_sum = tl_sum;
+        if (L == 0) *out = s;
+    }
+};
+
+// One warp, one trace: the body shared by the CUDA kernel and the CPU-side
+// unit-test emulation.
+template <int SPL>
+MSG_DI void simulate_trace(const SimArgs& a, const DevTables* tables, WarpSmem<SPL>* ws, uint32_t t) {
+    TraceSim<SPL> sim;
+    sim.setup(a, tables, ws, t);
+    sim.run();
+    sim.finish(a.summary + t);
+}
+
+}  // namespace msgk

@@ -1,0 +1,60 @@
+// engine_kernels.cu — sm_100a kernels of the MIG scheduler engine.
+//
+//   sim_kernel<SPL>   one warp per trace: the reference's whole event loop
+//                     (sim.cpp:71-410) with the scheduler (scheduler.cpp)
+//                     and migration planners (migration.cpp) in-kernel; no
+//                     host round trips.  SPL = slots per lane = ceil(8G/32).
+//
+// The host side (host_runtime.cpp) calls the launch_* wrappers below.
+#include <cuda_runtime.h>
+
+#include "engine_core.cuh"
+#include "kernels.h"
+
+namespace msgk {
+
+constexpr int kWarpsPerBlock = 4;
+
+template <int SPL>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) sim_kernel(SimArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    DevTables* tb = reinterpret_cast<DevTables*>(smem);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.tables);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (unsigned i = threadIdx.x; i < sizeof(DevTables) / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const unsigned w = threadIdx.x >> 5;
+    const uint32_t t = blockIdx.x * kWarpsPerBlock + w;
+    if (t >= a.n_traces) return;
+    WarpSmem<SPL>* ws = reinterpret_cast<WarpSmem<SPL>*>(smem + sizeof(DevTables) + w * sizeof(WarpSmem<SPL>));
+    simulate_trace<SPL>(a, tb, ws, t);
+}
+
+template <int SPL>
+static cudaError_t launch_sim_t(const SimArgs& a, cudaStream_t stream) {
+    static_assert(sizeof(DevTables) % 16 == 0, "tables must be 16-byte sized");
+    static_assert(sizeof(WarpSmem<SPL>) % 16 == 0, "warp state must be 16-byte sized");
+    const size_t smem = sizeof(DevTables) + kWarpsPerBlock * sizeof(WarpSmem<SPL>);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(sim_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const unsigned blocks = (a.n_traces + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blocks == 0) return cudaSuccess;
+    sim_kernel<SPL><<<blocks, 32 * kWarpsPerBlock, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream) {
+    switch (spl) {
+        case 1: return launch_sim_t<1>(a, stream);
+        case 2: return launch_sim_t<2>(a, stream);
+        case 4: return launch_sim_t<4>(a, stream);
+        case 8: return launch_sim_t<8>(a, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace msgk

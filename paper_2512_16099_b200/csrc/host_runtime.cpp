@@ -1,0 +1,634 @@
+// host_runtime.cpp — the C ABI of include/migsched_b200.h.
+//
+// Host responsibilities only: validation with the reference's error order
+// (Engine::Engine, sim.cpp:73-116), staging traces into HBM in job-id (rank)
+// order, launching the sm_100a kernels, and decoding the kernels' compact
+// records into the ABI structs.  Every scheduling decision, planner step and
+// event-loop step runs on the GPU (engine_core.cuh); there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "dev_types.h"
+#include "host_tables.h"
+#include "staging.h"
+#include "kernels.h"
+#include "migsched_b200.h"
+
+using namespace msgk;
+
+namespace {
+
+template <class F>
+void parallel_for(uint32_t n, uint32_t min_per_thread, F&& f) {
+    uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
+    uint32_t threads = std::min(hw, std::max(1u, n / std::max(1u, min_per_thread)));
+    if (threads <= 1) {
+        for (uint32_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::atomic<uint32_t> next{0};
+    auto worker = [&]() {
+        for (;;) {
+            const uint32_t base = next.fetch_add(16);
+            if (base >= n) return;
+            const uint32_t end = std::min(n, base + 16);
+            for (uint32_t i = base; i < end; ++i) f(i);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (uint32_t t = 1; t < threads; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+struct msg_engine {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    DevBuf tables;
+    DevBuf flush;
+    uint64_t launches = 0;
+    std::string last_error;
+    int sm_count = 0;
+    char name[256] = {0};
+    msg_staged* cached = nullptr;
+};
+
+struct msg_staged {
+    msg_engine* eng = nullptr;
+    uint32_t n_in = 0;
+    uint32_t out_flags = 0;
+    int spl = 1;
+    std::vector<int32_t> status;      // per input trace (validation)
+    std::vector<std::string> message;
+    std::vector<int32_t> dev_index;   // input trace -> device trace or -1
+    std::vector<uint32_t> src_of;     // device trace -> input trace
+    std::vector<int32_t> gpu_count;   // per input trace
+    std::vector<double> overlap;      // per device trace
+    std::vector<DevTrace> traces;
+    std::vector<DevConfig> configs;
+    std::vector<uint32_t> init;
+    uint64_t n_jobs = 0, ev_total = 0, tl_total = 0;
+    bool any_perm = false;
+    uint32_t ev_per_job = 16, tl_per_job = 8;
+    uint64_t handler_events = 0;
+    // pinned host mirrors (rank order)
+    HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
+    HostBuf h_jobs, h_events, h_timeline, h_summary;
+    // device
+    DevBuf d_arrival, d_service, d_profile, d_perm, d_traces, d_configs, d_init, d_tables_unused;
+    DevBuf d_queue, d_jobs, d_events, d_timeline, d_summary;
+};
+
+struct msg_batch_result {
+    std::vector<msg_trace_summary> summaries;
+    std::vector<std::string> messages;
+    std::vector<std::vector<msg_job_row>> jobs;
+    std::vector<std::vector<msg_event>> events;
+    std::vector<std::vector<msg_timeline_point>> timeline;
+};
+
+namespace {
+
+msg_status cuda_fail(msg_engine* e, cudaError_t err, const char* what) {
+    if (e) e->last_error = std::string("CudaError: ") + what + ": " + cudaGetErrorString(err);
+    return MSG_ERR_CUDA;
+}
+
+#define CK(expr)                                                   \
+    do {                                                           \
+        cudaError_t _e = (expr);                                   \
+        if (_e != cudaSuccess) return cuda_fail(eng, _e, #expr);   \
+    } while (0)
+
+msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
+                      uint32_t flags, msg_staged* s) {
+    if (!b || (b->n_traces && (!b->offsets || !b->job_id || !b->arrival_s || !b->profile || !b->service_s)) ||
+        (n_cfgs == 0 && b->n_traces)) {
+        eng->last_error = "InvalidArgument: null batch arrays or no configs";
+        return MSG_ERR_INVALID_ARGUMENT;
+    }
+    s->eng = eng;
+    s->n_in = b->n_traces;
+    s->out_flags = flags;
+    s->status.assign(s->n_in, MSG_OK);
+    s->message.assign(s->n_in, std::string());
+    s->dev_index.assign(s->n_in, -1);
+    s->gpu_count.assign(s->n_in, 0);
+    s->src_of.clear();
+    s->traces.clear();
+    s->configs.clear();
+    s->init.clear();
+    s->overlap.clear();
+    s->handler_events = 0;
+
+    // Configs referenced by the batch.
+    std::vector<CfgState> cs(n_cfgs);
+    for (uint32_t i = 0; i < n_cfgs; ++i) cs[i] = validate_config(cfgs[i]);
+    for (uint32_t i = 0; i < n_cfgs; ++i) {
+        cs[i].dev.init_off = (uint32_t)s->init.size();
+        s->init.insert(s->init.end(), cs[i].init.begin(), cs[i].init.end());
+        s->configs.push_back(cs[i].dev);
+    }
+
+    // Per-trace validation (parallel), in input order.
+    std::vector<TraceCheck> checks(s->n_in);
+    for (uint32_t t = 0; t < s->n_in; ++t) {
+        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
+        if (ci >= n_cfgs) {
+            eng->last_error = "InvalidArgument: config_index out of range";
+            return MSG_ERR_INVALID_ARGUMENT;
+        }
+    }
+    parallel_for(s->n_in, 64, [&](uint32_t t) {
+        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
+        if (cs[ci].status != MSG_OK) {
+            checks[t].status = cs[ci].status;
+            checks[t].message = cs[ci].message;
+            return;
+        }
+        checks[t] = check_trace(b, t);
+    });
+
+    uint64_t njobs = 0;
+    int maxG = 1;
+    for (uint32_t t = 0; t < s->n_in; ++t) {
+        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
+        s->gpu_count[t] = cfgs[ci].gpu_count;
+        s->status[t] = checks[t].status;
+        s->message[t] = checks[t].message;
+        if (checks[t].status != MSG_OK) continue;
+        DevTrace tr{};
+        tr.job_off = njobs;
+        tr.n_jobs = (uint32_t)(b->offsets[t + 1] - b->offsets[t]);
+        tr.cfg = ci;
+        tr.has_perm = checks[t].identity ? 0 : 1;
+        s->dev_index[t] = (int32_t)s->traces.size();
+        s->src_of.push_back(t);
+        s->traces.push_back(tr);
+        s->overlap.push_back(cfgs[ci].migration_overlap_s);
+        njobs += tr.n_jobs;
+        maxG = std::max(maxG, cfgs[ci].gpu_count);
+    }
+    s->n_jobs = njobs;
+    s->spl = maxG <= 4 ? 1 : maxG <= 8 ? 2 : maxG <= 16 ? 4 : 8;
+    // Output capacities.
+    uint64_t ev = 0, tl = 0;
+    for (auto& tr : s->traces) {
+        tr.ev_off = ev;
+        tr.tl_off = tl;
+        tr.ev_cap = (flags & MSG_OUT_EVENTS) ? s->ev_per_job * tr.n_jobs + 256 : 0;
+        tr.tl_cap = (flags & MSG_OUT_TIMELINE) ? s->tl_per_job * tr.n_jobs + 64 : 0;
+        ev += tr.ev_cap;
+        tl += tr.tl_cap;
+    }
+    s->ev_total = ev;
+    s->tl_total = tl;
+
+    // Host staging into pinned buffers, rank (job-id) order.
+    const size_t N = std::max<uint64_t>(njobs, 1);
+    CK(s->h_arrival.ensure(N * sizeof(double)));
+    CK(s->h_service.ensure(N * sizeof(double)));
+    CK(s->h_profile.ensure(N));
+    CK(s->h_ids.ensure(N * sizeof(int64_t)));
+    bool any_perm = false;
+    for (auto& tr : s->traces) any_perm |= tr.has_perm != 0;
+    s->any_perm = any_perm;
+    if (any_perm) CK(s->h_perm.ensure(N * sizeof(uint32_t)));
+    double* ha = s->h_arrival.as<double>();
+    double* hs = s->h_service.as<double>();
+    uint8_t* hp = s->h_profile.as<uint8_t>();
+    int64_t* hid = s->h_ids.as<int64_t>();
+    uint32_t* hperm = any_perm ? s->h_perm.as<uint32_t>() : nullptr;
+    parallel_for((uint32_t)s->traces.size(), 32, [&](uint32_t d) {
+        stage_trace_arrays(b, s->src_of[d], s->traces[d], ha, hs, hp, hid, hperm);
+    });
+
+    // Device buffers + H2D.
+    cudaStream_t st = eng->stream;
+    CK(s->d_arrival.ensure(N * sizeof(double)));
+    CK(s->d_service.ensure(N * sizeof(double)));
+    CK(s->d_profile.ensure(N));
+    CK(s->d_queue.ensure(N * sizeof(int32_t)));
+    CK(s->d_jobs.ensure(N * sizeof(JobOut)));
+    CK(s->d_traces.ensure(std::max<size_t>(s->traces.size(), 1) * sizeof(DevTrace)));
+    CK(s->d_configs.ensure(std::max<size_t>(s->configs.size(), 1) * sizeof(DevConfig)));
+    CK(s->d_init.ensure(std::max<size_t>(s->init.size(), 1) * sizeof(uint32_t)));
+    CK(s->d_summary.ensure(std::max<size_t>(s->traces.size(), 1) * sizeof(DevSummary)));
+    if (any_perm) CK(s->d_perm.ensure(N * sizeof(uint32_t)));
+    if (s->ev_total) CK(s->d_events.ensure(s->ev_total * sizeof(EventRec)));
+    if (s->tl_total) CK(s->d_timeline.ensure(s->tl_total * 2 * sizeof(double)));
+    if (njobs) {
+        CK(cudaMemcpyAsync(s->d_arrival.p, ha, njobs * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(s->d_service.p, hs, njobs * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(s->d_profile.p, hp, njobs, cudaMemcpyHostToDevice, st));
+        if (any_perm) CK(cudaMemcpyAsync(s->d_perm.p, hperm, njobs * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    }
+    if (!s->traces.empty())
+        CK(cudaMemcpyAsync(s->d_traces.p, s->traces.data(), s->traces.size() * sizeof(DevTrace),
+                           cudaMemcpyHostToDevice, st));
+    if (!s->configs.empty())
+        CK(cudaMemcpyAsync(s->d_configs.p, s->configs.data(), s->configs.size() * sizeof(DevConfig),
+                           cudaMemcpyHostToDevice, st));
+    if (!s->init.empty())
+        CK(cudaMemcpyAsync(s->d_init.p, s->init.data(), s->init.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           st));
+    // The pageable vectors above must stay valid until the copies finish.
+    CK(cudaStreamSynchronize(st));
+    return MSG_OK;
+}
+
+SimArgs make_args(msg_engine* eng, msg_staged* s) {
+    SimArgs a{};
+    a.traces = s->d_traces.as<DevTrace>();
+    a.configs = s->d_configs.as<DevConfig>();
+    a.init_slots = s->d_init.as<uint32_t>();
+    a.tables = eng->tables.as<DevTables>();
+    a.arrival = s->d_arrival.as<double>();
+    a.service = s->d_service.as<double>();
+    a.profile = s->d_profile.as<uint8_t>();
+    a.perm = s->any_perm ? s->d_perm.as<uint32_t>() : nullptr;
+    a.queue = s->d_queue.as<int32_t>();
+    a.jobs = s->d_jobs.as<JobOut>();
+    a.events = s->ev_total ? s->d_events.as<EventRec>() : nullptr;
+    a.timeline = s->tl_total ? s->d_timeline.as<double>() : nullptr;
+    a.summary = s->d_summary.as<DevSummary>();
+    a.n_traces = (uint32_t)s->traces.size();
+    a.out_flags = s->out_flags;
+    return a;
+}
+
+msg_status launch_impl(msg_engine* eng, msg_staged* s) {
+    if (s->traces.empty()) return MSG_OK;
+    const SimArgs a = make_args(eng, s);
+    cudaError_t e = launch_sim(s->spl, a, eng->stream);
+    if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim");
+    ++eng->launches;
+    return MSG_OK;
+}
+
+msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) {
+    cudaStream_t st = eng->stream;
+    const size_t T = s->traces.size();
+    for (int attempt = 0;; ++attempt) {
+        CK(s->h_summary.ensure(std::max<size_t>(T, 1) * sizeof(DevSummary)));
+        if (T) CK(cudaMemcpyAsync(s->h_summary.p, s->d_summary.p, T * sizeof(DevSummary), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        // Output-capacity overflow: grow and re-run (deterministic, same result).
+        const DevSummary* ds = s->h_summary.as<DevSummary>();
+        bool overflow = false;
+        for (size_t d = 0; d < T; ++d)
+            overflow |= (s->traces[d].ev_cap && ds[d].n_events > s->traces[d].ev_cap) ||
+                        (s->traces[d].tl_cap && ds[d].timeline_samples > s->traces[d].tl_cap);
+        if (!overflow) break;
+        if (attempt > 6) {
+            eng->last_error = "Unsupported: event log exceeds the output capacity";
+            return MSG_ERR_UNSUPPORTED;
+        }
+        s->ev_per_job *= 4;
+        s->tl_per_job *= 4;
+        uint64_t ev = 0, tl = 0;
+        for (auto& tr : s->traces) {
+            tr.ev_off = ev;
+            tr.tl_off = tl;
+            tr.ev_cap = (s->out_flags & MSG_OUT_EVENTS) ? s->ev_per_job * tr.n_jobs + 256 : 0;
+            tr.tl_cap = (s->out_flags & MSG_OUT_TIMELINE) ? s->tl_per_job * tr.n_jobs + 64 : 0;
+            ev += tr.ev_cap;
+            tl += tr.tl_cap;
+        }
+        s->ev_total = ev;
+        s->tl_total = tl;
+        if (ev) CK(s->d_events.ensure(ev * sizeof(EventRec)));
+        if (tl) CK(s->d_timeline.ensure(tl * 2 * sizeof(double)));
+        CK(cudaMemcpy(s->d_traces.p, s->traces.data(), T * sizeof(DevTrace), cudaMemcpyHostToDevice));
+        msg_status ls = launch_impl(eng, s);
+        if (ls != MSG_OK) return ls;
+    }
+    const bool want_jobs = (s->out_flags & MSG_OUT_JOBS) != 0;
+    const bool want_ev = (s->out_flags & MSG_OUT_EVENTS) != 0;
+    const bool want_tl = (s->out_flags & MSG_OUT_TIMELINE) != 0;
+    if (want_jobs && s->n_jobs) {
+        CK(s->h_jobs.ensure(s->n_jobs * sizeof(JobOut)));
+        CK(cudaMemcpyAsync(s->h_jobs.p, s->d_jobs.p, s->n_jobs * sizeof(JobOut), cudaMemcpyDeviceToHost, st));
+    }
+    if (want_ev && s->ev_total) {
+        CK(s->h_events.ensure(s->ev_total * sizeof(EventRec)));
+        CK(cudaMemcpyAsync(s->h_events.p, s->d_events.p, s->ev_total * sizeof(EventRec), cudaMemcpyDeviceToHost, st));
+    }
+    if (want_tl && s->tl_total) {
+        CK(s->h_timeline.ensure(s->tl_total * 2 * sizeof(double)));
+        CK(cudaMemcpyAsync(s->h_timeline.p, s->d_timeline.p, s->tl_total * 2 * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+
+    auto res = std::make_unique<msg_batch_result>();
+    res->summaries.resize(s->n_in);
+    res->messages = s->message;
+    if (want_jobs) res->jobs.resize(s->n_in);
+    if (want_ev) res->events.resize(s->n_in);
+    if (want_tl) res->timeline.resize(s->n_in);
+    const DevSummary* ds = s->h_summary.as<DevSummary>();
+    const JobOut* hj = s->h_jobs.as<JobOut>();
+    const EventRec* he = s->h_events.as<EventRec>();
+    const double* ht = s->h_timeline.as<double>();
+    const double* ha = s->h_arrival.as<double>();
+    const uint8_t* hp = s->h_profile.as<uint8_t>();
+    const int64_t* hid = s->h_ids.as<int64_t>();
+    std::atomic<uint64_t> handler{0};
+    parallel_for(s->n_in, 64, [&](uint32_t t) {
+        msg_trace_summary& o = res->summaries[t];
+        std::memset(&o, 0, sizeof(o));
+        o.status = s->status[t];
+        o.gpu_count = s->gpu_count[t];
+        const int32_t d = s->dev_index[t];
+        if (d < 0) return;
+        const DevTrace& tr = s->traces[d];
+        const DevSummary& x = ds[d];
+        o.status = x.status;
+        o.n_jobs = tr.n_jobs;
+        o.handler_events = x.handler_events;
+        o.n_events = x.n_events;
+        o.timeline_samples = x.timeline_samples;
+        o.migration_count = x.migrations;
+        o.reconfig_op_count = x.reconfig_ops;
+        o.enqueue_count = x.enqueues;
+        o.dequeue_count = x.dequeues;
+        o.max_arrival_frag_evals = x.max_arr;
+        o.max_intra_iter_frag_evals = x.max_intra;
+        o.max_inter_iter_frag_evals = x.max_inter;
+        o.mean_wait_s = x.mean_wait;
+        o.mean_execution_s = x.mean_exec;
+        o.mean_turnaround_s = x.mean_turn;
+        o.workload_makespan_s = x.makespan;
+        o.timeline_sum = x.tl_sum;
+        handler += x.handler_events;
+        const int64_t* ids = hid + tr.job_off;
+        if (x.status == MSG_ERR_JOBS_PENDING) {
+            const int64_t jid = x.pending_rank >= 0 ? ids[x.pending_rank] : -1;
+            res->messages[t] = "JobsPending: job " + std::to_string(jid) + " did not complete";
+            return;  // the reference throws: no report, no log
+        }
+        if (want_jobs) {
+            auto& rows = res->jobs[t];
+            rows.resize(tr.n_jobs);
+            for (uint32_t r = 0; r < tr.n_jobs; ++r) {
+                const JobOut& j = hj[tr.job_off + r];
+                msg_job_row& row = rows[r];
+                std::memset(&row, 0, sizeof(row));
+                row.id = ids[r];
+                row.arrival_s = ha[tr.job_off + r];
+                row.scheduled_s = j.sched;
+                row.completed_s = j.done;
+                row.wait_s = row.scheduled_s - row.arrival_s;          // sim.cpp:473-475
+                row.execution_s = row.completed_s - row.scheduled_s;
+                row.turnaround_s = row.wait_s + row.execution_s;
+                row.profile = hp[tr.job_off + r];
+                row.gpu = j.gpu;
+                row.migrations = j.mig;
+            }
+        }
+        if (want_ev) {
+            auto& evs = res->events[t];
+            const uint64_t n = std::min<uint64_t>(x.n_events, tr.ev_cap);
+            evs.resize(n);
+            for (uint64_t i = 0; i < n; ++i) decode_event(he[tr.ev_off + i], ids, s->overlap[d], &evs[i]);
+        }
+        if (want_tl) {
+            auto& tlv = res->timeline[t];
+            const uint64_t n = std::min<uint64_t>(x.timeline_samples, tr.tl_cap);
+            tlv.resize(n);
+            for (uint64_t i = 0; i < n; ++i)
+                tlv[i] = msg_timeline_point{ht[2 * (tr.tl_off + i)], ht[2 * (tr.tl_off + i) + 1]};
+        }
+    });
+    s->handler_events = handler.load();
+    *out = res.release();
+    return MSG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* msg_status_name(int status) {
+    if (status >= 0 && status <= 13) return kStatusNames[status];
+    if (status == MSG_ERR_CUDA) return "CudaError";
+    if (status == MSG_ERR_UNSUPPORTED) return "Unsupported";
+    if (status == MSG_ERR_INVALID_ARGUMENT) return "InvalidArgument";
+    return "Unknown";
+}
+
+msg_status msg_engine_create(int device, msg_engine** out) {
+    if (!out) return MSG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto e = std::make_unique<msg_engine>();
+    msg_engine* eng = e.get();
+    e->device = device;
+    int n = 0;
+    cudaError_t err = cudaGetDeviceCount(&n);
+    if (err != cudaSuccess || device < 0 || device >= n) {
+        return MSG_ERR_CUDA;  // no usable device: there is no CPU fallback
+    }
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    e->sm_count = prop.multiProcessorCount;
+    std::snprintf(e->name, sizeof(e->name), "%s", prop.name);
+    if (prop.major < 10) {
+        return MSG_ERR_CUDA;  // kernels are built for sm_100a only
+    }
+    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e->ev0));
+    CK(cudaEventCreate(&e->ev1));
+    DevTables t;
+    if (build_tables(&t) != 31) return MSG_ERR_INVALID_ARGUMENT;
+    CK(e->tables.ensure(sizeof(DevTables)));
+    CK(cudaMemcpy(e->tables.p, &t, sizeof(DevTables), cudaMemcpyHostToDevice));
+    *out = e.release();
+    return MSG_OK;
+}
+
+void msg_engine_destroy(msg_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    if (e->cached) msg_staged_free(e->cached);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    if (e->ev0) cudaEventDestroy(e->ev0);
+    if (e->ev1) cudaEventDestroy(e->ev1);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+}
+
+const char* msg_engine_last_error(const msg_engine* e) { return e ? e->last_error.c_str() : "no engine"; }
+
+uint64_t msg_engine_launch_count(const msg_engine* e) { return e ? e->launches : 0; }
+
+msg_status msg_engine_device_info(const msg_engine* e, char* name, size_t name_len, int32_t* sm_count) {
+    if (!e) return MSG_ERR_INVALID_ARGUMENT;
+    if (name && name_len) std::snprintf(name, name_len, "%s", e->name);
+    if (sm_count) *sm_count = e->sm_count;
+    return MSG_OK;
+}
+
+msg_status msg_stage(msg_engine* eng, const msg_trace_batch* batch, const msg_config* cfgs, uint32_t n_cfgs,
+                     uint32_t out_flags, msg_staged** out) {
+    if (!eng || !out) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(eng->device);
+    auto s = std::make_unique<msg_staged>();
+    msg_status st = stage_impl(eng, batch, cfgs, n_cfgs, out_flags, s.get());
+    if (st != MSG_OK) return st;
+    *out = s.release();
+    return MSG_OK;
+}
+
+msg_status msg_launch(msg_engine* eng, msg_staged* s) {
+    if (!eng || !s) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(eng->device);
+    return launch_impl(eng, s);
+}
+
+msg_status msg_collect(msg_engine* eng, msg_staged* s, msg_batch_result** out) {
+    if (!eng || !s || !out) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(eng->device);
+    return collect_impl(eng, s, out);
+}
+
+void msg_staged_free(msg_staged* s) { delete s; }
+
+uint64_t msg_staged_handler_events(const msg_staged* s) { return s ? s->handler_events : 0; }
+
+msg_status msg_run_batch(msg_engine* eng, const msg_trace_batch* batch, const msg_config* cfgs, uint32_t n_cfgs,
+                         uint32_t out_flags, msg_batch_result** out) {
+    if (!eng || !out) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(eng->device);
+    if (!eng->cached) eng->cached = new msg_staged();  // grow-only workspace reused across calls
+    msg_staged* s = eng->cached;
+    s->ev_per_job = 16;
+    s->tl_per_job = 8;
+    msg_status st = stage_impl(eng, batch, cfgs, n_cfgs, out_flags, s);
+    if (st != MSG_OK) return st;
+    st = launch_impl(eng, s);
+    if (st != MSG_OK) return st;
+    return collect_impl(eng, s, out);
+}
+
+msg_status msg_engine_sync(msg_engine* eng) {
+    if (!eng) return MSG_ERR_INVALID_ARGUMENT;
+    CK(cudaStreamSynchronize(eng->stream));
+    return MSG_OK;
+}
+
+msg_status msg_time_launch(msg_engine* eng, msg_staged* s, float* ms) {
+    if (!eng || !s || !ms) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(eng->device);
+    CK(cudaEventRecord(eng->ev0, eng->stream));
+    msg_status st = launch_impl(eng, s);
+    if (st != MSG_OK) return st;
+    CK(cudaEventRecord(eng->ev1, eng->stream));
+    CK(cudaEventSynchronize(eng->ev1));
+    CK(cudaEventElapsedTime(ms, eng->ev0, eng->ev1));
+    return MSG_OK;
+}
+
+msg_status msg_engine_flush_l2(msg_engine* eng) {
+    if (!eng) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(eng->device);
+    const size_t bytes = 256ull << 20;
+    CK(eng->flush.ensure(bytes));
+    CK(cudaMemsetAsync(eng->flush.p, eng->launches & 0xFF, bytes, eng->stream));
+    CK(cudaStreamSynchronize(eng->stream));
+    return MSG_OK;
+}
+
+uint32_t msg_result_n_traces(const msg_batch_result* r) { return r ? (uint32_t)r->summaries.size() : 0; }
+
+const msg_trace_summary* msg_result_summary(const msg_batch_result* r, uint32_t t) {
+    return (r && t < r->summaries.size()) ? &r->summaries[t] : nullptr;
+}
+
+const msg_job_row* msg_result_jobs(const msg_batch_result* r, uint32_t t, uint64_t* n) {
+    if (n) *n = 0;
+    if (!r || t >= r->jobs.size()) return nullptr;
+    if (n) *n = r->jobs[t].size();
+    return r->jobs[t].data();
+}
+
+const msg_event* msg_result_events(const msg_batch_result* r, uint32_t t, uint64_t* n) {
+    if (n) *n = 0;
+    if (!r || t >= r->events.size()) return nullptr;
+    if (n) *n = r->events[t].size();
+    return r->events[t].data();
+}
+
+const msg_timeline_point* msg_result_timeline(const msg_batch_result* r, uint32_t t, uint64_t* n) {
+    if (n) *n = 0;
+    if (!r || t >= r->timeline.size()) return nullptr;
+    if (n) *n = r->timeline[t].size();
+    return r->timeline[t].data();
+}
+
+const char* msg_result_message(const msg_batch_result* r, uint32_t t) {
+    return (r && t < r->messages.size()) ? r->messages[t].c_str() : "";
+}
+
+void msg_result_free(msg_batch_result* r) { delete r; }
+
+}  // extern "C"

@@ -1,0 +1,13 @@
+// Host-visible launch wrappers of engine_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dev_types.h"
+
+namespace msgk {
+
+
+// Launch the per-trace event-loop kernel; spl in {1, 2, 4, 8}.
+cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream);
+
+}  // namespace msgk

@@ -1,0 +1,249 @@
+"""ctypes binding of libmigsched_b200.so (include/migsched_b200.h).
+
+The product path: every call here executes the sm_100a kernels.  If the
+shared library or a CUDA device is missing, the calls raise — there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .model import ConfigPack, MigschedError, SimConfig, TraceBatch, WorkloadSpec
+from .results import TraceResult
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmigsched_b200.so")
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA engine library (fails loudly if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"CUDA engine library missing: {LIB_PATH}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    L = C.CDLL(LIB_PATH)
+    vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
+    sig = {
+        "msg_status_name": (C.c_char_p, [C.c_int]),
+        "msg_engine_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "msg_engine_destroy": (None, [vp]),
+        "msg_engine_last_error": (C.c_char_p, [vp]),
+        "msg_engine_launch_count": (u64, [vp]),
+        "msg_engine_device_info": (C.c_int, [vp, C.c_char_p, C.c_size_t, C.POINTER(i32)]),
+        "msg_run_batch": (C.c_int, [vp, vp, vp, u32, u32, C.POINTER(vp)]),
+        "msg_stage": (C.c_int, [vp, vp, vp, u32, u32, C.POINTER(vp)]),
+        "msg_launch": (C.c_int, [vp, vp]),
+        "msg_collect": (C.c_int, [vp, vp, C.POINTER(vp)]),
+        "msg_staged_free": (None, [vp]),
+        "msg_staged_handler_events": (u64, [vp]),
+        "msg_engine_sync": (C.c_int, [vp]),
+        "msg_time_launch": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
+        "msg_engine_flush_l2": (C.c_int, [vp]),
+        "msg_result_n_traces": (u32, [vp]),
+        "msg_result_summary": (vp, [vp, u32]),
+        "msg_result_jobs": (vp, [vp, u32, C.POINTER(u64)]),
+        "msg_result_events": (vp, [vp, u32, C.POINTER(u64)]),
+        "msg_result_timeline": (vp, [vp, u32, C.POINTER(u64)]),
+        "msg_result_message": (C.c_char_p, [vp, u32]),
+        "msg_result_free": (None, [vp]),
+        "msg_workload_preset": (C.c_int, [C.c_char_p, vp]),
+        "msg_generate": (C.c_int, [vp, vp, vp, vp, vp]),
+        "msg_generate_many": (C.c_int, [vp, u64, u32, i32, vp, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(st: int, eng=None):
+    if st != 0:
+        msg = ""
+        if eng is not None and eng._h:
+            msg = lib().msg_engine_last_error(eng._h).decode()
+        raise MigschedError(abi.STATUS_NAMES.get(st, str(st)), msg)
+
+
+class Staged:
+    """A batch resident in HBM (msg_stage); launch/collect any number of times."""
+
+    def __init__(self, engine: "Engine", handle, n_traces: int, keep):
+        self.engine = engine
+        self._h = handle
+        self.n_traces = n_traces
+        self._keep = keep
+
+    def launch(self):
+        _check(lib().msg_launch(self.engine._h, self._h), self.engine)
+
+    def time_launch(self) -> float:
+        ms = C.c_float()
+        _check(lib().msg_time_launch(self.engine._h, self._h, C.byref(ms)), self.engine)
+        return ms.value
+
+    def collect(self) -> list:
+        r = C.c_void_p()
+        _check(lib().msg_collect(self.engine._h, self._h, C.byref(r)), self.engine)
+        try:
+            return _decode(r)
+        finally:
+            lib().msg_result_free(r)
+
+    @property
+    def handler_events(self) -> int:
+        return int(lib().msg_staged_handler_events(self._h))
+
+    def free(self):
+        if self._h:
+            lib().msg_staged_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Engine:
+    """One CUDA device + stream (msg_engine)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        st = lib().msg_engine_create(device, C.byref(h))
+        if st != 0:
+            raise MigschedError(abi.STATUS_NAMES.get(st, str(st)),
+                                f"cannot create the CUDA engine on device {device}")
+        self._h = h
+
+    def close(self):
+        if self._h:
+            lib().msg_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().msg_engine_launch_count(self._h))
+
+    def device_info(self):
+        buf = C.create_string_buffer(256)
+        sm = C.c_int32()
+        lib().msg_engine_device_info(self._h, buf, 256, C.byref(sm))
+        return buf.value.decode(), sm.value
+
+    def sync(self):
+        _check(lib().msg_engine_sync(self._h), self)
+
+    def flush_l2(self):
+        _check(lib().msg_engine_flush_l2(self._h), self)
+
+    def run_batch(self, batch: TraceBatch, cfgs: Sequence[SimConfig], out_flags: int = abi.OUT_JOBS) -> list:
+        """migsched::run over every trace of the batch (sim.cpp:504-507)."""
+        pack = ConfigPack(cfgs)
+        r = C.c_void_p()
+        _check(lib().msg_run_batch(self._h, C.addressof(batch._c), C.addressof(pack.c[0]), len(pack),
+                                   out_flags, C.byref(r)), self)
+        try:
+            return _decode(r)
+        finally:
+            lib().msg_result_free(r)
+
+    def stage(self, batch: TraceBatch, cfgs: Sequence[SimConfig], out_flags: int = 0) -> Staged:
+        pack = ConfigPack(cfgs)
+        h = C.c_void_p()
+        _check(lib().msg_stage(self._h, C.addressof(batch._c), C.addressof(pack.c[0]), len(pack), out_flags,
+                               C.byref(h)), self)
+        return Staged(self, h, batch.n_traces, (batch, pack))
+
+
+def _decode(r) -> list:
+    L = lib()
+    out = []
+    n = L.msg_result_n_traces(r)
+    cnt = C.c_uint64()
+    for t in range(n):
+        sp = L.msg_result_summary(r, t)
+        summary = np.frombuffer(C.string_at(sp, abi.SUMMARY_DTYPE.itemsize), abi.SUMMARY_DTYPE)[0].copy()
+        msg = L.msg_result_message(r, t).decode()
+
+        def arr(fn, dtype):
+            p = fn(r, t, C.byref(cnt))
+            if not p or cnt.value == 0:
+                return None if not p else np.zeros(0, dtype)
+            return np.frombuffer(C.string_at(p, cnt.value * dtype.itemsize), dtype).copy()
+
+        out.append(
+            TraceResult(
+                int(summary["status"]),
+                msg,
+                summary,
+                arr(L.msg_result_jobs, abi.JOB_DTYPE),
+                arr(L.msg_result_events, abi.EVENT_DTYPE),
+                arr(L.msg_result_timeline, abi.TIMELINE_DTYPE),
+            )
+        )
+    return out
+
+
+_default_engine: Optional[Engine] = None
+
+
+def default_engine() -> Engine:
+    global _default_engine
+    if _default_engine is None:
+        _default_engine = Engine(0)
+    return _default_engine
+
+
+def run(trace, cfg: SimConfig, out_flags: int = abi.OUT_JOBS | abi.OUT_EVENTS | abi.OUT_TIMELINE) -> TraceResult:
+    """Drop-in for migsched::run(trace, cfg) (sim.hpp:114): raises
+    MigschedError with the reference's error code on failure."""
+    batch = TraceBatch.from_traces([list(trace)])
+    res = default_engine().run_batch(batch, [cfg], out_flags)[0]
+    return res.raise_for_status()
+
+
+def generate(spec: WorkloadSpec):
+    """migsched::generate (workload.cpp:98-127) -> list of Job."""
+    from .model import Job
+
+    n = spec.job_count
+    ids = np.zeros(max(n, 1), np.int64)
+    arr = np.zeros(max(n, 1), np.float64)
+    prof = np.zeros(max(n, 1), np.int32)
+    svc = np.zeros(max(n, 1), np.float64)
+    s = spec.to_abi()
+    _check(lib().msg_generate(C.byref(s), ids.ctypes.data, arr.ctypes.data, prof.ctypes.data, svc.ctypes.data))
+    return [Job(int(ids[i]), float(arr[i]), int(prof[i]), float(svc[i])) for i in range(n)]
+
+
+def generate_batch(spec: WorkloadSpec, seed0: int, n_seeds: int, threads: int = 0) -> TraceBatch:
+    """n_seeds traces with seeds seed0.. as one TraceBatch (host threads)."""
+    n = spec.job_count * n_seeds
+    offsets = np.zeros(n_seeds + 1, np.uint64)
+    ids = np.zeros(max(n, 1), np.int64)
+    arr = np.zeros(max(n, 1), np.float64)
+    prof = np.zeros(max(n, 1), np.int32)
+    svc = np.zeros(max(n, 1), np.float64)
+    s = spec.to_abi()
+    _check(lib().msg_generate_many(C.byref(s), seed0, n_seeds, threads, offsets.ctypes.data, ids.ctypes.data,
+                                   arr.ctypes.data, prof.ctypes.data, svc.ctypes.data))
+    return TraceBatch(offsets, ids[:n], arr[:n], prof[:n], svc[:n])

@@ -1,0 +1,169 @@
+// TEST INFRASTRUCTURE ONLY — runs the unchanged device code
+// (paper_2512_16099_b200/csrc/engine_core.cuh) on 32 host threads per trace,
+// with the product's own staging/decoding (staging.h), and returns results
+// in the ABI record formats so tests can diff them against the reference.
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "engine_core.cuh"
+#include "staging.h"
+
+using namespace msgk;
+
+namespace {
+
+struct EmuResult {
+    int status = 0;
+    std::string message;
+    msg_trace_summary summary{};
+    std::vector<msg_event> events;
+    std::vector<msg_job_row> jobs;
+    std::vector<msg_timeline_point> timeline;
+};
+
+template <int SPL>
+void run_warp(const SimArgs& a, const DevTables* tb) {
+    auto ws = std::make_unique<WarpSmem<SPL>>();
+    std::memset(ws.get(), 0xA5, sizeof(WarpSmem<SPL>));  // garbage, like real smem
+    wp::EmuWarp warp;
+    std::vector<std::thread> lanes;
+    for (unsigned l = 0; l < 32; ++l) {
+        lanes.emplace_back([&, l]() {
+            wp::g_warp = &warp;
+            wp::g_lane = l;
+            wp::g_phase = 0;
+            simulate_trace<SPL>(a, tb, ws.get(), 0);
+        });
+    }
+    for (auto& t : lanes) t.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
+    auto* r = new EmuResult();
+    CfgState cs = validate_config(*c);
+    r->summary.gpu_count = c->gpu_count;
+    if (cs.status != MSG_OK) {
+        r->status = r->summary.status = cs.status;
+        r->message = cs.message;
+        return r;
+    }
+    TraceCheck tc = check_trace(b, t);
+    if (tc.status != MSG_OK) {
+        r->status = r->summary.status = tc.status;
+        r->message = tc.message;
+        return r;
+    }
+    DevTrace tr{};
+    tr.n_jobs = (uint32_t)(b->offsets[t + 1] - b->offsets[t]);
+    tr.has_perm = tc.identity ? 0 : 1;
+    tr.ev_cap = 64 * tr.n_jobs + 256;
+    tr.tl_cap = 32 * tr.n_jobs + 64;
+    const size_t N = std::max<uint32_t>(tr.n_jobs, 1);
+    std::vector<double> ha(N), hs(N);
+    std::vector<uint8_t> hp(N);
+    std::vector<int64_t> hid(N);
+    std::vector<uint32_t> hperm(N);
+    stage_trace_arrays(b, t, tr, ha.data(), hs.data(), hp.data(), hid.data(), hperm.data());
+    cs.dev.init_off = 0;
+    DevTables tables;
+    build_tables(&tables);
+    std::vector<int32_t> queue(N);
+    std::vector<JobOut> jobs(N);
+    std::vector<EventRec> evs(tr.ev_cap);
+    std::vector<double> tl(2 * (size_t)tr.tl_cap);
+    DevSummary sum{};
+    SimArgs a{};
+    a.traces = &tr;
+    a.configs = &cs.dev;
+    a.init_slots = cs.init.empty() ? nullptr : cs.init.data();
+    a.tables = &tables;
+    a.arrival = ha.data();
+    a.service = hs.data();
+    a.profile = hp.data();
+    a.perm = hperm.data();
+    a.queue = queue.data();
+    a.jobs = jobs.data();
+    a.events = evs.data();
+    a.timeline = tl.data();
+    a.summary = &sum;
+    a.n_traces = 1;
+    a.out_flags = OF_JOBS | OF_EVENTS | OF_TIMELINE;
+    const int G = c->gpu_count;
+    if (G <= 4) run_warp<1>(a, &tables);
+    else if (G <= 8) run_warp<2>(a, &tables);
+    else if (G <= 16) run_warp<4>(a, &tables);
+    else run_warp<8>(a, &tables);
+
+    msg_trace_summary& o = r->summary;
+    o.status = sum.status;
+    o.n_jobs = tr.n_jobs;
+    o.handler_events = sum.handler_events;
+    o.n_events = sum.n_events;
+    o.timeline_samples = sum.timeline_samples;
+    o.migration_count = sum.migrations;
+    o.reconfig_op_count = sum.reconfig_ops;
+    o.enqueue_count = sum.enqueues;
+    o.dequeue_count = sum.dequeues;
+    o.max_arrival_frag_evals = sum.max_arr;
+    o.max_intra_iter_frag_evals = sum.max_intra;
+    o.max_inter_iter_frag_evals = sum.max_inter;
+    o.mean_wait_s = sum.mean_wait;
+    o.mean_execution_s = sum.mean_exec;
+    o.mean_turnaround_s = sum.mean_turn;
+    o.workload_makespan_s = sum.makespan;
+    o.timeline_sum = sum.tl_sum;
+    r->status = sum.status;
+    if (sum.status != MSG_OK) {
+        r->message = "JobsPending";
+        return r;
+    }
+    for (uint32_t k = 0; k < tr.n_jobs; ++k) {
+        msg_job_row row;
+        std::memset(&row, 0, sizeof(row));
+        row.id = hid[k];
+        row.arrival_s = ha[k];
+        row.scheduled_s = jobs[k].sched;
+        row.completed_s = jobs[k].done;
+        row.wait_s = row.scheduled_s - row.arrival_s;
+        row.execution_s = row.completed_s - row.scheduled_s;
+        row.turnaround_s = row.wait_s + row.execution_s;
+        row.profile = hp[k];
+        row.gpu = jobs[k].gpu;
+        row.migrations = jobs[k].mig;
+        r->jobs.push_back(row);
+    }
+    const uint64_t ne = std::min<uint64_t>(sum.n_events, tr.ev_cap);
+    r->events.resize(ne);
+    for (uint64_t i = 0; i < ne; ++i) decode_event(evs[i], hid.data(), c->migration_overlap_s, &r->events[i]);
+    const uint64_t nt = std::min<uint64_t>(sum.timeline_samples, tr.tl_cap);
+    for (uint64_t i = 0; i < nt; ++i) r->timeline.push_back({tl[2 * i], tl[2 * i + 1]});
+    return r;
+}
+
+int emu_result_status(void* h) { return static_cast<EmuResult*>(h)->status; }
+const char* emu_result_message(void* h) { return static_cast<EmuResult*>(h)->message.c_str(); }
+const msg_trace_summary* emu_result_summary(void* h) { return &static_cast<EmuResult*>(h)->summary; }
+const msg_event* emu_result_events(void* h, uint64_t* n) {
+    auto* r = static_cast<EmuResult*>(h);
+    *n = r->events.size();
+    return r->events.data();
+}
+const msg_job_row* emu_result_jobs(void* h, uint64_t* n) {
+    auto* r = static_cast<EmuResult*>(h);
+    *n = r->jobs.size();
+    return r->jobs.data();
+}
+const msg_timeline_point* emu_result_timeline(void* h, uint64_t* n) {
+    auto* r = static_cast<EmuResult*>(h);
+    *n = r->timeline.size();
+    return r->timeline.data();
+}
+void emu_result_free(void* h) { delete static_cast<EmuResult*>(h); }
+
+}  // extern "C"

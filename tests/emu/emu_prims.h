@@ -1,0 +1,101 @@
+// TEST INFRASTRUCTURE ONLY — host-thread emulation of one warp.
+//
+// Provides the wp:: primitives of paper_2512_16099_b200/csrc/warp_prims.cuh
+// so engine_core.cuh (the device code, unchanged) can be executed by 32
+// std::threads on the CPU-only build box.  Every collective is a full
+// barrier with double-buffered lane exchange; smem is plain shared host
+// memory.  Used by tests/test_emu_parity.py to check the kernel logic against
+// the reference before any GPU time is spent.  Never loaded by the product.
+#pragma once
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+
+#define MSG_DI inline
+
+namespace wp {
+
+struct EmuWarp {
+    std::atomic<unsigned> arrived{0};
+    std::atomic<unsigned> gen{0};
+    uint64_t buf[2][32];
+};
+
+inline thread_local EmuWarp* g_warp = nullptr;
+inline thread_local unsigned g_lane = 0;
+inline thread_local unsigned g_phase = 0;
+
+inline void barrier() {
+    EmuWarp* w = g_warp;
+    const unsigned g = w->gen.load(std::memory_order_acquire);
+    if (w->arrived.fetch_add(1, std::memory_order_acq_rel) == 31) {
+        w->arrived.store(0, std::memory_order_relaxed);
+        w->gen.fetch_add(1, std::memory_order_release);
+    } else {
+        unsigned spins = 0;
+        while (w->gen.load(std::memory_order_acquire) == g) {
+            if (++spins > 32) std::this_thread::yield();
+        }
+    }
+}
+
+inline const uint64_t* exchange(uint64_t v) {
+    uint64_t* b = g_warp->buf[g_phase & 1u];
+    b[g_lane] = v;
+    ++g_phase;
+    barrier();
+    return b;
+}
+
+inline unsigned lane() { return g_lane; }
+inline void sync() { barrier(); }
+inline unsigned ballot(bool p) {
+    const uint64_t* b = exchange(p ? 1u : 0u);
+    unsigned m = 0;
+    for (int i = 0; i < 32; ++i)
+        if (b[i]) m |= 1u << i;
+    return m;
+}
+inline unsigned rmin(unsigned x) {
+    const uint64_t* b = exchange(x);
+    unsigned m = 0xFFFFFFFFu;
+    for (int i = 0; i < 32; ++i) m = (unsigned)b[i] < m ? (unsigned)b[i] : m;
+    return m;
+}
+inline unsigned radd(unsigned x) {
+    const uint64_t* b = exchange(x);
+    unsigned m = 0;
+    for (int i = 0; i < 32; ++i) m += (unsigned)b[i];
+    return m;
+}
+inline unsigned ror(unsigned x) {
+    const uint64_t* b = exchange(x);
+    unsigned m = 0;
+    for (int i = 0; i < 32; ++i) m |= (unsigned)b[i];
+    return m;
+}
+inline unsigned shfl(unsigned x, int src) { return (unsigned)exchange(x)[src & 31]; }
+inline int shfl(int x, int src) { return (int)(unsigned)exchange((unsigned)x)[src & 31]; }
+inline double shfl(double x, int src) {
+    uint64_t u;
+    std::memcpy(&u, &x, 8);
+    const uint64_t r = exchange(u)[src & 31];
+    double d;
+    std::memcpy(&d, &r, 8);
+    return d;
+}
+inline int popc(unsigned x) { return __builtin_popcount(x); }
+inline int ffs(unsigned x) { return __builtin_ffs((int)x); }
+// Built with -ffp-contract=off and no -march: plain SSE2 ops, one rounding each.
+inline double dadd(double a, double b) { return a + b; }
+inline double dsub(double a, double b) { return a - b; }
+inline double dmul(double a, double b) { return a * b; }
+inline double ddiv(double a, double b) { return a / b; }
+inline uint64_t dbits(double d) {
+    uint64_t u;
+    std::memcpy(&u, &d, 8);
+    return u;
+}
+
+}  // namespace wp
