@@ -1,0 +1,136 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the unmodified
+reference library, bit for bit — event logs, per-job rows, timelines and
+summaries (SURVEY §8c/§8d parity bar: placements, reconfigurations and
+migration sequences exact; makespan/JCT/timeline here also exact)."""
+import numpy as np
+import pytest
+
+from helpers import diff_results
+from oracle import refbind as rb
+from paper_2512_16099_b200 import abi
+from paper_2512_16099_b200.model import (
+    EXPONENTIAL,
+    FIXED,
+    FeatureFlags,
+    Job,
+    SchedulerConfig,
+    SimConfig,
+    TraceBatch,
+    WorkloadSpec,
+    preset,
+    preset_names,
+    static_layout_preset,
+)
+
+pytestmark = pytest.mark.gpu
+
+ALL = abi.OUT_JOBS | abi.OUT_EVENTS | abi.OUT_TIMELINE
+
+
+@pytest.fixture(scope="module")
+def engine():
+    from paper_2512_16099_b200.engine import Engine
+
+    return Engine(0)
+
+
+def _check(engine, batch, cfgs):
+    ref = rb.ref_run_batch_results(batch, cfgs)
+    gpu = engine.run_batch(batch, cfgs, ALL)
+    bad = [(t, d) for t, (r, g) in enumerate(zip(ref, gpu)) if (d := diff_results(r, g))]
+    assert not bad, bad[:3]
+    return ref, gpu
+
+
+def test_c1_default_run_8_and_4_gpus(engine):
+    b = rb.ref_generate_batch(preset("normal25"), [0])
+    for G in (8, 4):
+        ref, gpu = _check(engine, b, [SimConfig(gpu_count=G)])
+    # survey anchors: C1 at 8 GPUs
+    r8 = engine.run_batch(b, [SimConfig(gpu_count=8)], ALL)[0]
+    assert r8.workload_makespan_s == 5550.2306096587145
+    assert r8.migration_count == 74 and r8.reconfig_op_count == 156 and len(r8.events) == 704
+
+
+@pytest.mark.parametrize("name", preset_names())
+def test_presets_many_seeds(engine, name):
+    b = rb.ref_generate_batch(preset(name), range(64))
+    _check(engine, b, [SimConfig(gpu_count=4)])
+    _check(engine, b, [SimConfig(gpu_count=8)])
+
+
+def test_c3_ablation_combos_in_one_launch(engine):
+    combos = [FeatureFlags(False, False, False), FeatureFlags(True, False, False),
+              FeatureFlags(True, True, False), FeatureFlags(True, True, True)]
+    cfgs = [SimConfig(gpu_count=4, sched=SchedulerConfig(
+        features=f, static_layout=None if f.dynamic_partitioning else static_layout_preset("static-a")))
+        for f in combos]
+    parts = []
+    for ia in (10.0, 15.0, 25.0, 35.0, 50.0):
+        sp = preset("normal25")
+        sp.mean_interarrival_s = ia
+        parts.append(rb.ref_generate_batch(sp, range(8)))
+    traces = [p.trace(t) for p in parts for t in range(p.n_traces)]
+    all_traces = [tr for tr in traces for _ in cfgs]
+    ci = [c for _ in traces for c in range(len(cfgs))]
+    batch = TraceBatch.from_traces(all_traces, config_index=ci)
+    _check(engine, batch, cfgs)
+
+
+def test_c5_high_churn(engine):
+    sp = WorkloadSpec(mean_interarrival_s=0.4, median_s=4.0, sigma=1.2, profile_mix=(0.5, 0.3, 0.2, 0.0))
+    cfg = SimConfig(gpu_count=8, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                    reconfig_latency_s=0.1)
+    _check(engine, rb.ref_generate_batch(sp, range(128)), [cfg])
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5, 16, 32])
+def test_cluster_sizes_and_ties(engine, G):
+    sp = WorkloadSpec(mean_interarrival_s=4.0, family=FIXED, value_s=20.0, job_count=150)
+    _check(engine, rb.ref_generate_batch(sp, range(8)),
+           [SimConfig(gpu_count=G, reconfig_latency_s=0.25, migration_overlap_s=1.0)])
+    sp = WorkloadSpec(mean_interarrival_s=2.0, family=EXPONENTIAL, job_count=150)
+    _check(engine, rb.ref_generate_batch(sp, range(8)), [SimConfig(gpu_count=G, sched=SchedulerConfig(threshold=0.6))])
+
+
+def test_shuffled_ids_equal_times_and_errors(engine):
+    traces = [
+        [Job(7, 0.0, 5, 10.0), Job(3, 0.0, 3, 5.0), Job(5, 0.0, 5, 10.0), Job(1, 1.0, 2, 3.0)],
+        [Job(0, 10.0, 5, 1.0), Job(1, 5.0, 5, 1.0)],          # TraceUnsorted
+        [Job(0, 0.0, 9, 1.0)],                                 # UnknownProfile
+        [Job(0, 0.0, 5, 0.0)],                                 # BadSpec
+        [Job(4, 0.0, 5, 1.0), Job(4, 1.0, 5, 1.0)],            # duplicate id
+        [Job(0, -0.5, 0, 5.0), Job(1, -0.5, 0, 5.0), Job(2, 0.0, 5, 1.0)],
+        [],
+    ]
+    _check(engine, TraceBatch.from_traces(traces), [SimConfig(gpu_count=1)])
+    _check(engine, TraceBatch.from_traces(traces), [SimConfig(gpu_count=2, migration_overlap_s=3.0)])
+
+
+def test_jobs_pending_and_bad_configs(engine):
+    tr = [[Job(0, 0.0, 0, 10.0)]]
+    cfg = SimConfig(gpu_count=1, sched=SchedulerConfig(
+        features=FeatureFlags(True, False, True), static_layout=[[(2, 0), (2, 4)]]))
+    _check(engine, TraceBatch.from_traces(tr), [cfg])
+    for bad in (SimConfig(gpu_count=0), SimConfig(sched=SchedulerConfig(threshold=1.5)),
+                SimConfig(sched=SchedulerConfig(features=FeatureFlags(True, False, True)))):
+        _check(engine, TraceBatch.from_traces(tr), [bad])
+
+
+def test_c2_full_ensemble_summaries(engine):
+    """BASELINE config C2 at full size: 4096 traces x 200 jobs, 8 GPUs."""
+    from paper_2512_16099_b200.engine import generate_batch
+
+    b = generate_batch(preset("normal25"), 0, 4096)
+    cfg = SimConfig(gpu_count=8)
+    gpu = engine.run_batch(b, [cfg], 0)
+    ref, _ = rb.ref_run_batch_summaries(b, [cfg], threads=0)
+    got = np.array([g.summary for g in gpu])
+    for f in ("status", "handler_events", "migration_count", "reconfig_op_count", "dequeue_count",
+              "mean_turnaround_s", "workload_makespan_s", "mean_wait_s", "timeline_sum",
+              "max_arrival_frag_evals", "max_inter_iter_frag_evals", "max_intra_iter_frag_evals"):
+        assert got[f].tobytes() == ref[f].tobytes(), f
+    # SURVEY Appendix B aggregate anchors
+    assert int(got["handler_events"].sum()) == 1638400
+    assert int(got["migration_count"].sum()) == 311361
+    assert int(got["reconfig_op_count"].sum()) == 728524

@@ -1,0 +1,4 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -15
+python tools/quick_bench.py 2>&1 | tail -20
