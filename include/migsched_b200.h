@@ -270,6 +270,11 @@ const msg_event* msg_result_events(const msg_batch_result* result, uint32_t trac
 const msg_timeline_point* msg_result_timeline(const msg_batch_result* result, uint32_t trace,
                                               uint64_t* n);
 const char* msg_result_message(const msg_batch_result* result, uint32_t trace);
+/* Bulk views: every trace's summary (n_traces, contiguous), and every
+ * trace's job rows concatenated in trace order with n_traces + 1 offsets
+ * (NULL unless MSG_OUT_JOBS).  Traces that failed have no rows. */
+const msg_trace_summary* msg_result_summaries(const msg_batch_result* result);
+const msg_job_row* msg_result_all_jobs(const msg_batch_result* result, const uint64_t** offsets, uint64_t* n);
 void msg_result_free(msg_batch_result* result);
 
 /* ---- workload generation: migsched::generate (workload.hpp:45,
@@ -349,13 +354,41 @@ msg_status msg_schedule_batch(msg_engine* engine, int32_t op, uint32_t n, int32_
  * the profile table).  msg_pack_gpu_word builds it from 8 slots. */
 uint64_t msg_pack_gpu_word(const msg_instance* slots8);
 
-/* Batched scorer over large clusters: n snapshots × gpu_count packed words
- * (device pointers, resident in HBM), one profile per snapshot; writes one
- * msg_decision per snapshot (device pointer).  `keys_out` optionally
- * receives the packed 64-bit argmin key per snapshot (device pointer). */
-msg_status msg_score_device(msg_engine* engine, uint32_t n, int64_t gpu_count,
-                            const uint64_t* d_words, const uint8_t* d_profile,
-                            const msg_sched_config* cfg, uint64_t* d_keys_out);
+/* Batched scorer over large clusters (SURVEY §8d roofline path): n
+ * snapshots × gpu_count packed words (device pointers, resident in HBM), one
+ * job profile per snapshot (device).  d_out (device) receives 2 u64 per
+ * snapshot: d_out[2i] = argmin key
+ *   schedule:   pass << 41 | cost rank << 36 | !reused << 35 | gpu << 3 | start
+ *   first fit:  gpu << 3 | start
+ * or UINT64_MAX when the job would queue; d_out[2i+1] = (candidates on Lazy
+ * GPUs) << 32 | (candidates on Busy GPUs).  Asynchronous on the engine
+ * stream. */
+msg_status msg_score_device(msg_engine* engine, uint32_t n, int64_t gpu_count, const uint64_t* d_words,
+                            const uint8_t* d_profile, const msg_sched_config* cfg, uint64_t* d_out);
+/* Same launch bracketed by CUDA events on the engine stream; returns the
+ * kernel's device time in milliseconds (synchronous). */
+msg_status msg_time_score_device(msg_engine* engine, uint32_t n, int64_t gpu_count, const uint64_t* d_words,
+                                 const uint8_t* d_profile, const msg_sched_config* cfg, uint64_t* d_out,
+                                 float* ms);
+
+/* try_dequeue (scheduler.cpp:106-121): strict FCFS over each snapshot's
+ * queue (CSR: queue_offsets n+1, queue_job, queue_profile).  Slots are
+ * updated in place; placed[queue_offsets[i] + k] receives the k-th dequeued
+ * head of snapshot i, n_placed[i] how many were placed. */
+typedef struct msg_dequeue_item {
+    int64_t job;
+    int32_t gpu;
+    int32_t start;
+    int32_t size;
+    int32_t reused;
+    int32_t evaluated_candidates;
+    int32_t n_destroyed;
+} msg_dequeue_item;
+
+msg_status msg_try_dequeue_batch(msg_engine* engine, uint32_t n, int32_t gpu_count, msg_instance* slots,
+                                 const uint64_t* queue_offsets, const int64_t* queue_job,
+                                 const int32_t* queue_profile, const msg_sched_config* cfg,
+                                 msg_dequeue_item* placed, uint32_t* n_placed);
 
 /* Migration planning on snapshots: on_departure / plan_intra / plan_inter
  * (migration.cpp:71-220).  Slots are updated in place (moves are applied

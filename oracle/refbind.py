@@ -65,6 +65,9 @@ def ref_lib():
         lib.ref_plan.restype = C.c_int
         lib.ref_plan.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_double, C.c_int32,
                                  C.c_double, C.c_uint32, C.c_void_p, C.c_void_p]
+        lib.ref_try_dequeue.restype = C.c_int
+        lib.ref_try_dequeue.argtypes = [C.c_int32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
         lib.ref_frag_cost.argtypes = [C.c_uint8] * 4 + [C.POINTER(C.c_int64)] * 2
         lib.ref_oracle_run_all.restype = C.c_int
         lib.ref_enumerate_states.restype = C.c_int64
@@ -240,3 +243,22 @@ def ref_enumerate_states(depth: int):
         states.append([(int(buf[i + 1 + 2 * j]), int(buf[i + 2 + 2 * j])) for j in range(k)])
         i += 1 + 2 * k
     return states
+
+
+def ref_try_dequeue(slots: np.ndarray, queue, threshold=0.4, lb=True, dyn=True):
+    """queue: list of (job, profile). Returns (status, placed list of dicts, slots)."""
+    lib = ref_lib()
+    cfg = abi.MsgSchedConfig()
+    cfg.threshold = threshold
+    cfg.load_balancing = int(lb)
+    cfg.dynamic_partitioning = int(dyn)
+    slots = np.ascontiguousarray(slots, abi.INSTANCE_DTYPE).copy()
+    dt = np.dtype([("job", "<i8"), ("gpu", "<i4"), ("start", "<i4"), ("size", "<i4"), ("reused", "<i4"),
+                   ("evaluated_candidates", "<i4"), ("n_destroyed", "<i4")])
+    placed = np.zeros(max(len(queue), 1), dt)
+    n = np.zeros(1, np.uint32)
+    qj = np.array([j for j, _ in queue] or [0], np.int64)
+    qp = np.array([p for _, p in queue] or [0], np.int32)
+    st = lib.ref_try_dequeue(len(slots) // 8, slots.ctypes.data, len(queue), qj.ctypes.data, qp.ctypes.data,
+                             C.byref(cfg), placed.ctypes.data, n.ctypes.data)
+    return st, [dict(zip(dt.names, (x.item() for x in r))) for r in placed[: int(n[0])]], slots

@@ -1,0 +1,22 @@
+// Host-visible launch wrappers of the decision-level kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dev_types.h"
+
+namespace msgk {
+
+struct ScoreArgs {
+    const DevTables* tables;
+    const uint64_t* words;    // n * G packed GPU words (msg_pack_gpu_word)
+    const uint8_t* profile;   // n job profiles
+    uint64_t* out;            // 2 per snapshot: argmin key, (lazy << 32 | busy) candidate counts
+    uint64_t G;
+    uint32_t n;
+    uint32_t lb, dyn, lazymask;
+};
+
+cudaError_t launch_snapshot(const SnapArgs& a, cudaStream_t stream);
+cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream);
+
+}  // namespace msgk

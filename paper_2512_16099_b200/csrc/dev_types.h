@@ -125,6 +125,43 @@ struct SimArgs {
     uint32_t out_flags;
 };
 
+// Decision-level kernel arguments (decide.cu): one warp per cluster snapshot
+// of G <= 32 GPUs.  Slot words: state (ST_*) | profile << 4 | cseq << 8.
+enum : int32_t {
+    SOP_SCHEDULE = 0,
+    SOP_FIRST_FIT = 1,
+    SOP_DISPATCH = 2,
+    SOP_ON_DEPARTURE = 10,
+    SOP_PLAN_INTRA = 11,
+    SOP_PLAN_INTER = 12,
+    SOP_TRY_DEQUEUE = 20
+};
+struct SnapArgs {
+    const DevTables* tables;
+    const uint32_t* slot_in;   // n * G * 8
+    const int32_t* job_in;     // n * G * 8 job ranks, -1 none
+    uint32_t* slot_out;
+    int32_t* job_out;
+    const int32_t* arg;        // per snapshot: profile (schedule) or gpu (plans)
+    const int32_t* queue;      // try_dequeue: per snapshot q_cap job ranks
+    const uint32_t* q_len;     // try_dequeue: per snapshot queue length
+    const uint8_t* rank_profile;  // try_dequeue: per snapshot rank_cap profiles, indexed by job rank
+    JobOut* scratch;           // per snapshot rank_cap job outputs (unused results)
+    int32_t* out;              // per snapshot 8 ints
+    EventRec* events;          // per snapshot ev_cap records
+    uint32_t ev_cap;
+    uint32_t q_cap;
+    uint32_t rank_cap;
+    uint32_t n;
+    int32_t G;
+    int32_t op;
+    uint32_t cflags;
+    uint32_t lazymask;
+    double overlap;
+    int32_t enabled;
+    int32_t reserved;
+};
+
 // Constant geometry (profiles.cpp:8-15), packed per profile id.
 constexpr uint32_t kCsPack = 0x112347u;               // nibble p: compute slices
 constexpr uint32_t kMsPack = 0x122448u;               // nibble p: memory slices

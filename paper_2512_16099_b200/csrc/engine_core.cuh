@@ -140,6 +140,8 @@ struct TraceSim {
     uint64_t n_ev, n_handler, n_tl;
     int64_t n_mig, n_reconf, n_enq, n_deq;
     int max_arr, max_intra, max_inter;
+    uint32_t n_plan_iter;
+    bool snap_mode;
     double tl_sum, tl_mean;
     bool tl_dirty;
 
@@ -221,6 +223,8 @@ struct TraceSim {
         n_ev = n_handler = n_tl = 0;
         n_mig = n_reconf = n_enq = n_deq = 0;
         max_arr = max_intra = max_inter = 0;
+        n_plan_iter = 0;
+        snap_mode = false;
         tl_sum = 0.0;
         tl_mean = 0.0;
         tl_dirty = true;
@@ -251,6 +255,86 @@ struct TraceSim {
         }
         load_arrival();
         wp::sync();
+    }
+
+    // Decision-level mode (decide.cu): load one cluster snapshot instead of
+    // a trace.  Busy instances load as ST_RUN (running vs waiting does not
+    // matter to the scheduler or the planners), draining ones as ST_DRAIN.
+    MSG_DI void setup_snapshot(const SnapArgs& a, const DevTables* tables, WS* ws, uint32_t i) {
+        L = wp::lane();
+        sm = ws;
+        tb = tables;
+        G = a.G;
+        cflags = a.cflags;
+        lazymask = a.lazymask;
+        alpha = 0.0;
+        overlap = a.overlap;
+        latency = 0.0;
+        N = 0;
+        a_idx = 0;
+        now = 0.0;
+        q_head = 0;
+        q_tail = a.q_len ? a.q_len[i] : 0;
+        queue = a.queue ? const_cast<int32_t*>(a.queue) + (size_t)i * a.q_cap : nullptr;
+        prf = a.rank_profile ? a.rank_profile + (size_t)i * a.rank_cap : nullptr;
+        svc = nullptr;
+        arr = nullptr;
+        perm = nullptr;
+        jobs = a.scratch ? a.scratch + (size_t)i * a.rank_cap : nullptr;
+        evs = a.events + (size_t)i * a.ev_cap;
+        ev_cap = a.ev_cap;
+        tl = nullptr;
+        tl_cap = 0;
+        oflags = OF_EVENTS;
+        mseq_ctr = 0;
+        n_ev = n_handler = n_tl = 0;
+        n_mig = n_reconf = n_enq = n_deq = 0;
+        max_arr = max_intra = max_inter = 0;
+        n_plan_iter = 0;
+        snap_mode = true;
+        tl_sum = tl_mean = 0.0;
+        tl_dirty = true;
+        const size_t base = (size_t)i * (size_t)G * 8;
+        unsigned maxseq = 0;
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) {
+            const int slot = L + 32 * k;
+            if (slot < G * 8) {
+                const uint32_t v = a.slot_in[base + slot];
+                sm->st[slot] = (uint8_t)(v & 0xFu);
+                sm->prof[slot] = (uint8_t)((v >> 4) & 0xFu);
+                sm->cseq[slot] = v >> 8;
+                sm->job[slot] = a.job_in[base + slot];
+                sm->mig[slot] = 0;
+                if ((v & 0xFu) != ST_EMPTY) {
+                    maxseq = (v >> 8) > maxseq ? (v >> 8) : maxseq;
+                    any = true;
+                }
+            } else {
+                sm->st[slot] = ST_EMPTY;
+            }
+        }
+        const unsigned mx = NONE - wp::rmin(NONE - maxseq);
+        cseq_ctr = wp::ballot(any) ? mx + 1u : 0u;
+        wp::sync();
+        for (int g = 0; g < G; ++g) refresh_gpu(g);
+    }
+
+    MSG_DI void store_snapshot(const SnapArgs& a, uint32_t i) {
+        wp::sync();
+        const size_t base = (size_t)i * (size_t)G * 8;
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) {
+            const int slot = L + 32 * k;
+            if (slot < G * 8) {
+                const uint8_t s = sm->st[slot];
+                const bool busy = s == ST_RUN || s == ST_WAIT;
+                a.slot_out[base + slot] = (uint32_t)(busy ? ST_RUN : s) | ((uint32_t)sm->prof[slot] << 4) |
+                                          (sm->cseq[slot] << 8);
+                a.job_out[base + slot] = busy ? sm->job[slot] : -1;
+            }
+        }
     }
 
     // Prefetch the next arrival timer (pushed in trace order, popped in
@@ -554,7 +638,7 @@ struct TraceSim {
         const unsigned nops = (unsigned)wp::popc(cr.dmask) + (cr.reused ? 0u : 1u);
         const double ss = apply_placement(d.g, d.s, r, sv, nops);
         emit(kind, r, (unsigned)d.g, 0, (unsigned)p, (unsigned)d.s, 0, EF_PLACED | (cr.reused ? EF_REUSED : 0),
-             wp::dbits(ss));
+             snap_mode ? (uint64_t)d.evals : wp::dbits(ss));
         emit_reconfig(d.g, p, d.s, cr);
     }
 
@@ -565,7 +649,7 @@ struct TraceSim {
             wp::sync();
             const int32_t h = queue[q_head];
             const int p = prf[h];
-            const double sv = svc[h];
+            const double sv = svc ? svc[h] : 0.0;
             const Decision d = dispatch(p);
             if (!d.placed) break;
             max_arr = max_arr > (int)d.evals ? max_arr : (int)d.evals;
@@ -654,6 +738,7 @@ struct TraceSim {
             const unsigned best = wp::rmin(kmin);
             const int evals = (int)wp::radd(cnt);
             max_intra = max_intra > evals ? max_intra : evals;
+            ++n_plan_iter;
             if (best == NONE || (best >> 27) >= cur) break;  // strict improvement only
             const int wl = wp::ffs(wp::ballot(kmin == best)) - 1;
             apply_move(g * 8 + (wl & 7), g, (int)(best & 7u), false);
@@ -698,6 +783,7 @@ struct TraceSim {
             }
             const unsigned best = wp::rmin(kmin);
             int evals = (int)wp::radd(cnt);
+            ++n_plan_iter;
             if (best == NONE) {
                 max_inter = max_inter > evals ? max_inter : evals;
                 break;

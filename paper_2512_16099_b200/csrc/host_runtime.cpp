@@ -22,94 +22,11 @@
 #include "dev_types.h"
 #include "host_tables.h"
 #include "staging.h"
+#include "runtime.h"
 #include "kernels.h"
 #include "migsched_b200.h"
 
 using namespace msgk;
-
-namespace {
-
-template <class F>
-void parallel_for(uint32_t n, uint32_t min_per_thread, F&& f) {
-    uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
-    uint32_t threads = std::min(hw, std::max(1u, n / std::max(1u, min_per_thread)));
-    if (threads <= 1) {
-        for (uint32_t i = 0; i < n; ++i) f(i);
-        return;
-    }
-    std::atomic<uint32_t> next{0};
-    auto worker = [&]() {
-        for (;;) {
-            const uint32_t base = next.fetch_add(16);
-            if (base >= n) return;
-            const uint32_t end = std::min(n, base + 16);
-            for (uint32_t i = base; i < end; ++i) f(i);
-        }
-    };
-    std::vector<std::thread> pool;
-    for (uint32_t t = 1; t < threads; ++t) pool.emplace_back(worker);
-    worker();
-    for (auto& th : pool) th.join();
-}
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    cudaError_t ensure(size_t bytes) {
-        if (bytes <= cap && p) return cudaSuccess;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
-        cudaError_t e = cudaMalloc(&p, want);
-        if (e == cudaSuccess) cap = want;
-        return e;
-    }
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
-
-struct HostBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    cudaError_t ensure(size_t bytes) {
-        if (bytes <= cap && p) return cudaSuccess;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        cap = 0;
-        const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
-        cudaError_t e = cudaMallocHost(&p, want);
-        if (e == cudaSuccess) cap = want;
-        return e;
-    }
-    ~HostBuf() {
-        if (p) cudaFreeHost(p);
-    }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
-
-}  // namespace
-
-struct msg_engine {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    DevBuf tables;
-    DevBuf flush;
-    uint64_t launches = 0;
-    std::string last_error;
-    int sm_count = 0;
-    char name[256] = {0};
-    msg_staged* cached = nullptr;
-};
 
 struct msg_staged {
     msg_engine* eng = nullptr;
@@ -140,23 +57,14 @@ struct msg_staged {
 struct msg_batch_result {
     std::vector<msg_trace_summary> summaries;
     std::vector<std::string> messages;
-    std::vector<std::vector<msg_job_row>> jobs;
+    bool has_jobs = false;
+    std::vector<msg_job_row> jobs;        // all traces, trace-major
+    std::vector<uint64_t> job_off;        // n_traces + 1
     std::vector<std::vector<msg_event>> events;
     std::vector<std::vector<msg_timeline_point>> timeline;
 };
 
 namespace {
-
-msg_status cuda_fail(msg_engine* e, cudaError_t err, const char* what) {
-    if (e) e->last_error = std::string("CudaError: ") + what + ": " + cudaGetErrorString(err);
-    return MSG_ERR_CUDA;
-}
-
-#define CK(expr)                                                   \
-    do {                                                           \
-        cudaError_t _e = (expr);                                   \
-        if (_e != cudaSuccess) return cuda_fail(eng, _e, #expr);   \
-    } while (0)
 
 msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
                       uint32_t flags, msg_staged* s) {
@@ -382,7 +290,16 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
     auto res = std::make_unique<msg_batch_result>();
     res->summaries.resize(s->n_in);
     res->messages = s->message;
-    if (want_jobs) res->jobs.resize(s->n_in);
+    if (want_jobs) {
+        res->has_jobs = true;
+        res->job_off.assign(s->n_in + 1, 0);
+        for (uint32_t t = 0; t < s->n_in; ++t) {
+            const int32_t d = s->dev_index[t];
+            const bool rows = d >= 0 && s->h_summary.as<DevSummary>()[d].status == MSG_OK;
+            res->job_off[t + 1] = res->job_off[t] + (rows ? s->traces[d].n_jobs : 0);
+        }
+        res->jobs.resize(res->job_off[s->n_in]);
+    }
     if (want_ev) res->events.resize(s->n_in);
     if (want_tl) res->timeline.resize(s->n_in);
     const DevSummary* ds = s->h_summary.as<DevSummary>();
@@ -427,8 +344,7 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
             return;  // the reference throws: no report, no log
         }
         if (want_jobs) {
-            auto& rows = res->jobs[t];
-            rows.resize(tr.n_jobs);
+            msg_job_row* rows = res->jobs.data() + res->job_off[t];
             for (uint32_t r = 0; r < tr.n_jobs; ++r) {
                 const JobOut& j = hj[tr.job_off + r];
                 msg_job_row& row = rows[r];
@@ -606,9 +522,22 @@ const msg_trace_summary* msg_result_summary(const msg_batch_result* r, uint32_t 
 
 const msg_job_row* msg_result_jobs(const msg_batch_result* r, uint32_t t, uint64_t* n) {
     if (n) *n = 0;
-    if (!r || t >= r->jobs.size()) return nullptr;
-    if (n) *n = r->jobs[t].size();
-    return r->jobs[t].data();
+    if (!r || !r->has_jobs || t + 1 >= r->job_off.size()) return nullptr;
+    if (n) *n = r->job_off[t + 1] - r->job_off[t];
+    return r->jobs.data() + r->job_off[t];
+}
+
+const msg_trace_summary* msg_result_summaries(const msg_batch_result* r) {
+    return (r && !r->summaries.empty()) ? r->summaries.data() : nullptr;
+}
+
+const msg_job_row* msg_result_all_jobs(const msg_batch_result* r, const uint64_t** offsets, uint64_t* n) {
+    if (n) *n = 0;
+    if (offsets) *offsets = nullptr;
+    if (!r || !r->has_jobs) return nullptr;
+    if (offsets) *offsets = r->job_off.data();
+    if (n) *n = r->jobs.size();
+    return r->jobs.data();
 }
 
 const msg_event* msg_result_events(const msg_batch_result* r, uint32_t t, uint64_t* n) {

@@ -56,6 +56,8 @@ def lib():
         "msg_result_timeline": (vp, [vp, u32, C.POINTER(u64)]),
         "msg_result_message": (C.c_char_p, [vp, u32]),
         "msg_result_free": (None, [vp]),
+        "msg_result_summaries": (vp, [vp]),
+        "msg_result_all_jobs": (vp, [vp, C.POINTER(C.POINTER(u64)), C.POINTER(u64)]),
         "msg_workload_preset": (C.c_int, [C.c_char_p, vp]),
         "msg_generate": (C.c_int, [vp, vp, vp, vp, vp]),
         "msg_generate_many": (C.c_int, [vp, u64, u32, i32, vp, vp, vp, vp, vp]),
@@ -79,8 +81,9 @@ def _check(st: int, eng=None):
 class Staged:
     """A batch resident in HBM (msg_stage); launch/collect any number of times."""
 
-    def __init__(self, engine: "Engine", handle, n_traces: int, keep):
+    def __init__(self, engine: "Engine", handle, n_traces: int, keep, out_flags: int):
         self.engine = engine
+        self.out_flags = out_flags
         self._h = handle
         self.n_traces = n_traces
         self._keep = keep
@@ -97,7 +100,7 @@ class Staged:
         r = C.c_void_p()
         _check(lib().msg_collect(self.engine._h, self._h, C.byref(r)), self.engine)
         try:
-            return _decode(r)
+            return _decode(r, self.out_flags)
         finally:
             lib().msg_result_free(r)
 
@@ -162,7 +165,7 @@ class Engine:
         _check(lib().msg_run_batch(self._h, C.addressof(batch._c), C.addressof(pack.c[0]), len(pack),
                                    out_flags, C.byref(r)), self)
         try:
-            return _decode(r)
+            return _decode(r, out_flags)
         finally:
             lib().msg_result_free(r)
 
@@ -171,18 +174,36 @@ class Engine:
         h = C.c_void_p()
         _check(lib().msg_stage(self._h, C.addressof(batch._c), C.addressof(pack.c[0]), len(pack), out_flags,
                                C.byref(h)), self)
-        return Staged(self, h, batch.n_traces, (batch, pack))
+        return Staged(self, h, batch.n_traces, (batch, pack), out_flags)
 
 
-def _decode(r) -> list:
+def _decode(r, flags: int) -> list:
     L = lib()
     out = []
     n = L.msg_result_n_traces(r)
     cnt = C.c_uint64()
+    if n == 0:
+        return out
+    # bulk: summaries and job rows in two copies
+    summaries = np.frombuffer(C.string_at(L.msg_result_summaries(r), n * abi.SUMMARY_DTYPE.itemsize),
+                              abi.SUMMARY_DTYPE).copy()
+    offp = C.POINTER(C.c_uint64)()
+    jp = L.msg_result_all_jobs(r, C.byref(offp), C.byref(cnt))
+    jobs_all = offs = None
+    if jp:
+        jobs_all = np.frombuffer(C.string_at(jp, cnt.value * abi.JOB_DTYPE.itemsize), abi.JOB_DTYPE).copy()
+        offs = np.ctypeslib.as_array(offp, shape=(n + 1,)).copy()
+    with_events = bool(flags & abi.OUT_EVENTS)
+    with_tl = bool(flags & abi.OUT_TIMELINE)
     for t in range(n):
-        sp = L.msg_result_summary(r, t)
-        summary = np.frombuffer(C.string_at(sp, abi.SUMMARY_DTYPE.itemsize), abi.SUMMARY_DTYPE)[0].copy()
-        msg = L.msg_result_message(r, t).decode()
+        summary = summaries[t]
+        st = int(summary["status"])
+        msg = L.msg_result_message(r, t).decode() if st != 0 else ""
+        jobs = jobs_all[offs[t]:offs[t + 1]] if jobs_all is not None else None
+        out.append(TraceResult(st, msg, summary, jobs, None, None))
+    if not (with_events or with_tl):
+        return out
+    for t in range(n):
 
         def arr(fn, dtype):
             p = fn(r, t, C.byref(cnt))
@@ -190,16 +211,8 @@ def _decode(r) -> list:
                 return None if not p else np.zeros(0, dtype)
             return np.frombuffer(C.string_at(p, cnt.value * dtype.itemsize), dtype).copy()
 
-        out.append(
-            TraceResult(
-                int(summary["status"]),
-                msg,
-                summary,
-                arr(L.msg_result_jobs, abi.JOB_DTYPE),
-                arr(L.msg_result_events, abi.EVENT_DTYPE),
-                arr(L.msg_result_timeline, abi.TIMELINE_DTYPE),
-            )
-        )
+        out[t].events = arr(L.msg_result_events, abi.EVENT_DTYPE)
+        out[t].frag_timeline = arr(L.msg_result_timeline, abi.TIMELINE_DTYPE)
     return out
 
 

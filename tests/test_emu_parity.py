@@ -1,0 +1,46 @@
+"""CPU-side check of the DEVICE code's logic: engine_core.cuh compiled for
+the host with a 32-thread warp emulation (tests/emu, test-only) must
+reproduce the reference bit for bit.  This runs on the build box without a
+GPU; tests/test_gpu_parity.py repeats the comparison on the B200 itself."""
+import numpy as np
+import pytest
+
+from helpers import diff_results, emu_run_batch_results, golden_runs
+from oracle import refbind as rb
+from paper_2512_16099_b200.model import (
+    EXPONENTIAL,
+    FeatureFlags,
+    SchedulerConfig,
+    SimConfig,
+    TraceBatch,
+    WorkloadSpec,
+    static_layout_preset,
+)
+
+
+@pytest.mark.parametrize("name", sorted(golden_runs().keys()))
+def test_emulated_kernel_matches_golden(name):
+    batch, cfg, ref, _ = golden_runs()[name]
+    got = emu_run_batch_results(batch, [cfg])[0]
+    assert diff_results(ref, got) == ""
+
+
+@pytest.mark.skipif(not rb.port_available(), reason="oracle port not built")
+def test_emulated_kernel_vs_port_randomized():
+    from paper_2512_16099_b200.engine import generate
+
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        G = int(rng.choice([1, 2, 4, 5, 8, 12]))
+        dyn = bool(rng.integers(0, 2)) or G != 4
+        feats = FeatureFlags(bool(rng.integers(0, 2)), dyn, bool(rng.integers(0, 2)))
+        sp = WorkloadSpec(mean_interarrival_s=float(rng.choice([1.0, 5.0, 20.0])), job_count=60,
+                          family=int(rng.choice([0, EXPONENTIAL])), seed=int(rng.integers(0, 1 << 30)))
+        cfg = SimConfig(gpu_count=G, sched=SchedulerConfig(
+            threshold=float(rng.choice([0.0, 0.3, 0.5, 1.0])), features=feats,
+            static_layout=None if dyn else static_layout_preset("static-c")),
+            migration_overlap_s=float(rng.choice([0.0, 2.0])), reconfig_latency_s=float(rng.choice([0.0, 0.3])))
+        b = TraceBatch.from_traces([generate(sp)])
+        want = rb.port_run_batch_results(b, [cfg])[0]
+        got = emu_run_batch_results(b, [cfg])[0]
+        assert diff_results(want, got) == "", (G, feats, cfg)
