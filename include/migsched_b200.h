@@ -323,6 +323,7 @@ typedef struct msg_instance {
     uint16_t reserved0;
 } msg_instance;
 
+/* When placed == 0 every field except evaluated_candidates is zero. */
 typedef struct msg_decision {
     int32_t placed;   /* 0 = queue the job                         */
     int32_t gpu;

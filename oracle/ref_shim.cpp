@@ -439,6 +439,39 @@ int ref_plan(int32_t op, int32_t G, msg_instance* slots, int32_t gpu, double thr
     return MSG_OK;
 }
 
+// try_dequeue (scheduler.cpp:106-121) on one snapshot.
+int ref_try_dequeue(int32_t G, msg_instance* slots, uint32_t nq, const int64_t* qjob, const int32_t* qprof,
+                    const msg_sched_config* c, msg_dequeue_item* placed, uint32_t* n_placed) {
+    std::vector<GpuState> gpus;
+    for (int g = 0; g < G; ++g) gpus.push_back(build_gpu(slots + 8 * g, g));
+    SchedulerConfig cfg;
+    cfg.threshold = c->threshold;
+    cfg.features.load_balancing = c->load_balancing != 0;
+    cfg.features.dynamic_partitioning = c->dynamic_partitioning != 0;
+    std::deque<JobRequest> q;
+    for (uint32_t i = 0; i < nq; ++i) q.push_back({qjob[i], static_cast<ProfileId>(static_cast<std::uint8_t>(qprof[i]))});
+    try {
+        const auto res = try_dequeue(q, gpus, cfg);
+        *n_placed = static_cast<uint32_t>(res.size());
+        for (std::size_t i = 0; i < res.size(); ++i) {
+            msg_dequeue_item& o = placed[i];
+            o.job = res[i].job.id;
+            o.gpu = res[i].outcome.gpu;
+            o.start = res[i].outcome.placement.start;
+            o.size = res[i].outcome.placement.size;
+            o.reused = res[i].create.reused ? 1 : 0;
+            o.evaluated_candidates = res[i].evaluated_candidates;
+            int d = 0;
+            for (const ReconfigOp& op : res[i].create.ops) d += op.action == ReconfigAction::Destroy;
+            o.n_destroyed = d;
+        }
+        for (int g = 0; g < G; ++g) dump_gpu(gpus[g], slots + 8 * g);
+    } catch (const Error& e) {
+        return status_of(e.code());
+    }
+    return MSG_OK;
+}
+
 // Frag cost of a state word (busy_c, busy_m, blocked_c, blocked_m) as the
 // exact Frac pair (frag.cpp:44-58).
 void ref_frag_cost(uint8_t bc, uint8_t bm, uint8_t kc, uint8_t km, int64_t* num, int64_t* den) {

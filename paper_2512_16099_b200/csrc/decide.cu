@@ -28,57 +28,7 @@ __global__ void __launch_bounds__(32 * kSnapWarps) snapshot_kernel(SnapArgs a) {
     const uint32_t i = blockIdx.x * kSnapWarps + w;
     if (i >= a.n) return;
     WarpSmem<SPL>* ws = reinterpret_cast<WarpSmem<SPL>*>(smem + sizeof(DevTables) + w * sizeof(WarpSmem<SPL>));
-    TraceSim<SPL> sim;
-    sim.setup_snapshot(a, tb, ws, i);
-    int32_t out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const int arg = a.arg ? a.arg[i] : 0;
-    if (a.op <= SOP_DISPATCH) {
-        if (a.op == SOP_SCHEDULE) sim.cflags |= CF_LB;
-        if (a.op == SOP_FIRST_FIT) sim.cflags &= ~CF_LB;
-        const Decision d = sim.dispatch(arg);
-        out[0] = d.placed;
-        out[1] = d.placed ? d.g : -1;
-        out[2] = d.placed ? d.s : 0;
-        out[3] = d.placed ? (int)ms_of(arg) : 0;
-        out[4] = d.placed && d.reused;
-        out[5] = (int)d.evals;
-    } else if (a.op == SOP_TRY_DEQUEUE) {
-        sim.dequeue_pass();
-        out[0] = (int)sim.q_head;  // placed heads
-        out[1] = (int)sim.n_ev;
-        sim.store_snapshot(a, i);
-    } else {
-        // on_departure (migration.cpp:212-220) / plan_intra / plan_inter
-        int kind = -1, status = 0;
-        const unsigned w0 = ws->gw[arg];
-        const bool lazy = (sim.lazymask >> __popc(w0 & 0x7Fu)) & 1u;
-        if (a.op == SOP_ON_DEPARTURE) {
-            if (a.enabled) {
-                kind = lazy ? 1 : 0;
-                if (lazy) sim.plan_inter(arg);
-                else sim.plan_intra(arg);
-            }
-        } else if (a.op == SOP_PLAN_INTRA) {
-            kind = 0;
-            sim.plan_intra(arg);
-        } else {
-            if (!lazy) {
-                status = 5;  // NotLazy (migration.cpp:127-129)
-            } else {
-                kind = 1;
-                sim.plan_inter(arg);
-            }
-        }
-        out[0] = status;
-        out[1] = kind;
-        out[2] = (int)sim.n_mig;
-        out[3] = (int)sim.n_plan_iter;
-        out[4] = kind == 0 ? sim.max_intra : sim.max_inter;
-        out[5] = (int)sim.n_ev;
-        sim.store_snapshot(a, i);
-    }
-    if (sim.L == 0)
-        for (int k = 0; k < 8; ++k) a.out[(size_t)i * 8 + k] = out[k];
+    snapshot_op<SPL>(a, tb, ws, i);
 }
 
 template <int SPL>

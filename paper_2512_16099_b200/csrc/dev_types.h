@@ -100,10 +100,12 @@ struct DevSummary {
 // fragmentation metric (frag.cpp:44-58) and staged into shared memory.
 struct DevTables {
     uint8_t cost2rank[8 * 256];  // [popc(busy_c)][busy_m] -> rank of the 2-mask cost
-    uint32_t feas[256];          // blocked_m -> 6 x 3-bit feasible counts
-    uint32_t ideal[8 * 9];       // [popc busy_c][popc busy_m] -> 6 x 3-bit ideal counts
+    double cost4val[256];        // 4-mask cost id -> frag_cost as double (k / 25200.0)
     uint16_t rank2k[32];         // cost rank -> numerator over 25200
     uint8_t placeable[256];      // blocked_m -> profiles with >= 1 free legal start
+    uint8_t feasid[256];         // blocked_m -> id of its per-profile feasible-count vector
+    uint8_t idealid[80];         // popc(busy_c) * 9 + popc(busy_m) -> id of its ideal-count vector
+    uint8_t cost4pair[32 * 32];  // [ideal id][feasible id] -> 4-mask cost id
 };
 
 // Kernel arguments of the per-trace event loop (engine_core.cuh).

@@ -70,14 +70,6 @@ MSG_DI uint64_t time_key(double t) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-MSG_DI unsigned q420(unsigned id) {  // 420 / ideal, ideal in 1..7 (frag.cpp:10,55)
-    return id == 1 ? 420u : id == 2 ? 210u : id == 3 ? 140u : id == 4 ? 105u : id == 5 ? 84u
-           : id == 6 ? 70u : 60u;
-}
-MSG_DI unsigned q60(unsigned c) {  // 60 / counted, counted in 1..6
-    return c == 1 ? 60u : c == 2 ? 30u : c == 3 ? 20u : c == 4 ? 15u : c == 5 ? 12u : 10u;
-}
-
 template <int SPL>
 struct WarpSmem {
     static constexpr int NS = 32 * SPL;  // slots
@@ -111,7 +103,10 @@ struct Decision {
     unsigned evals;
 };
 
-template <int SPL>
+// SPL: slots per lane (ceil(8G/32)).  DETAIL: the kernel writes the event
+// log / timeline records when requested; the summary-only instantiation has
+// no emission code at all (smaller hot loop, fewer I-cache misses).
+template <int SPL, bool DETAIL = true>
 struct TraceSim {
     using WS = WarpSmem<SPL>;
     WS* sm;
@@ -137,8 +132,8 @@ struct TraceSim {
     double a_t, a_svc;
     uint32_t q_head, q_tail;
     uint32_t cseq_ctr, mseq_ctr;
-    uint64_t n_ev, n_handler, n_tl;
-    int64_t n_mig, n_reconf, n_enq, n_deq;
+    uint32_t n_ev, n_handler, n_tl;
+    uint32_t n_mig, n_reconf, n_enq, n_deq;
     int max_arr, max_intra, max_inter;
     uint32_t n_plan_iter;
     bool snap_mode;
@@ -150,28 +145,17 @@ struct TraceSim {
         return tb->cost2rank[wp::popc(bc) * 256 + bm];
     }
     MSG_DI unsigned k2w(unsigned w) const { return tb->rank2k[rank2(w_bc(w), w_bm(w))]; }
-    // 4-mask cost numerator over 25200: busy drives ideal, blocked drives
-    // feasibility (frag.cpp:44-58 via frag_cost_exact, :60-63).
-    MSG_DI unsigned k4w(unsigned w) const {
-        const unsigned ideal = tb->ideal[wp::popc(w_bc(w)) * 9 + wp::popc(w_bm(w))];
-        const unsigned feas = tb->feas[w_km(w)];
-        unsigned ratio = 0, counted = 0;
-#pragma unroll
-        for (int p = 0; p < 6; ++p) {
-            const unsigned id = (ideal >> (3 * p)) & 7u;
-            if (id) {
-                ratio += ((feas >> (3 * p)) & 7u) * q420(id);
-                ++counted;
-            }
-        }
-        if (!counted) return 0;
-        return (420u * counted - ratio) * q60(counted);
+    // frag_cost(gpu) (frag.cpp:60-65): 4-mask cost, busy drives ideal and
+    // blocked drives feasibility; tabulated exactly on the host.
+    MSG_DI double cost4w(unsigned w) const {
+        const unsigned row = (unsigned)wp::popc(w_bc(w)) * 9u + (unsigned)wp::popc(w_bm(w));
+        return tb->cost4val[tb->cost4pair[tb->idealid[row] * 32u + tb->feasid[w_km(w)]]];
     }
 
     // --------------------------------------------------------------- events
     MSG_DI void emit(uint8_t kind, int32_t job, unsigned gpu, unsigned gpu2, unsigned prof,
                      unsigned start, unsigned start2, unsigned flags, uint64_t aux) {
-        if ((oflags & OF_EVENTS) && n_ev < ev_cap && L == 0) {
+        if (DETAIL && (oflags & OF_EVENTS) && n_ev < ev_cap && L == 0) {
             EventRec r;
             r.t = now;
             r.aux = aux;
@@ -368,7 +352,7 @@ struct TraceSim {
         const unsigned w = wp::ror(c) | (wp::radd(r) << 24);
         if (L == 0) {
             sm->gw[g] = w;
-            sm->gcost[g] = wp::ddiv((double)k4w(w), 25200.0);
+            sm->gcost[g] = cost4w(w);
         }
         tl_dirty = true;
         wp::sync();
@@ -422,7 +406,7 @@ struct TraceSim {
             tl_mean = wp::ddiv(tot, (double)G);
             tl_dirty = false;
         }
-        if ((oflags & OF_TIMELINE) && n_tl < tl_cap && L == 0) {
+        if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && L == 0) {
             tl[2 * n_tl] = now;
             tl[2 * n_tl + 1] = tl_mean;
         }
@@ -515,7 +499,8 @@ struct TraceSim {
                 }
             }
             const unsigned k = wp::rmin(kmin);
-            const unsigned NL = wp::radd(nl), NB = wp::radd(nb);
+            const unsigned cnt = wp::radd(nl | (nb << 16));  // <= 8 candidates per lane
+            const unsigned NL = cnt & 0xFFFFu, NB = cnt >> 16;
             d.evals = NL + (NL == 0 ? NB : 0u);  // Busy pass only if Lazy found nothing
             d.placed = k != NONE;
             d.g = (int)((k >> 3) & 0x3FFFFFu);
@@ -811,13 +796,19 @@ struct TraceSim {
     }
 
     // ------------------------------------------------------------ handlers
+    // Handler bodies (sim.cpp:220-323), laid out so the steps every handler
+    // shares (advance_all first, reschedule + sample last, the dequeue pass)
+    // exist once in the instruction stream:
+    //   Arrival:      advance; place or enqueue;                       reschedule; sample
+    //   Completion:   advance; release; log; sample; dequeue; [plan; dequeue]; reschedule; sample
+    //   MigrationEnd: advance; finish draining; log; dequeue;          reschedule; sample
+    //   ServiceStart: advance; start service;                          reschedule; sample
     MSG_DI void handle_arrival() {  // sim.cpp:220-267
         const int32_t r = (int32_t)a_rank;
         const int p = a_prof;
         const double sv = a_svc;
         ++a_idx;
         load_arrival();
-        advance_all();
         bool enq = q_head < q_tail;  // never overtake a non-empty queue
         if (!enq) {
             const Decision d = dispatch(p);
@@ -832,59 +823,40 @@ struct TraceSim {
             emit(EV_ENQUEUE, r, 0, 0, 0, 0, 0, 0, 0);
             ++n_enq;
         }
-        reschedule();
-        sample();
     }
 
-    MSG_DI void handle_completion(int slot) {  // sim.cpp:269-301
-        advance_all();
+    // Completion (sim.cpp:269-301) and MigrationEnd (sim.cpp:303-315).
+    MSG_DI void handle_departure(int slot, bool completion) {
         wp::sync();
         const int g = slot >> 3;
         const int32_t r = sm->job[slot];
         const int m = sm->mig[slot];
         wp::sync();
         if (L == 0) {
-            sm->st[slot] = ST_IDLE;  // release_job: the instance stays, idle
-            jobs[r].done = now;
-            jobs[r].gpu = g;
-            jobs[r].mig = m;
+            sm->st[slot] = ST_IDLE;  // release_job / finish_draining: the instance stays, idle
+            if (completion) {
+                jobs[r].done = now;
+                jobs[r].gpu = g;
+                jobs[r].mig = m;
+            }
         }
         refresh_gpu(g);
-        emit(EV_COMPLETION, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
-        sample();  // post-departure level
-        dequeue_pass();
-        if (cflags & CF_MIG) {
-            on_departure(g);
+        emit(completion ? EV_COMPLETION : EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
+        if (completion) sample();  // post-departure level
+        const int passes = (completion && (cflags & CF_MIG)) ? 2 : 1;
+        for (int pass = 0; pass < passes; ++pass) {
+            if (pass) on_departure(g);
             dequeue_pass();
         }
-        reschedule();
-        sample();
-    }
-
-    MSG_DI void handle_migration_end(int slot) {  // sim.cpp:303-315
-        advance_all();
-        wp::sync();
-        const int g = slot >> 3;
-        const int32_t r = sm->job[slot];
-        wp::sync();
-        if (L == 0) sm->st[slot] = ST_IDLE;  // finish_draining
-        refresh_gpu(g);
-        emit(EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
-        dequeue_pass();
-        reschedule();
-        sample();
     }
 
     MSG_DI void handle_service_start(int slot) {  // sim.cpp:317-323
-        advance_all();
         wp::sync();
         if (L == 0) {
             sm->st[slot] = ST_RUN;  // start_service: rem already holds service_s
             sm->last[slot] = now;
         }
         refresh_gpu(slot >> 3);
-        reschedule();
-        sample();
     }
 
     MSG_DI void run() {  // Engine::execute (sim.cpp:123-141)
@@ -893,10 +865,12 @@ struct TraceSim {
             const int kind = next_event(slot);
             if (kind < 0) break;
             ++n_handler;
+            advance_all();
             if (kind == 3) handle_arrival();
-            else if (kind == 0) handle_completion(slot);
-            else if (kind == 1) handle_migration_end(slot);
-            else handle_service_start(slot);
+            else if (kind == 2) handle_service_start(slot);
+            else handle_departure(slot, kind == 0);
+            reschedule();
+            sample();
         }
     }
 
@@ -970,12 +944,69 @@ struct TraceSim {
 
 // One warp, one trace: the body shared by the CUDA kernel and the CPU-side
 // unit-test emulation.
-template <int SPL>
+template <int SPL, bool DETAIL = true>
 MSG_DI void simulate_trace(const SimArgs& a, const DevTables* tables, WarpSmem<SPL>* ws, uint32_t t) {
-    TraceSim<SPL> sim;
+    TraceSim<SPL, DETAIL> sim;
     sim.setup(a, tables, ws, t);
     sim.run();
     sim.finish(a.summary + t);
+}
+
+// One decision-level operation on one cluster snapshot (decide.cu): the
+// body shared by the CUDA kernel and the CPU-side unit-test emulation.
+template <int SPL>
+MSG_DI void snapshot_op(const SnapArgs& a, const DevTables* tb, WarpSmem<SPL>* ws, uint32_t i) {
+    TraceSim<SPL> sim;
+    sim.setup_snapshot(a, tb, ws, i);
+    int32_t out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int arg = a.arg ? a.arg[i] : 0;
+    if (a.op <= SOP_DISPATCH) {
+        if (a.op == SOP_SCHEDULE) sim.cflags |= CF_LB;
+        if (a.op == SOP_FIRST_FIT) sim.cflags &= ~CF_LB;
+        const Decision d = sim.dispatch(arg);
+        out[0] = d.placed;
+        out[1] = d.placed ? d.g : 0;
+        out[2] = d.placed ? d.s : 0;
+        out[3] = d.placed ? (int)ms_of(arg) : 0;
+        out[4] = d.placed && d.reused;
+        out[5] = (int)d.evals;
+    } else if (a.op == SOP_TRY_DEQUEUE) {
+        sim.dequeue_pass();
+        out[0] = (int)sim.q_head;  // placed heads
+        out[1] = (int)sim.n_ev;
+        sim.store_snapshot(a, i);
+    } else {
+        // on_departure (migration.cpp:212-220) / plan_intra / plan_inter
+        int kind = -1, status = 0;
+        const unsigned w0 = ws->gw[arg];
+        const bool lazy = (sim.lazymask >> wp::popc(w0 & 0x7Fu)) & 1u;
+        if (a.op == SOP_ON_DEPARTURE) {
+            if (a.enabled) {
+                kind = lazy ? 1 : 0;
+                if (lazy) sim.plan_inter(arg);
+                else sim.plan_intra(arg);
+            }
+        } else if (a.op == SOP_PLAN_INTRA) {
+            kind = 0;
+            sim.plan_intra(arg);
+        } else {
+            if (!lazy) {
+                status = 5;  // NotLazy (migration.cpp:127-129)
+            } else {
+                kind = 1;
+                sim.plan_inter(arg);
+            }
+        }
+        out[0] = status;
+        out[1] = kind;
+        out[2] = (int)sim.n_mig;
+        out[3] = (int)sim.n_plan_iter;
+        out[4] = kind == 0 ? sim.max_intra : sim.max_inter;
+        out[5] = (int)sim.n_ev;
+        sim.store_snapshot(a, i);
+    }
+    if (sim.L == 0)
+        for (int k = 0; k < 8; ++k) a.out[(size_t)i * 8 + k] = out[k];
 }
 
 }  // namespace msgk

@@ -13,10 +13,16 @@
 
 namespace msgk {
 
-constexpr int kWarpsPerBlock = 4;
+#ifndef MSG_SIM_WPB
+#define MSG_SIM_WPB 4
+#endif
+constexpr int kWarpsPerBlock = MSG_SIM_WPB;
 
-template <int SPL>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock) sim_kernel(SimArgs a) {
+template <int SPL, bool DETAIL>
+#ifndef MSG_SIM_MINB
+#define MSG_SIM_MINB 8
+#endif
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, MSG_SIM_MINB) sim_kernel(SimArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     DevTables* tb = reinterpret_cast<DevTables*>(smem);
     {
@@ -29,30 +35,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) sim_kernel(SimArgs a) {
     const uint32_t t = blockIdx.x * kWarpsPerBlock + w;
     if (t >= a.n_traces) return;
     WarpSmem<SPL>* ws = reinterpret_cast<WarpSmem<SPL>*>(smem + sizeof(DevTables) + w * sizeof(WarpSmem<SPL>));
-    simulate_trace<SPL>(a, tb, ws, t);
+    simulate_trace<SPL, DETAIL>(a, tb, ws, t);
 }
 
-template <int SPL>
+template <int SPL, bool DETAIL>
 static cudaError_t launch_sim_t(const SimArgs& a, cudaStream_t stream) {
     static_assert(sizeof(DevTables) % 16 == 0, "tables must be 16-byte sized");
     static_assert(sizeof(WarpSmem<SPL>) % 16 == 0, "warp state must be 16-byte sized");
     const size_t smem = sizeof(DevTables) + kWarpsPerBlock * sizeof(WarpSmem<SPL>);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(sim_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(sim_kernel<SPL, DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     const unsigned blocks = (a.n_traces + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return cudaSuccess;
-    sim_kernel<SPL><<<blocks, 32 * kWarpsPerBlock, smem, stream>>>(a);
+    sim_kernel<SPL, DETAIL><<<blocks, 32 * kWarpsPerBlock, smem, stream>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream) {
+    const bool detail = (a.out_flags & (OF_EVENTS | OF_TIMELINE)) != 0;
     switch (spl) {
-        case 1: return launch_sim_t<1>(a, stream);
-        case 2: return launch_sim_t<2>(a, stream);
-        case 4: return launch_sim_t<4>(a, stream);
-        case 8: return launch_sim_t<8>(a, stream);
+        case 1: return detail ? launch_sim_t<1, true>(a, stream) : launch_sim_t<1, false>(a, stream);
+        case 2: return detail ? launch_sim_t<2, true>(a, stream) : launch_sim_t<2, false>(a, stream);
+        case 4: return detail ? launch_sim_t<4, true>(a, stream) : launch_sim_t<4, false>(a, stream);
+        case 8: return detail ? launch_sim_t<8, true>(a, stream) : launch_sim_t<8, false>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -19,6 +19,9 @@
 #include <thread>
 #include <vector>
 
+#include <chrono>
+#include <cstdlib>
+
 #include "dev_types.h"
 #include "host_tables.h"
 #include "staging.h"
@@ -54,11 +57,26 @@ struct msg_staged {
     DevBuf d_queue, d_jobs, d_events, d_timeline, d_summary;
 };
 
+namespace {
+// MSG_PROFILE=1: per-phase host timings of msg_run_batch on stderr.
+struct PhaseTimer {
+    bool on = std::getenv("MSG_PROFILE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[msg] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+}  // namespace
+
 struct msg_batch_result {
     std::vector<msg_trace_summary> summaries;
     std::vector<std::string> messages;
     bool has_jobs = false;
-    std::vector<msg_job_row> jobs;        // all traces, trace-major
+    std::unique_ptr<msg_job_row[]> jobs;  // all traces, trace-major (filled in parallel, no zero-init pass)
+    uint64_t n_jobs_all = 0;
     std::vector<uint64_t> job_off;        // n_traces + 1
     std::vector<std::vector<msg_event>> events;
     std::vector<std::vector<msg_timeline_point>> timeline;
@@ -96,6 +114,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         s->configs.push_back(cs[i].dev);
     }
 
+    PhaseTimer pt;
     // Per-trace validation (parallel), in input order.
     std::vector<TraceCheck> checks(s->n_in);
     for (uint32_t t = 0; t < s->n_in; ++t) {
@@ -115,6 +134,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         checks[t] = check_trace(b, t);
     });
 
+    pt.mark("  validate");
     uint64_t njobs = 0;
     int maxG = 1;
     for (uint32_t t = 0; t < s->n_in; ++t) {
@@ -169,6 +189,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         stage_trace_arrays(b, s->src_of[d], s->traces[d], ha, hs, hp, hid, hperm);
     });
 
+    pt.mark("  stage arrays");
     // Device buffers + H2D.
     cudaStream_t st = eng->stream;
     CK(s->d_arrival.ensure(N * sizeof(double)));
@@ -298,7 +319,8 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
             const bool rows = d >= 0 && s->h_summary.as<DevSummary>()[d].status == MSG_OK;
             res->job_off[t + 1] = res->job_off[t] + (rows ? s->traces[d].n_jobs : 0);
         }
-        res->jobs.resize(res->job_off[s->n_in]);
+        res->n_jobs_all = res->job_off[s->n_in];
+        res->jobs.reset(new msg_job_row[std::max<uint64_t>(res->n_jobs_all, 1)]);
     }
     if (want_ev) res->events.resize(s->n_in);
     if (want_tl) res->timeline.resize(s->n_in);
@@ -344,7 +366,7 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
             return;  // the reference throws: no report, no log
         }
         if (want_jobs) {
-            msg_job_row* rows = res->jobs.data() + res->job_off[t];
+            msg_job_row* rows = res->jobs.get() + res->job_off[t];
             for (uint32_t r = 0; r < tr.n_jobs; ++r) {
                 const JobOut& j = hj[tr.job_off + r];
                 msg_job_row& row = rows[r];
@@ -479,11 +501,19 @@ msg_status msg_run_batch(msg_engine* eng, const msg_trace_batch* batch, const ms
     msg_staged* s = eng->cached;
     s->ev_per_job = 16;
     s->tl_per_job = 8;
+    PhaseTimer pt;
     msg_status st = stage_impl(eng, batch, cfgs, n_cfgs, out_flags, s);
+    pt.mark("stage (validate+H2D)");
     if (st != MSG_OK) return st;
     st = launch_impl(eng, s);
     if (st != MSG_OK) return st;
-    return collect_impl(eng, s, out);
+    if (pt.on) {
+        cudaStreamSynchronize(eng->stream);
+        pt.mark("kernel");
+    }
+    st = collect_impl(eng, s, out);
+    pt.mark("collect (D2H+decode)");
+    return st;
 }
 
 msg_status msg_engine_sync(msg_engine* eng) {
@@ -524,7 +554,7 @@ const msg_job_row* msg_result_jobs(const msg_batch_result* r, uint32_t t, uint64
     if (n) *n = 0;
     if (!r || !r->has_jobs || t + 1 >= r->job_off.size()) return nullptr;
     if (n) *n = r->job_off[t + 1] - r->job_off[t];
-    return r->jobs.data() + r->job_off[t];
+    return r->jobs.get() + r->job_off[t];
 }
 
 const msg_trace_summary* msg_result_summaries(const msg_batch_result* r) {
@@ -536,8 +566,8 @@ const msg_job_row* msg_result_all_jobs(const msg_batch_result* r, const uint64_t
     if (offsets) *offsets = nullptr;
     if (!r || !r->has_jobs) return nullptr;
     if (offsets) *offsets = r->job_off.data();
-    if (n) *n = r->jobs.size();
-    return r->jobs.data();
+    if (n) *n = r->n_jobs_all;
+    return r->jobs.get();
 }
 
 const msg_event* msg_result_events(const msg_batch_result* r, uint32_t t, uint64_t* n) {

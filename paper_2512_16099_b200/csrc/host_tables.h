@@ -90,6 +90,16 @@ inline int build_tables(DevTables* t) {
             t->cost2rank[pc * 256 + bm] = r;
         }
     for (size_t r = 0; r < 32; ++r) t->rank2k[r] = r < distinct.size() ? (uint16_t)distinct[r] : 0xFFFFu;
+    // Feasibility vectors (feasible_from_masks per profile, frag.cpp:18-26) of
+    // every blocked mask, and ideal vectors (ideal_from_masks, :12-16) of
+    // every (popc busy_c, popc busy_m): 32 and 18 distinct values.
+    std::vector<uint32_t> fvecs, ivecs;
+    auto intern = [](std::vector<uint32_t>& v, uint32_t x) {
+        auto it = std::find(v.begin(), v.end(), x);
+        if (it != v.end()) return (int)(it - v.begin());
+        v.push_back(x);
+        return (int)v.size() - 1;
+    };
     for (unsigned km = 0; km < 256; ++km) {
         uint32_t f = 0;
         uint8_t pl = 0;
@@ -98,15 +108,39 @@ inline int build_tables(DevTables* t) {
             f |= (uint32_t)n << (3 * p);
             if (n) pl |= (uint8_t)(1u << p);
         }
-        t->feas[km] = f;
+        t->feasid[km] = (uint8_t)intern(fvecs, f);
         t->placeable[km] = pl;
     }
     for (int pc = 0; pc < 8; ++pc)
         for (int pm = 0; pm < 9; ++pm) {
             uint32_t v = 0;
             for (int p = 0; p < 6; ++p) v |= (uint32_t)std::max(0, host_ideal(pc, pm, p)) << (3 * p);
-            t->ideal[pc * 9 + pm] = v;
+            t->idealid[pc * 9 + pm] = (uint8_t)intern(ivecs, v);
         }
+    if (fvecs.size() > 32 || ivecs.size() > 32) return -3;
+    // 4-mask cost (frag_cost_exact, frag.cpp:60-63) of each (ideal, feasible)
+    // vector pair; doubles are the correctly rounded k/25200, equal to the
+    // reference's Frac::to_double (num/den of the same rational).
+    std::vector<int> k4(32 * 32, 0);
+    for (size_t i = 0; i < ivecs.size(); ++i)
+        for (size_t f = 0; f < fvecs.size(); ++f) {
+            long ratio = 0;
+            int counted = 0;
+            for (int p = 0; p < 6; ++p) {
+                const int ideal = (ivecs[i] >> (3 * p)) & 7, feas = (fvecs[f] >> (3 * p)) & 7;
+                if (ideal == 0) continue;
+                ratio += (long)feas * (420 / ideal);
+                ++counted;
+            }
+            k4[i * 32 + f] = counted ? (int)((420L * counted - ratio) * (60 / counted)) : 0;
+        }
+    std::vector<int> d4 = k4;
+    std::sort(d4.begin(), d4.end());
+    d4.erase(std::unique(d4.begin(), d4.end()), d4.end());
+    if (d4.size() > 256) return -2;
+    for (size_t i = 0; i < k4.size(); ++i)
+        t->cost4pair[i] = (uint8_t)(std::lower_bound(d4.begin(), d4.end(), k4[i]) - d4.begin());
+    for (size_t i = 0; i < 256; ++i) t->cost4val[i] = i < d4.size() ? (double)d4[i] / 25200.0 : 0.0;
     return (int)distinct.size();
 }
 

@@ -4,11 +4,13 @@
 // any size: each GPU is one packed 64-bit state word (busy compute, busy
 // memory, blocked memory, 18 idle-exact placement bits; msg_pack_gpu_word).
 // A block streams a 2048-word chunk of one snapshot with 128-bit loads
-// (8 words per thread), scores every legal start of the job's profile with
-// the 2 KiB cost-rank table in shared memory, reduces packed u64 keys
-// [pass:1|cost rank:5|!reused:1|gpu:32|start:3] with REDUX.MIN (hi, then lo),
-// and merges per snapshot with one 64-bit atomicMin.  Candidate counts feed
-// evaluated_candidates (Lazy pass, Busy pass only when Lazy is empty).
+// (8 words per thread, all loads issued before use), scores every legal
+// start of the job's profile — the profile is block-uniform, so the scoring
+// loop is specialised per profile with compile-time footprints — and keeps
+// a 32-bit block-local key [pass:1|cost rank:5|!reused:1|word:11|start:3]
+// reduced with one REDUX.MIN per warp.  The block's winner becomes a 64-bit
+// global key [pass|rank|!reused|gpu:32|start] merged per snapshot with one
+// atomicMin; candidate counts (Lazy << 16 | Busy) ride one REDUX.ADD.
 //
 // Bound: HBM bandwidth — 8 B per scored GPU.
 #include <cuda_runtime.h>
@@ -20,130 +22,129 @@ namespace msgk {
 
 constexpr int kScoreThreads = 256;
 constexpr int kWordsPerThread = 8;
-constexpr int kChunk = kScoreThreads * kWordsPerThread;  // words per block
+constexpr int kChunk = kScoreThreads * kWordsPerThread;  // words per block (11-bit local index)
 
-__device__ __forceinline__ unsigned s_cs(int p) { return (kCsPack >> (4 * p)) & 0xFu; }
-__device__ __forceinline__ unsigned s_ms(int p) { return (kMsPack >> (4 * p)) & 0xFu; }
-__device__ __forceinline__ unsigned s_count(int p) { return (kCountPack >> (4 * p)) & 0xFu; }
-__device__ __forceinline__ unsigned s_stride(int p) { return (kStridePack >> (4 * p)) & 0xFu; }
-// first idle-exact bit of profile p (placements in profile-table order)
-__device__ __forceinline__ unsigned s_pbase(int p) { return (0xB7420100u >> (4 * p)) & 0xFu; }
-
-struct ScoreCtx {
-    unsigned fm[7], st[7];  // memory footprints and start indexes of the profile's legal starts
-    unsigned n, cs, pbase, lb, dyn, lazymask;
+template <int P>
+struct Prof {
+    static constexpr unsigned cs = (kCsPack >> (4 * P)) & 0xFu;
+    static constexpr unsigned ms = (kMsPack >> (4 * P)) & 0xFu;
+    static constexpr unsigned n = (kCountPack >> (4 * P)) & 0xFu;
+    static constexpr unsigned stride = (kStridePack >> (4 * P)) & 0xFu;
+    static constexpr unsigned pbase = (0x00B74210u >> (4 * P)) & 0xFu;  // first idle-exact bit
+    __host__ __device__ static constexpr unsigned fm(unsigned j) { return ((1u << ms) - 1u) << (j * stride); }
 };
 
-// All legal starts of the job's profile on one GPU word: candidate_starts
-// (scheduler.cpp:19-28: avail, exact-idle when dynamic partitioning is off),
-// post-placement cost rank, reuse flag, Lazy/Busy pass.
-__device__ __forceinline__ void score_word(const ScoreCtx& c, const uint8_t* lut, uint64_t w, uint64_t g,
-                                           uint64_t& best, unsigned& nl, unsigned& nb) {
+struct ScoreCfg {
+    unsigned lb, dyn, lazymask;
+};
+
+// candidate_starts (scheduler.cpp:19-28) of one GPU word, post-placement
+// cost rank, reuse flag and Lazy/Busy pass, folded into the running minimum.
+template <int P>
+__device__ __forceinline__ void score_word(const ScoreCfg& c, const uint8_t* lut, uint64_t w, unsigned local,
+                                           unsigned& best, unsigned& cnt_lb) {
+    using Q = Prof<P>;
     const unsigned lo = (unsigned)w;
     const unsigned bc = lo & 0x7Fu, bm = (lo >> 8) & 0xFFu, km = (lo >> 16) & 0xFFu;
-    const unsigned exact = (unsigned)(w >> 24) >> c.pbase;
+    const unsigned exact = (unsigned)(w >> (24 + Q::pbase));
     const unsigned pc = __popc(bc);
     const unsigned lazy = (c.lazymask >> pc) & 1u;
-    const uint64_t head = c.lb ? (((uint64_t)(lazy ^ 1u) << 41) | (g << 3)) : (g << 3);
-    // popc(busy_c | fc) = pc + cs whenever the start is free
-    const unsigned row = min(pc + c.cs, 7u) * 256u;
+    const unsigned head = c.lb ? (((lazy ^ 1u) << 31) | (local << 3)) : (local << 3);
+    const unsigned row = min(pc + Q::cs, 7u) * 256u;  // popc(busy_c | fc) when the start is free
     unsigned cnt = 0;
 #pragma unroll
-    for (int j = 0; j < 7; ++j) {
-        if ((unsigned)j < c.n) {
-            const unsigned ex = (exact >> j) & 1u;
-            if (!(c.fm[j] & km) && (c.dyn || ex)) {
-                ++cnt;
-                const uint64_t key = c.lb ? (head | ((uint64_t)lut[row + (bm | c.fm[j])] << 36) |
-                                             ((uint64_t)(ex ^ 1u) << 35) | c.st[j])
-                                          : (head | c.st[j]);
-                best = key < best ? key : best;
-            }
+    for (unsigned j = 0; j < Q::n; ++j) {
+        const unsigned ex = (exact >> j) & 1u;
+        if (!(Q::fm(j) & km) && (c.dyn || ex)) {
+            ++cnt;
+            const unsigned key = c.lb ? (head | ((unsigned)lut[row + (bm | Q::fm(j))] << 26) | ((ex ^ 1u) << 25) |
+                                         (j * Q::stride))
+                                      : (head | (j * Q::stride));
+            best = min(best, key);
         }
     }
-    nl += lazy ? cnt : 0u;
-    nb += lazy ? 0u : cnt;
+    cnt_lb += lazy ? cnt << 16 : cnt;
+}
+
+template <int P>
+__device__ __forceinline__ void score_chunk(const ScoreArgs& a, const ScoreCfg& c, const uint8_t* lut,
+                                            const uint64_t* words, uint64_t c0, unsigned& best, unsigned& cnt) {
+    const unsigned t2 = threadIdx.x * 2u;
+    if ((a.G & 1) == 0 && c0 + kChunk <= a.G) {
+        ulonglong2 v[kWordsPerThread / 2];
+#pragma unroll
+        for (int k = 0; k < kWordsPerThread / 2; ++k)
+            v[k] = __ldcs(reinterpret_cast<const ulonglong2*>(words + c0 + t2 + (unsigned)k * 2 * kScoreThreads));
+#pragma unroll
+        for (int k = 0; k < kWordsPerThread / 2; ++k) {
+            const unsigned l = t2 + (unsigned)k * 2 * kScoreThreads;
+            score_word<P>(c, lut, v[k].x, l, best, cnt);
+            score_word<P>(c, lut, v[k].y, l + 1, best, cnt);
+        }
+    } else {
+        for (unsigned l = threadIdx.x; l < kChunk && c0 + l < a.G; l += kScoreThreads)
+            score_word<P>(c, lut, words[c0 + l], l, best, cnt);
+    }
 }
 
 __global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreArgs a) {
     __shared__ __align__(16) uint8_t lut[8 * 256];
-    __shared__ uint64_t wbest[kScoreThreads / 32];
-    __shared__ unsigned wnl[kScoreThreads / 32], wnb[kScoreThreads / 32];
+    __shared__ unsigned wbest[kScoreThreads / 32], wcnt[kScoreThreads / 32];
     for (unsigned i = threadIdx.x; i < 8 * 256 / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(lut)[i] = reinterpret_cast<const uint4*>(a.tables->cost2rank)[i];
     const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
     const uint64_t snap = blockIdx.x / chunks_per;
     const uint64_t c0 = (blockIdx.x % chunks_per) * kChunk;
     const int p = a.profile[snap];
-    ScoreCtx c;
-    c.n = s_count(p);
-    c.cs = s_cs(p);
-    c.pbase = s_pbase(p);
-    c.lb = a.lb;
-    c.dyn = a.dyn;
-    c.lazymask = a.lazymask;
-#pragma unroll
-    for (int j = 0; j < 7; ++j) {
-        const unsigned s = (unsigned)j < c.n ? (unsigned)j * s_stride(p) : 0u;
-        c.st[j] = s;
-        c.fm[j] = (unsigned)j < c.n ? (((1u << s_ms(p)) - 1u) << s) : 0xFFu;
-    }
+    const ScoreCfg c{a.lb, a.dyn, a.lazymask};
     __syncthreads();
     const uint64_t* words = a.words + snap * a.G;
-    uint64_t best = ~0ull;
-    unsigned nl = 0, nb = 0;
-    const uint64_t base = c0 + (uint64_t)threadIdx.x * 2;
-    if ((a.G & 1) == 0 && c0 + kChunk <= a.G) {
-        // full chunk: 4 coalesced 16-byte loads per thread, issued together
-        ulonglong2 v[kWordsPerThread / 2];
-#pragma unroll
-        for (int k = 0; k < kWordsPerThread / 2; ++k)
-            v[k] = __ldcs(reinterpret_cast<const ulonglong2*>(words + base + (uint64_t)k * 2 * kScoreThreads));
-#pragma unroll
-        for (int k = 0; k < kWordsPerThread / 2; ++k) {
-            const uint64_t g = base + (uint64_t)k * 2 * kScoreThreads;
-            score_word(c, lut, v[k].x, g, best, nl, nb);
-            score_word(c, lut, v[k].y, g + 1, best, nl, nb);
-        }
-    } else {
-        for (uint64_t g = c0 + threadIdx.x; g < c0 + kChunk && g < a.G; g += kScoreThreads)
-            score_word(c, lut, words[g], g, best, nl, nb);
+    unsigned best = 0xFFFFFFFFu, cnt = 0;
+    switch (p) {
+        case 0: score_chunk<0>(a, c, lut, words, c0, best, cnt); break;
+        case 1: score_chunk<1>(a, c, lut, words, c0, best, cnt); break;
+        case 2: score_chunk<2>(a, c, lut, words, c0, best, cnt); break;
+        case 3: score_chunk<3>(a, c, lut, words, c0, best, cnt); break;
+        case 4: score_chunk<4>(a, c, lut, words, c0, best, cnt); break;
+        default: score_chunk<5>(a, c, lut, words, c0, best, cnt); break;
     }
-    // warp: u64 min as (hi, lo) REDUX pair; counts by REDUX.ADD
-    const unsigned hi = (unsigned)(best >> 32);
-    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
-    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? (unsigned)best : 0xffffffffu);
-    nl = __reduce_add_sync(0xffffffffu, nl);
-    nb = __reduce_add_sync(0xffffffffu, nb);
+    best = __reduce_min_sync(0xffffffffu, best);
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
     const unsigned w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        wbest[w] = ((uint64_t)mh << 32) | ml;
-        wnl[w] = nl;
-        wnb[w] = nb;
+        wbest[w] = best;
+        wcnt[w] = cnt;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t b = wbest[0];
-        unsigned tl = wnl[0], tb = wnb[0];
-        for (int k = 1; k < kScoreThreads / 32; ++k) {
-            b = wbest[k] < b ? wbest[k] : b;
-            tl += wnl[k];
-            tb += wnb[k];
+    if (threadIdx.x < 32) {
+        const bool v = threadIdx.x < kScoreThreads / 32;
+        const unsigned b = __reduce_min_sync(0xffffffffu, v ? wbest[threadIdx.x] : 0xFFFFFFFFu);
+        const unsigned n = __reduce_add_sync(0xffffffffu, v ? wcnt[threadIdx.x] : 0u);
+        if (threadIdx.x == 0) {
+            if (b != 0xFFFFFFFFu) {
+                // local [pass|rank|!reused|word|start] -> global [pass|rank|!reused|gpu:32|start]
+                const uint64_t gpu = c0 + ((b >> 3) & (kChunk - 1));
+                const uint64_t g64 = ((uint64_t)(b >> 25) << 35) | (gpu << 3) | (b & 7u);
+                atomicMin(reinterpret_cast<unsigned long long*>(a.out + 2 * snap), (unsigned long long)g64);
+            }
+            if (n)
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.out + 2 * snap + 1),
+                          ((unsigned long long)(n >> 16) << 32) | (n & 0xFFFFu));
         }
-        if (b != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(a.out + 2 * snap), (unsigned long long)b);
-        if (tl | tb)
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.out + 2 * snap + 1),
-                      ((unsigned long long)tl << 32) | tb);
+    }
+}
+
+__global__ void score_init_kernel(uint64_t* out, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        out[2 * i] = ~0ull;  // no candidate yet
+        out[2 * i + 1] = 0;  // (lazy << 32 | busy) candidate counts
     }
 }
 
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     if (!a.n || !a.G) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(a.out, 0, 16 * (size_t)a.n, stream);
-    if (e != cudaSuccess) return e;
-    // keys start at ~0 (no candidate); counts at 0
-    e = cudaMemset2DAsync(a.out, 16, 0xFF, 8, a.n, stream);
-    if (e != cudaSuccess) return e;
+    score_init_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(a.out, a.n);
     const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
     const uint64_t blocks = chunks_per * a.n;
     if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;

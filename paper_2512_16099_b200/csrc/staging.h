@@ -270,4 +270,125 @@ inline void decode_event(const EventRec& r, const int64_t* ids, double overlap, 
     out->present = pr;
 }
 
+// ---- decision-level snapshots (host_decide.cpp) ---------------------------
+inline int placement_index(int p, int s) {  // idle-exact bit (profile-table order)
+    static const int base[6] = {0, 1, 2, 4, 7, 11};
+    const int stride = (kStridePack >> (4 * p)) & 0xF;
+    return base[p] + s / stride;
+}
+
+inline uint32_t lazymask_of(double threshold) {
+    uint32_t m = 0;
+    for (int pc = 0; pc <= 7; ++pc)
+        if ((double)pc / 7.0 < threshold) m |= 1u << pc;
+    return m;
+}
+
+// A snapshot must be representable as the reference's GpuState: valid
+// (profile, start) per instance, pairwise slice-disjoint (gpu.cpp:146-156).
+inline msg_status check_gpu(const msg_instance* s8, std::string* err) {
+    unsigned used = 0;
+    for (int s = 0; s < 8; ++s) {
+        const msg_instance& x = s8[s];
+        if (x.state == MSG_SLOT_EMPTY) continue;
+        if (x.state > MSG_SLOT_DRAINING) {
+            *err = "InvalidArgument: bad slot state";
+            return MSG_ERR_INVALID_ARGUMENT;
+        }
+        if (x.profile < 0 || x.profile >= MSG_PROFILE_COUNT) {
+            *err = "UnknownProfile: snapshot instance with an unknown profile";
+            return MSG_ERR_UNKNOWN_PROFILE;
+        }
+        if (!((host_startmask(x.profile) >> s) & 1u)) {
+            *err = "InvalidPlacement: instance at an illegal start";
+            return MSG_ERR_INVALID_PLACEMENT;
+        }
+        if (host_fpm(x.profile, s) & used) {
+            *err = "SlicesBusy: overlapping instances in a snapshot";
+            return MSG_ERR_SLICES_BUSY;
+        }
+        used |= host_fpm(x.profile, s);
+    }
+    return MSG_OK;
+}
+
+inline uint32_t to_st(uint8_t state) {
+    return state == MSG_SLOT_IDLE ? ST_IDLE : state == MSG_SLOT_BUSY ? ST_RUN : state == MSG_SLOT_DRAINING ? ST_DRAIN
+                                                                                                          : ST_EMPTY;
+}
+
+struct Staged {
+    std::vector<uint32_t> words;
+    std::vector<int32_t> jobs;
+    std::vector<std::vector<int64_t>> ids;  // per snapshot: rank -> job id
+};
+
+// Slot words + per-snapshot job ranks (dense, id order) over the busy jobs and
+// any extra ids (queued requests).
+inline msg_status stage_snapshots(uint32_t n, int G, const msg_instance* slots, const uint64_t* qoff, const int64_t* qjob,
+                           Staged* st, std::string* err) {
+    const size_t per = (size_t)G * 8;
+    st->words.resize(n * per);
+    st->jobs.resize(n * per);
+    st->ids.assign(n, {});
+    for (uint32_t i = 0; i < n; ++i) {
+        const msg_instance* sn = slots + i * per;
+        for (int g = 0; g < G; ++g) {
+            msg_status e = check_gpu(sn + g * 8, err);
+            if (e != MSG_OK) return e;
+        }
+        std::vector<int64_t>& ids = st->ids[i];
+        for (size_t k = 0; k < per; ++k)
+            if (sn[k].state == MSG_SLOT_BUSY) ids.push_back(sn[k].job);
+        if (qoff)
+            for (uint64_t k = qoff[i]; k < qoff[i + 1]; ++k) ids.push_back(qjob[k]);
+        std::sort(ids.begin(), ids.end());
+        if (std::adjacent_find(ids.begin(), ids.end()) != ids.end()) {
+            *err = "InvalidArgument: a job id appears twice in one snapshot";
+            return MSG_ERR_INVALID_ARGUMENT;
+        }
+        if (ids.size() >= (1u << 22)) {
+            *err = "Unsupported: too many jobs in one snapshot";
+            return MSG_ERR_UNSUPPORTED;
+        }
+        for (size_t k = 0; k < per; ++k) {
+            const msg_instance& x = sn[k];
+            st->words[i * per + k] = to_st(x.state) | ((uint32_t)(x.state ? x.profile : 0) << 4) | (x.seq << 8);
+            st->jobs[i * per + k] =
+                x.state == MSG_SLOT_BUSY
+                    ? (int32_t)(std::lower_bound(ids.begin(), ids.end(), x.job) - ids.begin())
+                    : -1;
+        }
+    }
+    return MSG_OK;
+}
+
+// Write the kernel's slot words back as msg_instance, renumbering `seq`
+// densely per GPU in creation order.
+inline void unstage_snapshots(uint32_t n, int G, const std::vector<uint32_t>& w, const std::vector<int32_t>& j,
+                       const Staged& st, msg_instance* slots) {
+    const size_t per = (size_t)G * 8;
+    for (uint32_t i = 0; i < n; ++i)
+        for (int g = 0; g < G; ++g) {
+            const size_t b = i * per + g * 8;
+            int order[8], m = 0;
+            for (int s = 0; s < 8; ++s)
+                if ((w[b + s] & 0xF) != ST_EMPTY) order[m++] = s;
+            for (int x = 1; x < m; ++x)  // insertion sort by creation sequence
+                for (int y = x; y > 0 && (w[b + order[y]] >> 8) < (w[b + order[y - 1]] >> 8); --y)
+                    std::swap(order[y], order[y - 1]);
+            for (int s = 0; s < 8; ++s) slots[b + s] = msg_instance{-1, 0, -1, MSG_SLOT_EMPTY, 0};
+            for (int r = 0; r < m; ++r) {
+                const int s = order[r];
+                const uint32_t v = w[b + s];
+                const uint32_t stt = v & 0xF;
+                msg_instance& o = slots[b + s];
+                o.seq = (uint32_t)r;
+                o.profile = (int8_t)((v >> 4) & 0xF);
+                o.state = stt == ST_IDLE ? MSG_SLOT_IDLE : stt == ST_DRAIN ? MSG_SLOT_DRAINING : MSG_SLOT_BUSY;
+                o.job = (o.state == MSG_SLOT_BUSY && j[b + s] >= 0) ? st.ids[i][j[b + s]] : -1;
+            }
+        }
+}
+
 }  // namespace msgk

@@ -16,7 +16,7 @@ from . import abi
 from .model import ConfigPack, MigschedError, SimConfig, TraceBatch, WorkloadSpec
 from .results import TraceResult
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmigsched_b200.so")
+LIB_PATH = os.environ.get("MSG_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmigsched_b200.so")
 
 _lib = None
 
@@ -99,10 +99,7 @@ class Staged:
     def collect(self) -> list:
         r = C.c_void_p()
         _check(lib().msg_collect(self.engine._h, self._h, C.byref(r)), self.engine)
-        try:
-            return _decode(r, self.out_flags)
-        finally:
-            lib().msg_result_free(r)
+        return _decode(r, self.out_flags)
 
     @property
     def handler_events(self) -> int:
@@ -164,10 +161,7 @@ class Engine:
         r = C.c_void_p()
         _check(lib().msg_run_batch(self._h, C.addressof(batch._c), C.addressof(pack.c[0]), len(pack),
                                    out_flags, C.byref(r)), self)
-        try:
-            return _decode(r, out_flags)
-        finally:
-            lib().msg_result_free(r)
+        return _decode(r, out_flags)
 
     def stage(self, batch: TraceBatch, cfgs: Sequence[SimConfig], out_flags: int = 0) -> Staged:
         pack = ConfigPack(cfgs)
@@ -177,42 +171,66 @@ class Engine:
         return Staged(self, h, batch.n_traces, (batch, pack), out_flags)
 
 
+class _ResultHolder:
+    """Owns a msg_batch_result; numpy views into it keep this object alive."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().msg_result_free(self.handle)
+        except Exception:
+            pass
+
+
+class _Mem:
+    """Array-interface wrapper over library memory that pins its owner."""
+
+    def __init__(self, ptr, nbytes, owner):
+        self.__array_interface__ = {"data": (ptr, False), "shape": (nbytes,), "typestr": "|u1", "version": 3}
+        self.owner = owner
+
+
+def _view(ptr, n, dtype, owner):
+    """Zero-copy numpy view of n records at ptr, keeping `owner` alive."""
+    if not ptr or n == 0:
+        return np.zeros(0, dtype)
+    return np.asarray(_Mem(ptr, n * dtype.itemsize, owner)).view(dtype)
+
+
 def _decode(r, flags: int) -> list:
+    """Decode a msg_batch_result; per-job rows and events are zero-copy views
+    into the library's result buffers (freed when the last view dies)."""
     L = lib()
+    owner = _ResultHolder(r)
     out = []
     n = L.msg_result_n_traces(r)
     cnt = C.c_uint64()
     if n == 0:
         return out
-    # bulk: summaries and job rows in two copies
-    summaries = np.frombuffer(C.string_at(L.msg_result_summaries(r), n * abi.SUMMARY_DTYPE.itemsize),
-                              abi.SUMMARY_DTYPE).copy()
+    summaries = _view(L.msg_result_summaries(r), n, abi.SUMMARY_DTYPE, owner)
     offp = C.POINTER(C.c_uint64)()
     jp = L.msg_result_all_jobs(r, C.byref(offp), C.byref(cnt))
     jobs_all = offs = None
     if jp:
-        jobs_all = np.frombuffer(C.string_at(jp, cnt.value * abi.JOB_DTYPE.itemsize), abi.JOB_DTYPE).copy()
+        jobs_all = _view(jp, cnt.value, abi.JOB_DTYPE, owner)
         offs = np.ctypeslib.as_array(offp, shape=(n + 1,)).copy()
-    with_events = bool(flags & abi.OUT_EVENTS)
-    with_tl = bool(flags & abi.OUT_TIMELINE)
+    status = summaries["status"]
     for t in range(n):
-        summary = summaries[t]
-        st = int(summary["status"])
+        st = int(status[t])
         msg = L.msg_result_message(r, t).decode() if st != 0 else ""
         jobs = jobs_all[offs[t]:offs[t + 1]] if jobs_all is not None else None
-        out.append(TraceResult(st, msg, summary, jobs, None, None))
-    if not (with_events or with_tl):
-        return out
-    for t in range(n):
-
-        def arr(fn, dtype):
-            p = fn(r, t, C.byref(cnt))
-            if not p or cnt.value == 0:
-                return None if not p else np.zeros(0, dtype)
-            return np.frombuffer(C.string_at(p, cnt.value * dtype.itemsize), dtype).copy()
-
-        out[t].events = arr(L.msg_result_events, abi.EVENT_DTYPE)
-        out[t].frag_timeline = arr(L.msg_result_timeline, abi.TIMELINE_DTYPE)
+        out.append(TraceResult(st, msg, summaries[t], jobs, None, None))
+    if flags & (abi.OUT_EVENTS | abi.OUT_TIMELINE):
+        for t in range(n):
+            if flags & abi.OUT_EVENTS:
+                p = L.msg_result_events(r, t, C.byref(cnt))
+                out[t].events = _view(p, cnt.value, abi.EVENT_DTYPE, owner)
+            if flags & abi.OUT_TIMELINE:
+                p = L.msg_result_timeline(r, t, C.byref(cnt))
+                out[t].frag_timeline = _view(p, cnt.value, abi.TIMELINE_DTYPE, owner)
     return out
 
 

@@ -167,3 +167,64 @@ const msg_timeline_point* emu_result_timeline(void* h, uint64_t* n) {
 void emu_result_free(void* h) { delete static_cast<EmuResult*>(h); }
 
 }  // extern "C"
+
+namespace {
+template <int SPL>
+void run_snap_warp(const SnapArgs& a, const DevTables* tb, uint32_t i) {
+    auto ws = std::make_unique<WarpSmem<SPL>>();
+    std::memset(ws.get(), 0xA5, sizeof(WarpSmem<SPL>));
+    wp::EmuWarp warp;
+    std::vector<std::thread> lanes;
+    for (unsigned l = 0; l < 32; ++l)
+        lanes.emplace_back([&, l]() {
+            wp::g_warp = &warp;
+            wp::g_lane = l;
+            wp::g_phase = 0;
+            snapshot_op<SPL>(a, tb, ws.get(), i);
+        });
+    for (auto& t : lanes) t.join();
+}
+}  // namespace
+
+extern "C" {
+// Decision-level snapshot op (decide.cu body) on the host emulation:
+// op = SOP_*, slots updated in place (plans), out = n x 8 ints, events =
+// n x ev_cap records.  Returns 0 or a staging status.
+int emu_snapshot(int32_t op, uint32_t n, int32_t G, msg_instance* slots, const int32_t* arg, double threshold,
+                 int32_t lb, int32_t dyn, int32_t enabled, double overlap, int32_t* out, EventRec* events,
+                 uint32_t ev_cap) {
+    Staged st;
+    std::string err;
+    msg_status e = stage_snapshots(n, G, slots, nullptr, nullptr, &st, &err);
+    if (e != MSG_OK) return e;
+    DevTables tables;
+    build_tables(&tables);
+    std::vector<uint32_t> wout(st.words.size());
+    std::vector<int32_t> jout(st.jobs.size());
+    SnapArgs a{};
+    a.tables = &tables;
+    a.slot_in = st.words.data();
+    a.job_in = st.jobs.data();
+    a.slot_out = wout.data();
+    a.job_out = jout.data();
+    a.arg = arg;
+    a.out = out;
+    a.events = events;
+    a.ev_cap = ev_cap;
+    a.n = n;
+    a.G = G;
+    a.op = op;
+    a.cflags = (lb ? CF_LB : 0u) | (dyn ? CF_DYN : 0u);
+    a.lazymask = lazymask_of(threshold);
+    a.overlap = overlap;
+    a.enabled = enabled;
+    for (uint32_t i = 0; i < n; ++i) {
+        if (G <= 4) run_snap_warp<1>(a, &tables, i);
+        else if (G <= 8) run_snap_warp<2>(a, &tables, i);
+        else if (G <= 16) run_snap_warp<4>(a, &tables, i);
+        else run_snap_warp<8>(a, &tables, i);
+    }
+    if (op > SOP_DISPATCH) unstage_snapshots(n, G, wout, jout, st, slots);
+    return 0;
+}
+}
