@@ -120,12 +120,16 @@ def profile_traffic(name):
 
 
 def workload(rank):
+    """This rank's shard of the C2 ensemble (weak scaling: TRACES_RUN seeds per
+    rank, paper_2512_16099_b200.ensemble.rank_seeds)."""
     from paper_2512_16099_b200.engine import generate_batch
+    from paper_2512_16099_b200.ensemble import rank_seeds
     from paper_2512_16099_b200.model import SimConfig, preset
 
     spec = preset("normal25")
     spec.job_count = JOBS
-    return generate_batch(spec, rank * 1_000_000, TRACES_RUN), SimConfig(gpu_count=GPUS_PER_CLUSTER)
+    seed0, n = rank_seeds(rank, TRACES_RUN)
+    return generate_batch(spec, seed0, n), SimConfig(gpu_count=GPUS_PER_CLUSTER)
 
 
 def cpu_baseline(batch, cfg, target_s=8.0):
