@@ -75,7 +75,6 @@ struct WarpSmem {
     static constexpr int NS = 32 * SPL;  // slots
     static constexpr int NG = 4 * SPL;   // GPUs
     double rem[NS];    // RunJob::remaining_work (WAIT: service demand)
-    double last[NS];   // RunJob::last_update
     double tkey[NS];   // timer time of the slot
     double gcost[NG];  // frag_cost(gpu) for the timeline (4-mask form)
     int32_t job[NS];   // bound job rank (RUN/WAIT) or migrating job (DRAIN)
@@ -139,6 +138,12 @@ struct TraceSim {
     bool snap_mode;
     double tl_sum, tl_mean;
     bool tl_dirty;
+    // RunJob::last_update of EVERY running job equals the time of the last
+    // handler: advance_all stamps all of them, start_service stamps `now`,
+    // moves carry it (sim.cpp:153-165,212-218).  So dt is warp-uniform.
+    double t_prev;
+    double my_f;     // lanes 0..6: slowdown(L+1) = 1 + alpha*L
+    double inv_g;    // 1/G when G is a power of two (then x/G == x*inv_g exactly)
 
     // ---------------------------------------------------------------- tables
     MSG_DI unsigned rank2(unsigned bc, unsigned bm) const {
@@ -200,6 +205,7 @@ struct TraceSim {
         alpha = c.alpha;
         overlap = c.overlap;
         latency = c.latency;
+        init_factors();
         now = 0.0;
         a_idx = 0;
         q_head = q_tail = 0;
@@ -254,6 +260,7 @@ struct TraceSim {
         alpha = 0.0;
         overlap = a.overlap;
         latency = 0.0;
+        init_factors();
         N = 0;
         a_idx = 0;
         now = 0.0;
@@ -365,20 +372,28 @@ struct TraceSim {
         return wp::dadd(1.0, wp::dmul(alpha, (double)((int)k - 1)));
     }
 
-    // advance_all (sim.cpp:153-165)
+    MSG_DI void init_factors() {
+        my_f = factor(L < 7 ? L + 1u : 1u);
+        inv_g = ((G & (G - 1)) == 0) ? 1.0 / (double)G : 0.0;
+        t_prev = 0.0;
+    }
+
+    // advance_all (sim.cpp:153-165): rem -= dt / slowdown(k) for every running
+    // job.  dt is uniform (see t_prev), so the <= 7 distinct quotients are
+    // computed once, lane k-1 holding dt / slowdown(k), and fetched by shuffle.
     MSG_DI void advance_all() {
+        const double dt = wp::dsub(now, t_prev);
+        t_prev = now;
+        if (!(dt > 0.0)) return;  // dt <= 0: last_update = now only
+        const double q = wp::ddiv(dt, my_f);
         wp::sync();
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
-            if (sm->st[slot] == ST_RUN) {
-                const double dt = wp::dsub(now, sm->last[slot]);
-                if (dt > 0.0) {
-                    const double f = factor(w_k(sm->gw[slot >> 3]));
-                    sm->rem[slot] = wp::dsub(sm->rem[slot], wp::ddiv(dt, f));
-                }
-                sm->last[slot] = now;
-            }
+            const bool run = sm->st[slot] == ST_RUN;
+            const unsigned k = run ? w_k(sm->gw[slot >> 3]) : 1u;
+            const double qk = wp::shfl(q, (int)k - 1);
+            if (run) sm->rem[slot] = wp::dsub(sm->rem[slot], qk);
         }
     }
 
@@ -388,8 +403,10 @@ struct TraceSim {
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
-            if (sm->st[slot] == ST_RUN) {
-                const double f = factor(w_k(sm->gw[slot >> 3]));
+            const bool run = sm->st[slot] == ST_RUN;
+            const unsigned k = run ? w_k(sm->gw[slot >> 3]) : 1u;
+            const double f = wp::shfl(my_f, (int)k - 1);
+            if (run) {
                 double r = sm->rem[slot];
                 if (r < 0.0) r = 0.0;  // std::max(rem, 0.0)
                 sm->tkey[slot] = wp::dadd(now, wp::dmul(r, f));
@@ -403,7 +420,7 @@ struct TraceSim {
             wp::sync();
             double tot = 0.0;
             for (int g = 0; g < G; ++g) tot = wp::dadd(tot, sm->gcost[g]);
-            tl_mean = wp::ddiv(tot, (double)G);
+            tl_mean = inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
             tl_dirty = false;
         }
         if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && L == 0) {
@@ -603,13 +620,8 @@ struct TraceSim {
             sm->job[slot] = r;
             sm->mig[slot] = 0;
             sm->rem[slot] = sv;
-            if (delay > 0.0) {
-                sm->st[slot] = ST_WAIT;
-                sm->tkey[slot] = ss;
-            } else {
-                sm->st[slot] = ST_RUN;
-                sm->last[slot] = now;
-            }
+            sm->st[slot] = delay > 0.0 ? ST_WAIT : ST_RUN;  // WAIT: ServiceStart timer at ss
+            sm->tkey[slot] = ss;
             jobs[r].sched = ss;
         }
         refresh_gpu(g);
@@ -654,7 +666,7 @@ struct TraceSim {
         const int q = sm->prof[from_slot];
         const int32_t r = sm->job[from_slot];
         const uint8_t jst = sm->st[from_slot];
-        const double jrem = sm->rem[from_slot], jlast = sm->last[from_slot], jtk = sm->tkey[from_slot];
+        const double jrem = sm->rem[from_slot], jtk = sm->tkey[from_slot];
         const unsigned jmig = sm->mig[from_slot];
         const unsigned fcb = k2w(sm->gw[fg]);
         const unsigned tcb = k2w(sm->gw[tg]);
@@ -667,7 +679,6 @@ struct TraceSim {
             sm->job[dst] = r;
             sm->mig[dst] = (uint16_t)(jmig + 1u);
             sm->rem[dst] = jrem;
-            sm->last[dst] = jlast;
             sm->tkey[dst] = jtk;
             if (overlap <= 0.0) {
                 sm->st[from_slot] = ST_IDLE;  // finish_draining at once
@@ -854,7 +865,6 @@ struct TraceSim {
         wp::sync();
         if (L == 0) {
             sm->st[slot] = ST_RUN;  // start_service: rem already holds service_s
-            sm->last[slot] = now;
         }
         refresh_gpu(slot >> 3);
     }

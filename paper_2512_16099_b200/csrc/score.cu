@@ -3,17 +3,19 @@
 // schedule() / first_fit_schedule() (scheduler.cpp:47-98) for snapshots of
 // any size: each GPU is one packed 64-bit state word (busy compute, busy
 // memory, blocked memory, 18 idle-exact placement bits; msg_pack_gpu_word).
-// A block streams a 2048-word chunk of one snapshot with 128-bit loads
-// (8 words per thread, all loads issued before use), scores every legal
+// A persistent grid streams 1024-word chunks of the snapshots with 128-bit
+// loads (4 words per thread, issued before use), scores every legal
 // start of the job's profile — the profile is block-uniform, so the scoring
 // loop is specialised per profile with compile-time footprints — and keeps
 // a 32-bit block-local key [pass:1|cost rank:5|!reused:1|word:11|start:3]
-// reduced with one REDUX.MIN per warp.  The block's winner becomes a 64-bit
+// reduced with one REDUX.MIN per warp.  Each warp's winner becomes a 64-bit
 // global key [pass|rank|!reused|gpu:32|start] merged per snapshot with one
 // atomicMin; candidate counts (Lazy << 16 | Busy) ride one REDUX.ADD.
 //
 // Bound: HBM bandwidth — 8 B per scored GPU.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "decide.h"
 #include "dev_types.h"
@@ -21,8 +23,8 @@
 namespace msgk {
 
 constexpr int kScoreThreads = 256;
-constexpr int kWordsPerThread = 8;
-constexpr int kChunk = kScoreThreads * kWordsPerThread;  // words per block (11-bit local index)
+constexpr int kWordsPerThread = 4;
+constexpr int kChunk = kScoreThreads * kWordsPerThread;  // words per chunk (<= 2048: 11-bit local index)
 
 template <int P>
 struct Prof {
@@ -66,9 +68,15 @@ __device__ __forceinline__ void score_word(const ScoreCfg& c, const uint8_t* lut
     cnt_lb += lazy ? cnt << 16 : cnt;
 }
 
+// One chunk of one snapshot: every thread scores kWordsPerThread words,
+// loaded up front with 128-bit evict-first loads; the warp's winner and
+// candidate counts go straight to the snapshot's slots with one 64-bit
+// atomicMin / atomicAdd (no block-level synchronisation).
 template <int P>
 __device__ __forceinline__ void score_chunk(const ScoreArgs& a, const ScoreCfg& c, const uint8_t* lut,
-                                            const uint64_t* words, uint64_t c0, unsigned& best, unsigned& cnt) {
+                                            uint64_t snap, uint64_t c0) {
+    const uint64_t* words = a.words + snap * a.G;
+    unsigned best = 0xFFFFFFFFu, cnt = 0;
     const unsigned t2 = threadIdx.x * 2u;
     if ((a.G & 1) == 0 && c0 + kChunk <= a.G) {
         ulonglong2 v[kWordsPerThread / 2];
@@ -85,51 +93,41 @@ __device__ __forceinline__ void score_chunk(const ScoreArgs& a, const ScoreCfg& 
         for (unsigned l = threadIdx.x; l < kChunk && c0 + l < a.G; l += kScoreThreads)
             score_word<P>(c, lut, words[c0 + l], l, best, cnt);
     }
-}
-
-__global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreArgs a) {
-    __shared__ __align__(16) uint8_t lut[8 * 256];
-    __shared__ unsigned wbest[kScoreThreads / 32], wcnt[kScoreThreads / 32];
-    for (unsigned i = threadIdx.x; i < 8 * 256 / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(lut)[i] = reinterpret_cast<const uint4*>(a.tables->cost2rank)[i];
-    const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
-    const uint64_t snap = blockIdx.x / chunks_per;
-    const uint64_t c0 = (blockIdx.x % chunks_per) * kChunk;
-    const int p = a.profile[snap];
-    const ScoreCfg c{a.lb, a.dyn, a.lazymask};
-    __syncthreads();
-    const uint64_t* words = a.words + snap * a.G;
-    unsigned best = 0xFFFFFFFFu, cnt = 0;
-    switch (p) {
-        case 0: score_chunk<0>(a, c, lut, words, c0, best, cnt); break;
-        case 1: score_chunk<1>(a, c, lut, words, c0, best, cnt); break;
-        case 2: score_chunk<2>(a, c, lut, words, c0, best, cnt); break;
-        case 3: score_chunk<3>(a, c, lut, words, c0, best, cnt); break;
-        case 4: score_chunk<4>(a, c, lut, words, c0, best, cnt); break;
-        default: score_chunk<5>(a, c, lut, words, c0, best, cnt); break;
-    }
     best = __reduce_min_sync(0xffffffffu, best);
     cnt = __reduce_add_sync(0xffffffffu, cnt);
-    const unsigned w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        wbest[w] = best;
-        wcnt[w] = cnt;
+        if (best != 0xFFFFFFFFu) {
+            // local [pass|rank|!reused|word|start] -> global [pass|rank|!reused|gpu:32|start]
+            const uint64_t gpu = c0 + ((best >> 3) & (kChunk - 1));
+            const uint64_t g64 = ((uint64_t)(best >> 25) << 35) | (gpu << 3) | (best & 7u);
+            atomicMin(reinterpret_cast<unsigned long long*>(a.out + 2 * snap), (unsigned long long)g64);
+        }
+        if (cnt)
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.out + 2 * snap + 1),
+                      ((unsigned long long)(cnt >> 16) << 32) | (cnt & 0xFFFFu));
     }
+}
+
+// Persistent grid: each block walks chunks blockIdx.x, +gridDim.x, ...; the
+// cost-rank table is staged into shared memory once per block.
+__global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreArgs a) {
+    __shared__ __align__(16) uint8_t lut[8 * 256];
+    for (unsigned i = threadIdx.x; i < 8 * 256 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(lut)[i] = reinterpret_cast<const uint4*>(a.tables->cost2rank)[i];
     __syncthreads();
-    if (threadIdx.x < 32) {
-        const bool v = threadIdx.x < kScoreThreads / 32;
-        const unsigned b = __reduce_min_sync(0xffffffffu, v ? wbest[threadIdx.x] : 0xFFFFFFFFu);
-        const unsigned n = __reduce_add_sync(0xffffffffu, v ? wcnt[threadIdx.x] : 0u);
-        if (threadIdx.x == 0) {
-            if (b != 0xFFFFFFFFu) {
-                // local [pass|rank|!reused|word|start] -> global [pass|rank|!reused|gpu:32|start]
-                const uint64_t gpu = c0 + ((b >> 3) & (kChunk - 1));
-                const uint64_t g64 = ((uint64_t)(b >> 25) << 35) | (gpu << 3) | (b & 7u);
-                atomicMin(reinterpret_cast<unsigned long long*>(a.out + 2 * snap), (unsigned long long)g64);
-            }
-            if (n)
-                atomicAdd(reinterpret_cast<unsigned long long*>(a.out + 2 * snap + 1),
-                          ((unsigned long long)(n >> 16) << 32) | (n & 0xFFFFu));
+    const ScoreCfg c{a.lb, a.dyn, a.lazymask};
+    const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
+    const uint64_t total = chunks_per * a.n;
+    for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
+        const uint64_t snap = ch / chunks_per;
+        const uint64_t c0 = (ch % chunks_per) * kChunk;
+        switch (a.profile[snap]) {
+            case 0: score_chunk<0>(a, c, lut, snap, c0); break;
+            case 1: score_chunk<1>(a, c, lut, snap, c0); break;
+            case 2: score_chunk<2>(a, c, lut, snap, c0); break;
+            case 3: score_chunk<3>(a, c, lut, snap, c0); break;
+            case 4: score_chunk<4>(a, c, lut, snap, c0); break;
+            default: score_chunk<5>(a, c, lut, snap, c0); break;
         }
     }
 }
@@ -145,9 +143,14 @@ __global__ void score_init_kernel(uint64_t* out, uint32_t n) {
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     if (!a.n || !a.G) return cudaSuccess;
     score_init_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(a.out, a.n);
-    const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
-    const uint64_t blocks = chunks_per * a.n;
-    if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const uint64_t chunks = ((a.G + kChunk - 1) / kChunk) * a.n;
+    const uint64_t blocks = std::min<uint64_t>(chunks, (uint64_t)sms * 8);  // 8 x 256 threads per SM
     score_kernel<<<(unsigned)blocks, kScoreThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
