@@ -1,0 +1,859 @@
+// cluster_core.cuh — the event loop for LARGE clusters (G > 32 GPUs, up to
+// the 16384-GPU C4 configuration): one thread block replays one trace of the
+// reference's discrete-event scheduler (proj/src/sim.cpp:71-410).
+//
+// Same semantics and the same packed-key decisions as the warp engine
+// (engine_core.cuh), with the state moved to global memory (L2-resident:
+// ~64 B per (GPU, start) slot) and block-wide reductions:
+//   * the 8 slots of GPU g are slots 8g..8g+7 of the trace's cluster arena;
+//     per GPU a mask word (busy compute | busy memory | blocked memory |
+//     running count), the idle-exact placement bits and the 4-mask cost id;
+//   * an ACTIVE list holds the slots that carry a timer (running, waiting
+//     for service start, draining), so next-event search, advance_all and
+//     reschedule scan ~R entries, not 8G slots;
+//   * GPU-local steps (create_instance, refresh of a GPU word) run on one
+//     thread; plan_intra on warp 0; schedule, plan_inter and the next-event
+//     search are block-wide argmins over packed keys: per-warp REDUX chain,
+//     then one __syncthreads and the same chain over the 32 warp winners.
+// Bit-exact with the reference, except the fragmentation timeline above
+// kExactTimelineGpus GPUs: there the per-sample mean is
+// RN(RN(sum_g k_g / 25200) / G) from the exact integer sum of the per-GPU
+// cost numerators instead of the reference's sequential double sum (relative
+// difference <= G * 2^-53, i.e. < 2e-12 at 16384 GPUs; SURVEY §7 hard part 6).
+#pragma once
+#include "engine_core.cuh"
+
+namespace msgk {
+
+constexpr int kExactTimelineGpus = 512;
+
+struct BlockScratch {
+    unsigned hi[2][32], lo[2][32], tie[2][32], ms[2][32];
+    int pay[2][32];
+    unsigned sum[2][32];
+    double q[8];       // dt / slowdown(k), k = 1..7
+    double f[8];       // slowdown(k)
+    unsigned u[8];     // small broadcasts from one thread / warp 0
+    int dl_slot[8];    // create_instance: destroyed starts in creation order
+    int dl_prof[8];
+    unsigned long long ksum;  // sum of per-GPU 4-mask cost numerators
+    double tl;
+};
+
+template <bool DETAIL>
+struct ClusterSim {
+    BlockScratch* sc;
+    const DevTables* tb;
+    // arena views of this trace
+    uint8_t* st;
+    uint8_t* prof;
+    uint16_t* mig;
+    uint32_t* cseq;
+    int32_t* job;
+    uint32_t* mseq;
+    double* rem;
+    double* tkey;
+    int32_t* apos;
+    int32_t* act;
+    uint32_t* gw;
+    uint32_t* gx;
+    uint8_t* gcid;
+    const double* arr;
+    const double* svc;
+    const uint8_t* prf;
+    const uint32_t* perm;
+    int32_t* queue;
+    JobOut* jobs;
+    EventRec* evs;
+    double* tl;
+    uint32_t N, ev_cap, tl_cap, oflags;
+    int G;
+    uint32_t cflags, lazymask;
+    double alpha, overlap, latency, inv_g;
+    // block-uniform state (every thread holds the same values)
+    unsigned T, W, L, w;  // thread, warp, lane, warps
+    int bph;              // scratch double-buffer parity
+    double now, t_prev;
+    uint32_t a_idx, a_rank;
+    int a_prof;
+    double a_t, a_svc;
+    uint32_t q_head, q_tail, n_act;
+    uint32_t cseq_ctr, mseq_ctr;
+    uint32_t n_ev, n_handler, n_tl, n_mig, n_reconf, n_enq, n_deq;
+    int max_arr, max_intra, max_inter;
+    double tl_sum, tl_mean;
+    bool tl_dirty;
+
+    // ------------------------------------------------------------- tables
+    MSG_DI unsigned rank2(unsigned bc, unsigned bm) const { return tb->cost2rank[wp::popc(bc) * 256 + bm]; }
+    MSG_DI unsigned k2w(unsigned wd) const { return tb->rank2k[rank2(w_bc(wd), w_bm(wd))]; }
+    MSG_DI static unsigned pidx(int p, int s) {  // idle-exact bit of placement (p, s)
+        return ((0x00B74210u >> (4 * p)) & 0xFu) + (unsigned)s / stride_of(p);
+    }
+
+    // ----------------------------------------------------- block reductions
+    // Lexicographic (hi, lo, tie, ms) minimum within the warp; every lane
+    // ends with the winning tuple and its payload.
+    MSG_DI void warp_lexmin(unsigned& hi, unsigned& lo, unsigned& tie, unsigned& ms, int& pay) {
+        const unsigned mhi = wp::rmin(hi);
+        const unsigned mlo = wp::rmin(hi == mhi ? lo : NONE);
+        const unsigned mtie = wp::rmin((hi == mhi && lo == mlo) ? tie : NONE);
+        const bool m3 = hi == mhi && lo == mlo && tie == mtie;
+        const unsigned mms = wp::rmin(m3 ? ms : NONE);
+        const int wl = wp::ffs(wp::ballot(m3 && ms == mms)) - 1;
+        pay = wp::shfl(pay, wl < 0 ? 0 : wl);
+        hi = mhi;
+        lo = mlo;
+        tie = mtie;
+        ms = mms;
+    }
+    // ... and over the whole block (one __syncthreads).
+    MSG_DI void block_lexmin(unsigned& hi, unsigned& lo, unsigned& tie, unsigned& ms, int& pay) {
+        warp_lexmin(hi, lo, tie, ms, pay);
+        if (L == 0) {
+            sc->hi[bph][W] = hi;
+            sc->lo[bph][W] = lo;
+            sc->tie[bph][W] = tie;
+            sc->ms[bph][W] = ms;
+            sc->pay[bph][W] = pay;
+        }
+        wp::bsync();
+        const bool v = L < w;
+        hi = v ? sc->hi[bph][L] : NONE;
+        lo = v ? sc->lo[bph][L] : NONE;
+        tie = v ? sc->tie[bph][L] : NONE;
+        ms = v ? sc->ms[bph][L] : NONE;
+        pay = v ? sc->pay[bph][L] : -1;
+        warp_lexmin(hi, lo, tie, ms, pay);
+        bph ^= 1;
+    }
+    MSG_DI unsigned block_sum(unsigned x) {
+        x = wp::radd(x);
+        if (L == 0) sc->sum[bph][W] = x;
+        wp::bsync();
+        x = wp::radd(L < w ? sc->sum[bph][L] : 0u);
+        bph ^= 1;
+        return x;
+    }
+
+    // --------------------------------------------------------------- events
+    MSG_DI void emit(uint8_t kind, int32_t jb, unsigned gpu, unsigned gpu2, unsigned pr, unsigned start,
+                     unsigned start2, unsigned flags, uint64_t aux) {
+        if (DETAIL && (oflags & OF_EVENTS) && n_ev < ev_cap && T == 0) {
+            EventRec r;
+            r.t = now;
+            r.aux = aux;
+            r.job = jb;
+            r.gpu = (uint16_t)gpu;
+            r.gpu2 = (uint16_t)gpu2;
+            r.kind = kind;
+            r.profile = (uint8_t)pr;
+            r.start = (uint8_t)start;
+            r.start2 = (uint8_t)start2;
+            r.flags = (uint8_t)flags;
+            r.pad[0] = r.pad[1] = r.pad[2] = 0;
+            evs[n_ev] = r;
+        }
+        ++n_ev;
+    }
+
+    // ---------------------------------------------------------------- setup
+    MSG_DI void setup(const SimArgs& a, const DevTables* tables, BlockScratch* scratch, uint32_t t) {
+        T = wp::tid();
+        L = wp::lane();
+        W = T >> 5;
+        w = wp::nthreads() >> 5;
+        bph = 0;
+        sc = scratch;
+        tb = tables;
+        const DevTrace tr = a.traces[t];
+        const DevConfig c = a.configs[tr.cfg];
+        G = c.G;
+        const uint64_t go = tr.cl_goff, so = 8 * go;
+        st = a.c_st + so;
+        prof = a.c_prof + so;
+        mig = a.c_mig + so;
+        cseq = a.c_cseq + so;
+        job = a.c_job + so;
+        mseq = a.c_mseq + so;
+        rem = a.c_rem + so;
+        tkey = a.c_tkey + so;
+        apos = a.c_apos + so;
+        act = a.c_act + so;
+        gw = a.c_gw + go;
+        gx = a.c_gx + go;
+        gcid = a.c_gcid + go;
+        N = tr.n_jobs;
+        arr = a.arrival + tr.job_off;
+        svc = a.service + tr.job_off;
+        prf = a.profile + tr.job_off;
+        perm = tr.has_perm ? a.perm + tr.job_off : nullptr;
+        queue = a.queue + tr.job_off;
+        jobs = a.jobs + tr.job_off;
+        evs = a.events ? a.events + tr.ev_off : nullptr;
+        tl = a.timeline ? a.timeline + 2 * tr.tl_off : nullptr;
+        ev_cap = tr.ev_cap;
+        tl_cap = tr.tl_cap;
+        oflags = a.out_flags;
+        if (!evs) oflags &= ~OF_EVENTS;
+        if (!tl) oflags &= ~OF_TIMELINE;
+        cflags = c.flags;
+        lazymask = c.lazymask;
+        alpha = c.alpha;
+        overlap = c.overlap;
+        latency = c.latency;
+        inv_g = ((G & (G - 1)) == 0) ? 1.0 / (double)G : 0.0;
+        now = t_prev = 0.0;
+        a_idx = 0;
+        q_head = q_tail = 0;
+        n_act = 0;
+        mseq_ctr = 0;
+        n_ev = n_handler = n_tl = n_mig = n_reconf = n_enq = n_deq = 0;
+        max_arr = max_intra = max_inter = 0;
+        tl_sum = tl_mean = 0.0;
+        tl_dirty = true;
+        const unsigned nt = wp::nthreads();
+        for (uint64_t i = T; i < 8ull * G; i += nt) {
+            st[i] = ST_EMPTY;
+            mig[i] = 0;
+            apos[i] = -1;
+        }
+        // empty GPU: masks 0, cost id of frag 0 (every profile fully feasible)
+        const uint8_t empty_id = tb->cost4pair[tb->idealid[0] * 32u + tb->feasid[0]];
+        for (uint64_t g = T; g < (uint64_t)G; g += nt) {
+            gw[g] = 0;
+            gx[g] = 0;
+            gcid[g] = empty_id;
+        }
+        if (T < 7) sc->f[T] = wp::dadd(1.0, wp::dmul(alpha, (double)(int)T));  // slowdown(T+1)
+        if (T == 0) sc->ksum = (unsigned long long)tb->cost4k[empty_id] * (unsigned long long)G;
+        wp::bsync();
+        // static layout (sim.cpp:86-95)
+        if (T == 0) {
+            for (uint32_t k = 0; k < c.n_init; ++k) {
+                const uint32_t v = a.init_slots[c.init_off + k];
+                const int slot = (int)(v & 0xFFFFFFu);
+                st[slot] = ST_IDLE;
+                prof[slot] = (uint8_t)(v >> 24);
+                cseq[slot] = k;
+            }
+            for (uint32_t k = 0; k < c.n_init; ++k) refresh_gpu((int)((a.init_slots[c.init_off + k] & 0xFFFFFFu) >> 3));
+        }
+        cseq_ctr = c.n_init;
+        load_arrival();
+        wp::bsync();
+    }
+
+    MSG_DI void load_arrival() {
+        if (a_idx < N) {
+            const uint32_t r = perm ? perm[a_idx] : a_idx;
+            a_rank = r;
+            a_t = arr[r];
+            a_prof = prf[r];
+            a_svc = svc[r];
+        }
+    }
+
+    // ------------------------------------------- GPU words (single thread)
+    // busy/blocked masks (gpu.cpp:10-48), running count, idle-exact
+    // placements, 4-mask cost id; keeps the integer cost total current.
+    MSG_DI void refresh_gpu(int g) {
+        unsigned bc = 0, bm = 0, km = 0, k = 0, x = 0;
+        for (int s = 0; s < 8; ++s) {
+            const uint8_t v = st[8 * g + s];
+            if (v == ST_EMPTY) continue;
+            const int p = prof[8 * g + s];
+            const unsigned m = fpm(p, s);
+            if (v == ST_IDLE) {
+                x |= 1u << pidx(p, s);
+            } else if (v == ST_DRAIN) {
+                km |= m;
+            } else {
+                bc |= fpc(p, s);
+                bm |= m;
+                km |= m;
+                k += v == ST_RUN;
+            }
+        }
+        const unsigned word = bc | (bm << 8) | (km << 16) | (k << 24);
+        gw[g] = word;
+        gx[g] = x;
+        const unsigned row = (unsigned)wp::popc(bc) * 9u + (unsigned)wp::popc(bm);
+        const uint8_t id = tb->cost4pair[tb->idealid[row] * 32u + tb->feasid[km]];
+        sc->ksum += (unsigned long long)tb->cost4k[id] - (unsigned long long)tb->cost4k[gcid[g]];
+        gcid[g] = id;
+    }
+
+    // active list (single thread): slots carrying a timer
+    MSG_DI void act_add(int slot) {
+        act[n_act] = slot;
+        apos[slot] = (int32_t)n_act;
+    }
+    MSG_DI void act_remove(int slot, uint32_t n) {  // n = list size before removal
+        const int i = apos[slot];
+        const int last = act[n - 1];
+        act[i] = last;
+        apos[last] = i;
+        apos[slot] = -1;
+    }
+
+    // ---------------------------------------------------- contention model
+    MSG_DI void advance_all() {  // sim.cpp:153-165 (uniform dt, see engine_core.cuh)
+        const double dt = wp::dsub(now, t_prev);
+        t_prev = now;
+        if (!(dt > 0.0)) return;
+        if (T < 7) sc->q[T] = wp::ddiv(dt, sc->f[T]);
+        wp::bsync();
+        for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
+            const int slot = act[i];
+            if (st[slot] == ST_RUN) rem[slot] = wp::dsub(rem[slot], sc->q[w_k(gw[slot >> 3]) - 1]);
+        }
+        wp::bsync();
+    }
+
+    MSG_DI void reschedule() {  // sim.cpp:167-175
+        wp::bsync();
+        for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
+            const int slot = act[i];
+            if (st[slot] == ST_RUN) {
+                double r = rem[slot];
+                if (r < 0.0) r = 0.0;
+                tkey[slot] = wp::dadd(now, wp::dmul(r, sc->f[w_k(gw[slot >> 3]) - 1]));
+            }
+        }
+        wp::bsync();
+    }
+
+    MSG_DI void sample() {  // sim.cpp:177-181
+        if (tl_dirty) {
+            wp::bsync();
+            if (T == 0) {
+                if (G <= kExactTimelineGpus) {
+                    double tot = 0.0;
+                    for (int g = 0; g < G; ++g) tot = wp::dadd(tot, tb->cost4val[gcid[g]]);
+                    sc->tl = inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
+                } else {
+                    const double tot = wp::ddiv((double)sc->ksum, 25200.0);
+                    sc->tl = inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
+                }
+            }
+            wp::bsync();
+            tl_mean = sc->tl;
+            tl_dirty = false;
+        }
+        if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && T == 0) {
+            tl[2 * n_tl] = now;
+            tl[2 * n_tl + 1] = tl_mean;
+        }
+        ++n_tl;
+        tl_sum = wp::dadd(tl_sum, tl_mean);
+    }
+
+    // --------------------------------------------------------- next event
+    MSG_DI int next_event(int& ev_slot) {
+        wp::bsync();
+        unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
+        int bsl = -1;
+        for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
+            const int slot = act[i];
+            const uint8_t s = st[slot];
+            const uint64_t tk = time_key(tkey[slot]);
+            const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;
+            const unsigned kind = s == ST_RUN ? 0u : (s == ST_DRAIN ? 1u : 2u);
+            const unsigned tie = (kind << 28) | (unsigned)job[slot];
+            const unsigned ms = s == ST_DRAIN ? mseq[slot] : 0u;
+            const bool better =
+                hi < bhi || (hi == bhi && (lo < blo || (lo == blo && (tie < btie || (tie == btie && ms < bms)))));
+            if (better) {
+                bhi = hi;
+                blo = lo;
+                btie = tie;
+                bms = ms;
+                bsl = slot;
+            }
+        }
+        block_lexmin(bhi, blo, btie, bms, bsl);
+        const bool have_arrival = a_idx < N;
+        if (bhi == NONE) {
+            if (!have_arrival) return -1;
+            now = a_t;
+            return 3;
+        }
+        if (have_arrival && time_key(a_t) < (((uint64_t)bhi << 32) | blo)) {
+            now = a_t;
+            return 3;
+        }
+        ev_slot = bsl;
+        now = tkey[bsl];
+        return (int)(btie >> 28);
+    }
+
+    // ------------------------------------------------------------ schedule
+    MSG_DI Decision dispatch(int p) {  // scheduler.cpp:47-104
+        wp::bsync();
+        Decision d;
+        const unsigned smask = startmask_of(p);
+        const unsigned n = count_of(p), stride = stride_of(p);
+        const unsigned pb = pidx(p, 0);
+        const bool dyn = (cflags & CF_DYN) != 0;
+        const bool lb = (cflags & CF_LB) != 0;
+        (void)smask;
+        uint64_t kmin = ~0ull;
+        unsigned nl = 0, nb = 0;
+        for (uint64_t g = T; g < (uint64_t)G; g += wp::nthreads()) {
+            const unsigned wd = gw[g];
+            const unsigned ex = gx[g] >> pb;
+            const unsigned lazy = (lazymask >> wp::popc(w_bc(wd))) & 1u;
+            for (unsigned j = 0; j < n; ++j) {
+                const int s = (int)(j * stride);
+                const bool exact = (ex >> j) & 1u;
+                if ((dyn || exact) && !(fpm(p, s) & w_km(wd))) {
+                    uint64_t key;
+                    if (lb) {
+                        const unsigned rk = rank2(w_bc(wd) | fpc(p, s), w_bm(wd) | fpm(p, s));
+                        key = ((uint64_t)(lazy ^ 1u) << 47) | ((uint64_t)rk << 42) | ((uint64_t)(exact ? 0u : 1u) << 41) |
+                              (g << 3) | (uint64_t)s;
+                        nl += lazy;
+                        nb += lazy ^ 1u;
+                    } else {
+                        key = (g << 3) | (uint64_t)s;
+                    }
+                    kmin = key < kmin ? key : kmin;
+                }
+            }
+        }
+        unsigned hi = (unsigned)(kmin >> 32), lo = (unsigned)kmin, z0 = 0, z1 = 0;
+        int pay = 0;
+        block_lexmin(hi, lo, z0, z1, pay);
+        const unsigned NL = block_sum(nl), NB = block_sum(nb);
+        const uint64_t k = ((uint64_t)hi << 32) | lo;
+        d.placed = k != ~0ull;
+        d.evals = lb ? NL + (NL == 0 ? NB : 0u) : 0u;
+        d.g = (int)((k >> 3) & 0x3FFFFFFFFull);
+        d.s = (int)(k & 7u);
+        d.reused = false;
+        if (d.placed) {
+            if (lb) d.reused = ((k >> 41) & 1u) == 0;
+            else d.reused = (gx[d.g] >> pidx(p, d.s)) & 1u;
+        }
+        return d;
+    }
+
+    // ---------------------------------------------------- create_instance
+    // gpu.cpp:71-101 on one thread; destroyed instances are listed in
+    // creation order for the Reconfig events.
+    MSG_DI CreateRes create(int g, int p, int s) {
+        wp::bsync();
+        if (T == 0) {
+            const int b = 8 * g;
+            const bool reused = st[b + s] == ST_IDLE && prof[b + s] == p;
+            unsigned dmask = 0;
+            int nd = 0;
+            if (!reused) {
+                for (int t = 0; t < 8; ++t) {
+                    if (st[b + t] == ST_IDLE && (fpm(prof[b + t], t) & fpm(p, s))) {
+                        dmask |= 1u << t;
+                        // insertion by creation sequence
+                        int i = nd++;
+                        while (i > 0 && cseq[b + sc->dl_slot[i - 1]] > cseq[b + t]) {
+                            sc->dl_slot[i] = sc->dl_slot[i - 1];
+                            sc->dl_prof[i] = sc->dl_prof[i - 1];
+                            --i;
+                        }
+                        sc->dl_slot[i] = t;
+                        sc->dl_prof[i] = prof[b + t];
+                    }
+                }
+                for (int t = 0; t < 8; ++t)
+                    if ((dmask >> t) & 1u) st[b + t] = ST_EMPTY;
+                prof[b + s] = (uint8_t)p;
+                cseq[b + s] = cseq_ctr;
+            }
+            st[b + s] = ST_RUN;  // placeholder, the caller binds the job
+            sc->u[0] = reused;
+            sc->u[1] = dmask;
+        }
+        wp::bsync();
+        CreateRes cr;
+        cr.reused = sc->u[0] != 0;
+        cr.dmask = sc->u[1];
+        cr.dprof = 0;
+        cr.dseq = 0;
+        if (!cr.reused) ++cseq_ctr;
+        wp::bsync();
+        return cr;
+    }
+
+    MSG_DI void emit_reconfig(int g, int p, int s, const CreateRes& cr) {
+        const int nd = wp::popc(cr.dmask);
+        for (int i = 0; i < nd; ++i) {
+            emit(EV_RECONFIG, -1, (unsigned)g, 0, (unsigned)sc->dl_prof[i], (unsigned)sc->dl_slot[i], 0, EF_DESTROY, 0);
+            ++n_reconf;
+        }
+        if (!cr.reused) {
+            emit(EV_RECONFIG, -1, (unsigned)g, 0, (unsigned)p, (unsigned)s, 0, 0, 0);
+            ++n_reconf;
+        }
+    }
+
+    MSG_DI double apply_placement(int g, int s, int32_t r, double sv, unsigned nops) {  // sim.cpp:199-218
+        const double delay = wp::dmul((double)nops, latency);
+        const double ss = wp::dadd(now, delay);
+        const int slot = 8 * g + s;
+        if (T == 0) {
+            job[slot] = r;
+            mig[slot] = 0;
+            rem[slot] = sv;
+            st[slot] = delay > 0.0 ? ST_WAIT : ST_RUN;
+            tkey[slot] = ss;
+            jobs[r].sched = ss;
+            act_add(slot);
+            refresh_gpu(g);
+        }
+        ++n_act;
+        tl_dirty = true;
+        wp::bsync();
+        return ss;
+    }
+
+    MSG_DI void place(const Decision& d, int32_t r, int p, double sv, uint8_t kind) {
+        const CreateRes cr = create(d.g, p, d.s);
+        const unsigned nops = (unsigned)wp::popc(cr.dmask) + (cr.reused ? 0u : 1u);
+        const double ss = apply_placement(d.g, d.s, r, sv, nops);
+        emit(kind, r, (unsigned)d.g, 0, (unsigned)p, (unsigned)d.s, 0, EF_PLACED | (cr.reused ? EF_REUSED : 0),
+             wp::dbits(ss));
+        emit_reconfig(d.g, p, d.s, cr);
+    }
+
+    MSG_DI void dequeue_pass() {  // sim.cpp:325-344
+        while (q_head < q_tail) {
+            wp::bsync();
+            const int32_t h = queue[q_head];
+            const int p = prf[h];
+            const double sv = svc[h];
+            const Decision d = dispatch(p);
+            if (!d.placed) break;
+            max_arr = max_arr > (int)d.evals ? max_arr : (int)d.evals;
+            ++q_head;
+            place(d, h, p, sv, EV_DEQUEUE);
+            ++n_deq;
+        }
+    }
+
+    // ------------------------------------------------------------ migration
+    MSG_DI void apply_move(int from_slot, int tg, int ts, bool inter) {  // migration.cpp:35-69
+        wp::bsync();
+        const int fg = from_slot >> 3, fs = from_slot & 7;
+        const int q = prof[from_slot];
+        const int32_t r = job[from_slot];
+        const uint8_t jst = st[from_slot];
+        const double jrem = rem[from_slot], jtk = tkey[from_slot];
+        const unsigned jmig = mig[from_slot];
+        const unsigned fcb = k2w(gw[fg]), tcb = k2w(gw[tg]);
+        wp::bsync();
+        if (T == 0) st[from_slot] = ST_DRAIN;  // start_draining
+        const CreateRes cr = create(tg, q, ts);
+        if (T == 0) {
+            const int dst = 8 * tg + ts;
+            st[dst] = jst;
+            job[dst] = r;
+            mig[dst] = (uint16_t)(jmig + 1u);
+            rem[dst] = jrem;
+            tkey[dst] = jtk;
+            act_add(dst);
+            if (overlap <= 0.0) {
+                st[from_slot] = ST_IDLE;
+                act_remove(from_slot, n_act + 1);
+            } else {
+                tkey[from_slot] = wp::dadd(now, overlap);
+                mseq[from_slot] = mseq_ctr;
+            }
+            refresh_gpu(fg);
+            if (tg != fg) refresh_gpu(tg);
+        }
+        if (overlap > 0.0) {
+            ++mseq_ctr;
+            ++n_act;
+        }
+        tl_dirty = true;
+        wp::bsync();
+        const unsigned fca = k2w(gw[fg]), tca = k2w(gw[tg]);
+        const uint64_t costs = (uint64_t)fcb | ((uint64_t)fca << 16) | ((uint64_t)tcb << 32) | ((uint64_t)tca << 48);
+        emit(EV_MIGRATION_START, r, (unsigned)fg, (unsigned)tg, (unsigned)q, (unsigned)fs, (unsigned)ts,
+             inter ? EF_INTER : 0, costs);
+        ++n_mig;
+        emit_reconfig(tg, q, ts, cr);
+        if (overlap <= 0.0) emit(EV_MIGRATION_END, r, (unsigned)fg, 0, 0, 0, 0, 0, 0);
+    }
+
+    MSG_DI void plan_intra(int g) {  // migration.cpp:71-123, on warp 0
+        for (;;) {
+            wp::bsync();
+            const unsigned wd = gw[g];
+            const unsigned bc = w_bc(wd), bm = w_bm(wd), km = w_km(wd);
+            const unsigned cur = rank2(bc, bm);
+            if (W == 0) {
+                const int own = (int)(L & 7u);
+                const int sl = 8 * g + own;
+                const uint8_t s = st[sl];
+                unsigned kmin = NONE, cnt = 0;
+                if (s == ST_RUN || s == ST_WAIT) {
+                    const int q = prof[sl];
+                    const unsigned r = (unsigned)job[sl];
+                    const unsigned ofc = fpc(q, own), ofm = fpm(q, own);
+                    const unsigned n = count_of(q), stride = stride_of(q);
+                    for (int h = 0; h < 2; ++h) {
+                        const unsigned j = (L >> 3) + 4u * (unsigned)h;
+                        if (j < n) {
+                            const int t = (int)(j * stride);
+                            if (t != own && !(fpm(q, t) & km)) {
+                                const unsigned rk = rank2((bc & ~ofc) | fpc(q, t), (bm & ~ofm) | fpm(q, t));
+                                const unsigned key = (rk << 27) | (r << 3) | (unsigned)t;
+                                kmin = key < kmin ? key : kmin;
+                                ++cnt;
+                            }
+                        }
+                    }
+                }
+                const unsigned best = wp::rmin(kmin);
+                const unsigned evals = wp::radd(cnt);
+                const int wl = wp::ffs(wp::ballot(kmin == best)) - 1;
+                if (L == 0) {
+                    sc->u[2] = best;
+                    sc->u[3] = evals;
+                    sc->u[4] = (unsigned)(wl & 7);
+                }
+            }
+            wp::bsync();
+            const unsigned best = sc->u[2];
+            const int evals = (int)sc->u[3];
+            const int from = (int)sc->u[4];
+            max_intra = max_intra > evals ? max_intra : evals;
+            wp::bsync();
+            if (best == NONE || (best >> 27) >= cur) break;
+            apply_move(8 * g + from, g, (int)(best & 7u), false);
+        }
+    }
+
+    MSG_DI void plan_inter(int g0) {  // migration.cpp:125-210
+        for (;;) {
+            wp::bsync();
+            const unsigned w0 = gw[g0];
+            const unsigned lazy_cs = (unsigned)wp::popc(w_bc(w0));
+            const unsigned km0 = w_km(w0);
+            const unsigned pl = tb->placeable[km0];
+            unsigned bhi = NONE, blo = NONE, z0 = 0, z1 = 0, cnt = 0;
+            int bsl = -1;
+            for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
+                const int slot = act[i];
+                const int g = slot >> 3, s = slot & 7;
+                const uint8_t v = st[slot];
+                if (g != g0 && (v == ST_RUN || v == ST_WAIT)) {
+                    const unsigned wd = gw[g];
+                    const unsigned src_cs = (unsigned)wp::popc(w_bc(wd));
+                    const int q = prof[slot];
+                    const unsigned cs = cs_of(q);
+                    if (!((lazymask >> src_cs) & 1u) && lazy_cs + cs < src_cs - cs && ((pl >> q) & 1u)) {
+                        const unsigned rk = rank2(w_bc(wd) & ~fpc(q, s), w_bm(wd) & ~fpm(q, s));
+                        // key (cost, gpu, job id): rank:5 | gpu:35 | job:24
+                        const uint64_t key = ((uint64_t)rk << 59) | ((uint64_t)g << 24) | (uint64_t)job[slot];
+                        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+                        if (hi < bhi || (hi == bhi && lo < blo)) {
+                            bhi = hi;
+                            blo = lo;
+                            bsl = slot;
+                        }
+                        ++cnt;
+                    }
+                }
+            }
+            block_lexmin(bhi, blo, z0, z1, bsl);
+            int evals = (int)block_sum(cnt);
+            if (bhi == NONE) {
+                max_inter = max_inter > evals ? max_inter : evals;
+                break;
+            }
+            const int from_slot = bsl;
+            const int q = prof[from_slot];
+            if (W == 0) {  // destination: minimum (cost, start) on g0, lane = start
+                const bool cand = L < 8 && ((startmask_of(q) >> L) & 1u) && !(fpm(q, (int)L) & km0);
+                const unsigned dk =
+                    cand ? ((rank2(w_bc(w0) | fpc(q, (int)L), w_bm(w0) | fpm(q, (int)L)) << 3) | L) : NONE;
+                const unsigned dbest = wp::rmin(dk);
+                const unsigned dcnt = wp::radd(cand ? 1u : 0u);
+                if (L == 0) {
+                    sc->u[5] = dbest;
+                    sc->u[6] = dcnt;
+                }
+            }
+            wp::bsync();
+            const unsigned dbest = sc->u[5];
+            evals += (int)sc->u[6];
+            max_inter = max_inter > evals ? max_inter : evals;
+            apply_move(from_slot, g0, (int)(dbest & 7u), true);
+        }
+    }
+
+    MSG_DI void on_departure(int g) {  // migration.cpp:212-220
+        wp::bsync();
+        if ((lazymask >> wp::popc(w_bc(gw[g]))) & 1u) plan_inter(g);
+        else plan_intra(g);
+    }
+
+    // ------------------------------------------------------------ handlers
+    MSG_DI void handle_arrival() {
+        const int32_t r = (int32_t)a_rank;
+        const int p = a_prof;
+        const double sv = a_svc;
+        ++a_idx;
+        load_arrival();
+        bool enq = q_head < q_tail;
+        if (!enq) {
+            const Decision d = dispatch(p);
+            max_arr = max_arr > (int)d.evals ? max_arr : (int)d.evals;
+            if (d.placed) place(d, r, p, sv, EV_ARRIVAL);
+            else enq = true;
+        }
+        if (enq) {
+            emit(EV_ARRIVAL, r, 0, 0, (unsigned)p, 0, 0, 0, 0);
+            if (T == 0) queue[q_tail] = r;
+            ++q_tail;
+            emit(EV_ENQUEUE, r, 0, 0, 0, 0, 0, 0, 0);
+            ++n_enq;
+        }
+    }
+
+    MSG_DI void handle_departure(int slot, bool completion) {
+        wp::bsync();
+        const int g = slot >> 3;
+        const int32_t r = job[slot];
+        const int m = mig[slot];
+        wp::bsync();
+        if (T == 0) {
+            st[slot] = ST_IDLE;
+            act_remove(slot, n_act);
+            if (completion) {
+                jobs[r].done = now;
+                jobs[r].gpu = g;
+                jobs[r].mig = m;
+            }
+            refresh_gpu(g);
+        }
+        --n_act;
+        tl_dirty = true;
+        wp::bsync();
+        emit(completion ? EV_COMPLETION : EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
+        if (completion) sample();
+        const int passes = (completion && (cflags & CF_MIG)) ? 2 : 1;
+        for (int pass = 0; pass < passes; ++pass) {
+            if (pass) on_departure(g);
+            dequeue_pass();
+        }
+    }
+
+    MSG_DI void handle_service_start(int slot) {
+        wp::bsync();
+        if (T == 0) {
+            st[slot] = ST_RUN;
+            refresh_gpu(slot >> 3);
+        }
+        tl_dirty = true;
+        wp::bsync();
+    }
+
+    MSG_DI void run() {
+        for (;;) {
+            int slot = -1;
+            const int kind = next_event(slot);
+            if (kind < 0) break;
+            ++n_handler;
+            advance_all();
+            if (kind == 3) handle_arrival();
+            else if (kind == 2) handle_service_start(slot);
+            else handle_departure(slot, kind == 0);
+            reschedule();
+            sample();
+        }
+    }
+
+    MSG_DI void finish(DevSummary* out) {  // metrics (sim.cpp:414-502), warp 0
+        wp::bsync();
+        DevSummary s;
+        s.status = q_head < q_tail ? STATUS_JOBS_PENDING : STATUS_OK;
+        s.reserved = 0;
+        s.pending_rank = -1;
+        if (s.status != STATUS_OK) {
+            unsigned mn = NONE;
+            for (uint32_t i = q_head + T; i < q_tail; i += wp::nthreads()) {
+                const unsigned r = (unsigned)queue[i];
+                mn = r < mn ? r : mn;
+            }
+            unsigned z0 = 0, z1 = 0, z2 = 0;
+            int pay = 0;
+            block_lexmin(mn, z0, z1, z2, pay);
+            s.pending_rank = (int32_t)mn;
+        }
+        if (W != 0) return;
+        double sw = 0.0, se = 0.0, stt = 0.0, first = 0.0, lastc = 0.0;
+        if (s.status == STATUS_OK) {
+            for (uint32_t base = 0; base < N; base += 32) {
+                const uint32_t j = base + L;
+                double wv = 0.0, e = 0.0, t = 0.0, a = 0.0, dn = 0.0;
+                if (j < N) {
+                    a = arr[j];
+                    const double sc0 = jobs[j].sched;
+                    dn = jobs[j].done;
+                    wv = wp::dsub(sc0, a);
+                    e = wp::dsub(dn, sc0);
+                    t = wp::dadd(wv, e);
+                }
+                const uint32_t n = N - base < 32 ? N - base : 32;
+                for (uint32_t k = 0; k < n; ++k) {
+                    const double wk = wp::shfl(wv, (int)k), ek = wp::shfl(e, (int)k), tk = wp::shfl(t, (int)k);
+                    const double ak = wp::shfl(a, (int)k), dk = wp::shfl(dn, (int)k);
+                    sw = wp::dadd(sw, wk);
+                    se = wp::dadd(se, ek);
+                    stt = wp::dadd(stt, tk);
+                    if (base + k == 0) {
+                        first = ak;
+                        lastc = dk;
+                    } else {
+                        first = ak < first ? ak : first;
+                        lastc = lastc < dk ? dk : lastc;
+                    }
+                }
+            }
+        }
+        if (N > 0 && s.status == STATUS_OK) {
+            const double n = (double)N;
+            s.mean_wait = wp::ddiv(sw, n);
+            s.mean_exec = wp::ddiv(se, n);
+            s.mean_turn = wp::ddiv(stt, n);
+            s.makespan = wp::dsub(lastc, first);
+        } else {
+            s.mean_wait = s.mean_exec = s.mean_turn = s.makespan = 0.0;
+        }
+        s.handler_events = n_handler;
+        s.n_events = n_ev;
+        s.timeline_samples = n_tl;
+        s.migrations = n_mig;
+        s.reconfig_ops = n_reconf;
+        s.enqueues = n_enq;
+        s.dequeues = n_deq;
+        s.max_arr = max_arr;
+        s.max_intra = max_intra;
+        s.max_inter = max_inter;
+        s.tl_sum = tl_sum;
+        if (L == 0) *out = s;
+    }
+};
+
+template <bool DETAIL>
+MSG_DI void simulate_large_trace(const SimArgs& a, const DevTables* tables, BlockScratch* sc, uint32_t t) {
+    ClusterSim<DETAIL> sim;
+    sim.setup(a, tables, sc, t);
+    sim.run();
+    sim.finish(a.summary + t);
+}
+
+}  // namespace msgk

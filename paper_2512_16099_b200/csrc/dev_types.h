@@ -37,7 +37,7 @@ struct DevConfig {
     uint32_t reserved;
 };
 
-// Packed static-layout instance: slot | profile << 16 (creation order = array order).
+// Packed static-layout instance: slot | profile << 24 (creation order = array order).
 struct DevTrace {
     uint64_t job_off;   // first job (rank order) in the batch arrays
     uint64_t ev_off;    // first event record
@@ -47,7 +47,8 @@ struct DevTrace {
     uint32_t ev_cap;
     uint32_t tl_cap;
     uint32_t has_perm;  // arrival order differs from rank order
-    uint32_t reserved;
+    uint32_t large;     // G > 32: simulated by the block engine (cluster_core.cuh)
+    uint64_t cl_goff;   // block engine: first GPU of this trace in the cluster arena
 };
 
 // Fixed 32-byte event record written by the kernel (decoded on the host into
@@ -101,6 +102,7 @@ struct DevSummary {
 struct DevTables {
     uint8_t cost2rank[8 * 256];  // [popc(busy_c)][busy_m] -> rank of the 2-mask cost
     double cost4val[256];        // 4-mask cost id -> frag_cost as double (k / 25200.0)
+    uint16_t cost4k[256];        // 4-mask cost id -> numerator k over 25200
     uint16_t rank2k[32];         // cost rank -> numerator over 25200
     uint8_t placeable[256];      // blocked_m -> profiles with >= 1 free legal start
     uint8_t feasid[256];         // blocked_m -> id of its per-profile feasible-count vector
@@ -125,6 +127,24 @@ struct SimArgs {
     DevSummary* summary;
     uint32_t n_traces;
     uint32_t out_flags;
+    // block engine (G > 32): cluster arena, indexed by GPU (cl_goff + g) or
+    // slot (8 * (cl_goff + g) + s), and the list of large traces
+    const uint32_t* large_idx;
+    uint32_t n_large;
+    uint32_t reserved;
+    uint8_t* c_st;
+    uint8_t* c_prof;
+    uint16_t* c_mig;
+    uint32_t* c_cseq;
+    int32_t* c_job;
+    uint32_t* c_mseq;
+    double* c_rem;
+    double* c_tkey;
+    int32_t* c_apos;
+    int32_t* c_act;
+    uint32_t* c_gw;
+    uint32_t* c_gx;
+    uint8_t* c_gcid;
 };
 
 // Decision-level kernel arguments (decide.cu): one warp per cluster snapshot

@@ -233,9 +233,9 @@ struct TraceSim {
         if (L == 0) {
             for (uint32_t k = 0; k < c.n_init; ++k) {
                 const uint32_t v = a.init_slots[c.init_off + k];
-                const int slot = (int)(v & 0xFFFFu);
+                const int slot = (int)(v & 0xFFFFFFu);
                 sm->st[slot] = ST_IDLE;
-                sm->prof[slot] = (uint8_t)(v >> 16);
+                sm->prof[slot] = (uint8_t)(v >> 24);
                 sm->cseq[slot] = k;
             }
         }

@@ -8,6 +8,7 @@
 // The host side (host_runtime.cpp) calls the launch_* wrappers below.
 #include <cuda_runtime.h>
 
+#include "cluster_core.cuh"
 #include "engine_core.cuh"
 #include "kernels.h"
 
@@ -33,7 +34,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MSG_SIM_MINB) sim_kernel(
     __syncthreads();
     const unsigned w = threadIdx.x >> 5;
     const uint32_t t = blockIdx.x * kWarpsPerBlock + w;
-    if (t >= a.n_traces) return;
+    if (t >= a.n_traces || a.traces[t].large) return;
     WarpSmem<SPL>* ws = reinterpret_cast<WarpSmem<SPL>*>(smem + sizeof(DevTables) + w * sizeof(WarpSmem<SPL>));
     simulate_trace<SPL, DETAIL>(a, tb, ws, t);
 }
@@ -50,6 +51,30 @@ static cudaError_t launch_sim_t(const SimArgs& a, cudaStream_t stream) {
     const unsigned blocks = (a.n_traces + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return cudaSuccess;
     sim_kernel<SPL, DETAIL><<<blocks, 32 * kWarpsPerBlock, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+// Block engine for clusters of more than 32 GPUs: one block per trace.
+constexpr int kClusterThreads = 512;
+
+template <bool DETAIL>
+__global__ void __launch_bounds__(kClusterThreads, 1) cluster_kernel(SimArgs a) {
+    __shared__ __align__(16) DevTables tb;
+    __shared__ BlockScratch sc;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.tables);
+        uint4* dst = reinterpret_cast<uint4*>(&tb);
+        for (unsigned i = threadIdx.x; i < sizeof(DevTables) / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    simulate_large_trace<DETAIL>(a, &tb, &sc, a.large_idx[blockIdx.x]);
+}
+
+cudaError_t launch_cluster(const SimArgs& a, cudaStream_t stream) {
+    if (!a.n_large) return cudaSuccess;
+    const bool detail = (a.out_flags & (OF_EVENTS | OF_TIMELINE)) != 0;
+    if (detail) cluster_kernel<true><<<a.n_large, kClusterThreads, 0, stream>>>(a);
+    else cluster_kernel<false><<<a.n_large, kClusterThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -49,6 +49,11 @@ struct msg_staged {
     bool any_perm = false;
     uint32_t ev_per_job = 16, tl_per_job = 8;
     uint64_t handler_events = 0;
+    // block engine (G > 32): large traces and their cluster arena
+    std::vector<uint32_t> large_idx;
+    uint64_t large_gpus = 0;
+    bool any_small = false;
+    DevBuf d_large_idx, c_st, c_prof, c_mig, c_cseq, c_job, c_mseq, c_rem, c_tkey, c_apos, c_act, c_gw, c_gx, c_gcid;
     // pinned host mirrors (rank order)
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
@@ -137,6 +142,9 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     pt.mark("  validate");
     uint64_t njobs = 0;
     int maxG = 1;
+    s->large_idx.clear();
+    s->large_gpus = 0;
+    s->any_small = false;
     for (uint32_t t = 0; t < s->n_in; ++t) {
         const uint32_t ci = b->config_index ? b->config_index[t] : 0;
         s->gpu_count[t] = cfgs[ci].gpu_count;
@@ -148,12 +156,20 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         tr.n_jobs = (uint32_t)(b->offsets[t + 1] - b->offsets[t]);
         tr.cfg = ci;
         tr.has_perm = checks[t].identity ? 0 : 1;
+        tr.large = cfgs[ci].gpu_count > (int)kMaxGpusEnsemble ? 1u : 0u;
+        if (tr.large) {
+            tr.cl_goff = s->large_gpus;
+            s->large_gpus += (uint64_t)cfgs[ci].gpu_count;
+            s->large_idx.push_back((uint32_t)s->traces.size());
+        } else {
+            s->any_small = true;
+            maxG = std::max(maxG, cfgs[ci].gpu_count);
+        }
         s->dev_index[t] = (int32_t)s->traces.size();
         s->src_of.push_back(t);
         s->traces.push_back(tr);
         s->overlap.push_back(cfgs[ci].migration_overlap_s);
         njobs += tr.n_jobs;
-        maxG = std::max(maxG, cfgs[ci].gpu_count);
     }
     s->n_jobs = njobs;
     s->spl = maxG <= 4 ? 1 : maxG <= 8 ? 2 : maxG <= 16 ? 4 : 8;
@@ -204,6 +220,25 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     if (any_perm) CK(s->d_perm.ensure(N * sizeof(uint32_t)));
     if (s->ev_total) CK(s->d_events.ensure(s->ev_total * sizeof(EventRec)));
     if (s->tl_total) CK(s->d_timeline.ensure(s->tl_total * 2 * sizeof(double)));
+    if (!s->large_idx.empty()) {
+        const size_t ng = s->large_gpus, ns = 8 * ng;
+        CK(s->d_large_idx.ensure(s->large_idx.size() * 4));
+        CK(s->c_st.ensure(ns));
+        CK(s->c_prof.ensure(ns));
+        CK(s->c_mig.ensure(ns * 2));
+        CK(s->c_cseq.ensure(ns * 4));
+        CK(s->c_job.ensure(ns * 4));
+        CK(s->c_mseq.ensure(ns * 4));
+        CK(s->c_rem.ensure(ns * 8));
+        CK(s->c_tkey.ensure(ns * 8));
+        CK(s->c_apos.ensure(ns * 4));
+        CK(s->c_act.ensure(ns * 4));
+        CK(s->c_gw.ensure(ng * 4));
+        CK(s->c_gx.ensure(ng * 4));
+        CK(s->c_gcid.ensure(ng));
+        CK(cudaMemcpyAsync(s->d_large_idx.p, s->large_idx.data(), s->large_idx.size() * 4, cudaMemcpyHostToDevice,
+                           st));
+    }
     if (njobs) {
         CK(cudaMemcpyAsync(s->d_arrival.p, ha, njobs * sizeof(double), cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(s->d_service.p, hs, njobs * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -241,15 +276,39 @@ SimArgs make_args(msg_engine* eng, msg_staged* s) {
     a.summary = s->d_summary.as<DevSummary>();
     a.n_traces = (uint32_t)s->traces.size();
     a.out_flags = s->out_flags;
+    a.n_large = (uint32_t)s->large_idx.size();
+    if (a.n_large) {
+        a.large_idx = s->d_large_idx.as<uint32_t>();
+        a.c_st = s->c_st.as<uint8_t>();
+        a.c_prof = s->c_prof.as<uint8_t>();
+        a.c_mig = s->c_mig.as<uint16_t>();
+        a.c_cseq = s->c_cseq.as<uint32_t>();
+        a.c_job = s->c_job.as<int32_t>();
+        a.c_mseq = s->c_mseq.as<uint32_t>();
+        a.c_rem = s->c_rem.as<double>();
+        a.c_tkey = s->c_tkey.as<double>();
+        a.c_apos = s->c_apos.as<int32_t>();
+        a.c_act = s->c_act.as<int32_t>();
+        a.c_gw = s->c_gw.as<uint32_t>();
+        a.c_gx = s->c_gx.as<uint32_t>();
+        a.c_gcid = s->c_gcid.as<uint8_t>();
+    }
     return a;
 }
 
 msg_status launch_impl(msg_engine* eng, msg_staged* s) {
     if (s->traces.empty()) return MSG_OK;
     const SimArgs a = make_args(eng, s);
-    cudaError_t e = launch_sim(s->spl, a, eng->stream);
-    if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim");
-    ++eng->launches;
+    if (s->any_small) {
+        cudaError_t e = launch_sim(s->spl, a, eng->stream);
+        if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim");
+        ++eng->launches;
+    }
+    if (a.n_large) {
+        cudaError_t e = launch_cluster(a, eng->stream);
+        if (e != cudaSuccess) return cuda_fail(eng, e, "launch_cluster");
+        ++eng->launches;
+    }
     return MSG_OK;
 }
 

@@ -140,7 +140,10 @@ inline int build_tables(DevTables* t) {
     if (d4.size() > 256) return -2;
     for (size_t i = 0; i < k4.size(); ++i)
         t->cost4pair[i] = (uint8_t)(std::lower_bound(d4.begin(), d4.end(), k4[i]) - d4.begin());
-    for (size_t i = 0; i < 256; ++i) t->cost4val[i] = i < d4.size() ? (double)d4[i] / 25200.0 : 0.0;
+    for (size_t i = 0; i < 256; ++i) {
+        t->cost4val[i] = i < d4.size() ? (double)d4[i] / 25200.0 : 0.0;
+        t->cost4k[i] = i < d4.size() ? (uint16_t)d4[i] : 0;
+    }
     return (int)distinct.size();
 }
 

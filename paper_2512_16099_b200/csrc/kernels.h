@@ -10,4 +10,7 @@ namespace msgk {
 // Launch the per-trace event-loop kernel; spl in {1, 2, 4, 8}.
 cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream);
 
+// Launch the block engine over a.large_idx (traces with more than 32 GPUs).
+cudaError_t launch_cluster(const SimArgs& a, cudaStream_t stream);
+
 }  // namespace msgk

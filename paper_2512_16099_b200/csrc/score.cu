@@ -3,8 +3,8 @@
 // schedule() / first_fit_schedule() (scheduler.cpp:47-98) for snapshots of
 // any size: each GPU is one packed 64-bit state word (busy compute, busy
 // memory, blocked memory, 18 idle-exact placement bits; msg_pack_gpu_word).
-// A persistent grid streams 1024-word chunks of the snapshots with 128-bit
-// loads (4 words per thread, issued before use), scores every legal
+// A persistent grid streams 512-word chunks of the snapshots with 128-bit
+// loads (2 words per thread, the next chunk in flight), scores every legal
 // start of the job's profile — the profile is block-uniform, so the scoring
 // loop is specialised per profile with compile-time footprints — and keeps
 // a 32-bit block-local key [pass:1|cost rank:5|!reused:1|word:11|start:3]
@@ -23,7 +23,10 @@
 namespace msgk {
 
 constexpr int kScoreThreads = 256;
-constexpr int kWordsPerThread = 4;
+#ifndef MSG_SCORE_WPT
+#define MSG_SCORE_WPT 2
+#endif
+constexpr int kWordsPerThread = MSG_SCORE_WPT;  // 2 or 4 (one or two 128-bit loads)
 constexpr int kChunk = kScoreThreads * kWordsPerThread;  // words per chunk (<= 2048: 11-bit local index)
 
 template <int P>
@@ -42,56 +45,73 @@ struct ScoreCfg {
 
 // candidate_starts (scheduler.cpp:19-28) of one GPU word, post-placement
 // cost rank, reuse flag and Lazy/Busy pass, folded into the running minimum.
-template <int P>
+template <int P, bool LB>
 __device__ __forceinline__ void score_word(const ScoreCfg& c, const uint8_t* lut, uint64_t w, unsigned local,
                                            unsigned& best, unsigned& cnt_lb) {
     using Q = Prof<P>;
     const unsigned lo = (unsigned)w;
-    const unsigned bc = lo & 0x7Fu, bm = (lo >> 8) & 0xFFu, km = (lo >> 16) & 0xFFu;
+    const unsigned bm = (lo >> 8) & 0xFFu, km = (lo >> 16) & 0xFFu;
     const unsigned exact = (unsigned)(w >> (24 + Q::pbase));
-    const unsigned pc = __popc(bc);
+    const unsigned pc = __popc(lo & 0x7Fu);
     const unsigned lazy = (c.lazymask >> pc) & 1u;
-    const unsigned head = c.lb ? (((lazy ^ 1u) << 31) | (local << 3)) : (local << 3);
-    const unsigned row = min(pc + Q::cs, 7u) * 256u;  // popc(busy_c | fc) when the start is free
+    const unsigned head = LB ? (((lazy ^ 1u) << 31) | (local << 3)) : (local << 3);
+    // LUT row of popc(busy_c | fc) = pc + cs (the start is free), | busy_m
+    const unsigned rb = (min(pc + Q::cs, 7u) << 8) | bm;
+    const unsigned allow = c.dyn ? 0x7Fu : exact;  // candidate_starts: exact-idle only without dyn
     unsigned cnt = 0;
+    // Branch-free: every legal start is scored, unavailable ones are masked.
 #pragma unroll
     for (unsigned j = 0; j < Q::n; ++j) {
-        const unsigned ex = (exact >> j) & 1u;
-        if (!(Q::fm(j) & km) && (c.dyn || ex)) {
-            ++cnt;
-            const unsigned key = c.lb ? (head | ((unsigned)lut[row + (bm | Q::fm(j))] << 26) | ((ex ^ 1u) << 25) |
-                                         (j * Q::stride))
-                                      : (head | (j * Q::stride));
-            best = min(best, key);
-        }
+        const unsigned ok = (((Q::fm(j) & km) == 0) ? 1u : 0u) & (allow >> j);
+        const unsigned r = lut[rb | Q::fm(j)];
+        const unsigned key = LB ? (head | (r << 26) | ((~exact >> j & 1u) << 25) | (j * Q::stride))
+                                : (head | (j * Q::stride));
+        best = min(best, ok ? key : 0xFFFFFFFFu);
+        cnt += ok;
     }
     cnt_lb += lazy ? cnt << 16 : cnt;
 }
 
-// One chunk of one snapshot: every thread scores kWordsPerThread words,
-// loaded up front with 128-bit evict-first loads; the warp's winner and
-// candidate counts go straight to the snapshot's slots with one 64-bit
-// atomicMin / atomicAdd (no block-level synchronisation).
-template <int P>
-__device__ __forceinline__ void score_chunk(const ScoreArgs& a, const ScoreCfg& c, const uint8_t* lut,
-                                            uint64_t snap, uint64_t c0) {
+// One chunk of one snapshot: every thread scores kWordsPerThread words it
+// loaded (128-bit, evict-first) one grid-stride iteration earlier — the
+// next chunk's load is in flight while this one is scored.  The warp's
+// winner and candidate counts go straight to the snapshot's slots with one
+// 64-bit atomicMin / atomicAdd (no block-level synchronisation).
+struct ChunkData {
+    ulonglong2 v[kWordsPerThread / 2];
+};
+
+__device__ __forceinline__ ChunkData load_chunk(const ScoreArgs& a, uint64_t ch, uint64_t chunks_per) {
+    ChunkData d;
+    const uint64_t snap = ch / chunks_per;
+    const uint64_t c0 = (ch % chunks_per) * kChunk;
     const uint64_t* words = a.words + snap * a.G;
+    const unsigned t2 = threadIdx.x * 2u;
+#pragma unroll
+    for (int k = 0; k < kWordsPerThread / 2; ++k) {
+        const uint64_t g = c0 + t2 + (unsigned)k * 2 * kScoreThreads;
+        if ((a.G & 1) == 0 && g + 1 < a.G) {
+            d.v[k] = __ldcs(reinterpret_cast<const ulonglong2*>(words + g));
+        } else {
+            d.v[k].x = g < a.G ? words[g] : 0ull;
+            d.v[k].y = g + 1 < a.G ? words[g + 1] : 0ull;
+        }
+    }
+    return d;
+}
+
+template <int P, bool LB>
+__device__ __forceinline__ void score_chunk(const ScoreArgs& a, const ScoreCfg& c, const uint8_t* lut,
+                                            const ChunkData& d, uint64_t snap, uint64_t c0) {
     unsigned best = 0xFFFFFFFFu, cnt = 0;
     const unsigned t2 = threadIdx.x * 2u;
-    if ((a.G & 1) == 0 && c0 + kChunk <= a.G) {
-        ulonglong2 v[kWordsPerThread / 2];
+    // words past the snapshot end score as fully occupied (no candidate)
+    constexpr uint64_t kFull = 0xFFFF7Full;
 #pragma unroll
-        for (int k = 0; k < kWordsPerThread / 2; ++k)
-            v[k] = __ldcs(reinterpret_cast<const ulonglong2*>(words + c0 + t2 + (unsigned)k * 2 * kScoreThreads));
-#pragma unroll
-        for (int k = 0; k < kWordsPerThread / 2; ++k) {
-            const unsigned l = t2 + (unsigned)k * 2 * kScoreThreads;
-            score_word<P>(c, lut, v[k].x, l, best, cnt);
-            score_word<P>(c, lut, v[k].y, l + 1, best, cnt);
-        }
-    } else {
-        for (unsigned l = threadIdx.x; l < kChunk && c0 + l < a.G; l += kScoreThreads)
-            score_word<P>(c, lut, words[c0 + l], l, best, cnt);
+    for (int k = 0; k < kWordsPerThread / 2; ++k) {
+        const unsigned l = t2 + (unsigned)k * 2 * kScoreThreads;
+        score_word<P, LB>(c, lut, c0 + l < a.G ? d.v[k].x : kFull, l, best, cnt);
+        score_word<P, LB>(c, lut, c0 + l + 1 < a.G ? d.v[k].y : kFull, l + 1, best, cnt);
     }
     best = __reduce_min_sync(0xffffffffu, best);
     cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -110,6 +130,7 @@ __device__ __forceinline__ void score_chunk(const ScoreArgs& a, const ScoreCfg& 
 
 // Persistent grid: each block walks chunks blockIdx.x, +gridDim.x, ...; the
 // cost-rank table is staged into shared memory once per block.
+template <bool LB>
 __global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreArgs a) {
     __shared__ __align__(16) uint8_t lut[8 * 256];
     for (unsigned i = threadIdx.x; i < 8 * 256 / 16; i += blockDim.x)
@@ -118,17 +139,24 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreArgs a) {
     const ScoreCfg c{a.lb, a.dyn, a.lazymask};
     const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
     const uint64_t total = chunks_per * a.n;
-    for (uint64_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
+    uint64_t ch = blockIdx.x;
+    if (ch >= total) return;
+    ChunkData cur = load_chunk(a, ch, chunks_per);
+    for (; ch < total; ch += gridDim.x) {
+        const uint64_t nxt = ch + gridDim.x;
+        ChunkData next;
+        if (nxt < total) next = load_chunk(a, nxt, chunks_per);
         const uint64_t snap = ch / chunks_per;
         const uint64_t c0 = (ch % chunks_per) * kChunk;
         switch (a.profile[snap]) {
-            case 0: score_chunk<0>(a, c, lut, snap, c0); break;
-            case 1: score_chunk<1>(a, c, lut, snap, c0); break;
-            case 2: score_chunk<2>(a, c, lut, snap, c0); break;
-            case 3: score_chunk<3>(a, c, lut, snap, c0); break;
-            case 4: score_chunk<4>(a, c, lut, snap, c0); break;
-            default: score_chunk<5>(a, c, lut, snap, c0); break;
+            case 0: score_chunk<0, LB>(a, c, lut, cur, snap, c0); break;
+            case 1: score_chunk<1, LB>(a, c, lut, cur, snap, c0); break;
+            case 2: score_chunk<2, LB>(a, c, lut, cur, snap, c0); break;
+            case 3: score_chunk<3, LB>(a, c, lut, cur, snap, c0); break;
+            case 4: score_chunk<4, LB>(a, c, lut, cur, snap, c0); break;
+            default: score_chunk<5, LB>(a, c, lut, cur, snap, c0); break;
         }
+        cur = next;
     }
 }
 
@@ -151,7 +179,8 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     }
     const uint64_t chunks = ((a.G + kChunk - 1) / kChunk) * a.n;
     const uint64_t blocks = std::min<uint64_t>(chunks, (uint64_t)sms * 8);  // 8 x 256 threads per SM
-    score_kernel<<<(unsigned)blocks, kScoreThreads, 0, stream>>>(a);
+    if (a.lb) score_kernel<true><<<(unsigned)blocks, kScoreThreads, 0, stream>>>(a);
+    else score_kernel<false><<<(unsigned)blocks, kScoreThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -66,12 +66,12 @@ inline CfgState validate_config(const msg_config& c) {
                     return fail(MSG_ERR_SLICES_BUSY,
                                 "layout instance overlaps an existing instance on GPU " + std::to_string(g));
                 used |= host_fpm(p, st);
-                s.init.push_back((uint32_t)(g * 8 + st) | ((uint32_t)p << 16));
+                s.init.push_back((uint32_t)(g * 8 + st) | ((uint32_t)p << 24));  // slot:24 | profile:8
             }
         }
     }
-    if ((uint32_t)c.gpu_count > kMaxGpusEnsemble)
-        return fail(MSG_ERR_UNSUPPORTED, "the ensemble engine supports at most 32 GPUs per cluster");
+    if (c.gpu_count >= (1 << 16))  // 16-bit GPU ids in the event records
+        return fail(MSG_ERR_UNSUPPORTED, "at most 65535 GPUs per cluster");
     s.dev.alpha = c.contention_alpha;
     s.dev.overlap = c.migration_overlap_s;
     s.dev.latency = c.reconfig_latency_s;

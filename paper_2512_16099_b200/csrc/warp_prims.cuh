@@ -39,6 +39,10 @@ MSG_DI double dsub(double a, double b) { return __dsub_rn(a, b); }
 MSG_DI double dmul(double a, double b) { return __dmul_rn(a, b); }
 MSG_DI double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 MSG_DI uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
+// block level (cluster_core.cuh)
+MSG_DI void bsync() { __syncthreads(); }
+MSG_DI unsigned tid() { return threadIdx.x; }
+MSG_DI unsigned nthreads() { return blockDim.x; }
 }  // namespace wp
 
 #else  // host emulation (tests/emu)

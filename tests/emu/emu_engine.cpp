@@ -2,11 +2,13 @@
 // (paper_2512_16099_b200/csrc/engine_core.cuh) on 32 host threads per trace,
 // with the product's own staging/decoding (staging.h), and returns results
 // in the ABI record formats so tests can diff them against the reference.
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "cluster_core.cuh"
 #include "engine_core.cuh"
 #include "staging.h"
 
@@ -38,6 +40,27 @@ void run_warp(const SimArgs& a, const DevTables* tb) {
         });
     }
     for (auto& t : lanes) t.join();
+}
+
+// Block engine (G > 32) on `nt` emulated threads (nt/32 warps + a block barrier).
+void run_block(const SimArgs& a, const DevTables* tb, unsigned nt) {
+    auto sc = std::make_unique<BlockScratch>();
+    std::memset(sc.get(), 0xA5, sizeof(BlockScratch));
+    wp::EmuBlock block;
+    block.n = nt;
+    std::vector<std::unique_ptr<wp::EmuWarp>> warps;
+    for (unsigned i = 0; i < nt / 32; ++i) warps.emplace_back(new wp::EmuWarp());
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t]() {
+            wp::g_block = &block;
+            wp::g_warp = warps[t / 32].get();
+            wp::g_lane = t % 32;
+            wp::g_tid = t;
+            wp::g_phase = 0;
+            simulate_large_trace<true>(a, tb, sc.get(), 0);
+        });
+    for (auto& x : th) x.join();
 }
 
 }  // namespace
@@ -95,7 +118,36 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
     a.n_traces = 1;
     a.out_flags = OF_JOBS | OF_EVENTS | OF_TIMELINE;
     const int G = c->gpu_count;
-    if (G <= 4) run_warp<1>(a, &tables);
+    // block-engine arena (used when G > 32, or when MSG_EMU_FORCE_BLOCK is set)
+    const size_t ns = 8 * (size_t)G;
+    std::vector<uint8_t> c_st(ns), c_prof(ns), c_gcid(G);
+    std::vector<uint16_t> c_mig(ns);
+    std::vector<uint32_t> c_cseq(ns), c_mseq(ns), c_gw(G), c_gx(G);
+    std::vector<int32_t> c_job(ns), c_apos(ns), c_act(ns);
+    std::vector<double> c_rem(ns), c_tkey(ns);
+    uint32_t large_idx = 0;
+    const bool block = G > 32 || std::getenv("MSG_EMU_FORCE_BLOCK") != nullptr;
+    if (block) {
+        tr.large = 1;
+        tr.cl_goff = 0;
+        a.large_idx = &large_idx;
+        a.n_large = 1;
+        a.c_st = c_st.data();
+        a.c_prof = c_prof.data();
+        a.c_mig = c_mig.data();
+        a.c_cseq = c_cseq.data();
+        a.c_job = c_job.data();
+        a.c_mseq = c_mseq.data();
+        a.c_rem = c_rem.data();
+        a.c_tkey = c_tkey.data();
+        a.c_apos = c_apos.data();
+        a.c_act = c_act.data();
+        a.c_gw = c_gw.data();
+        a.c_gx = c_gx.data();
+        a.c_gcid = c_gcid.data();
+        const char* nt = std::getenv("MSG_EMU_BLOCK_THREADS");
+        run_block(a, &tables, nt ? (unsigned)std::atoi(nt) : 64u);
+    } else if (G <= 4) run_warp<1>(a, &tables);
     else if (G <= 8) run_warp<2>(a, &tables);
     else if (G <= 16) run_warp<4>(a, &tables);
     else run_warp<8>(a, &tables);

@@ -26,6 +26,16 @@ inline thread_local EmuWarp* g_warp = nullptr;
 inline thread_local unsigned g_lane = 0;
 inline thread_local unsigned g_phase = 0;
 
+// Block emulation (cluster_core.cuh): nthreads std::threads, one EmuWarp per
+// 32 of them, plus a block-wide barrier.
+struct EmuBlock {
+    std::atomic<unsigned> arrived{0};
+    std::atomic<unsigned> gen{0};
+    unsigned n = 32;
+};
+inline thread_local EmuBlock* g_block = nullptr;
+inline thread_local unsigned g_tid = 0;
+
 inline void barrier() {
     EmuWarp* w = g_warp;
     const unsigned g = w->gen.load(std::memory_order_acquire);
@@ -49,6 +59,21 @@ inline const uint64_t* exchange(uint64_t v) {
 }
 
 inline unsigned lane() { return g_lane; }
+inline unsigned tid() { return g_tid; }
+inline unsigned nthreads() { return g_block ? g_block->n : 32u; }
+inline void bsync() {
+    EmuBlock* b = g_block;
+    const unsigned g = b->gen.load(std::memory_order_acquire);
+    if (b->arrived.fetch_add(1, std::memory_order_acq_rel) == b->n - 1) {
+        b->arrived.store(0, std::memory_order_relaxed);
+        b->gen.fetch_add(1, std::memory_order_release);
+    } else {
+        unsigned spins = 0;
+        while (b->gen.load(std::memory_order_acquire) == g) {
+            if (++spins > 32) std::this_thread::yield();
+        }
+    }
+}
 inline void sync() { barrier(); }
 inline unsigned ballot(bool p) {
     const uint64_t* b = exchange(p ? 1u : 0u);

@@ -1,0 +1,66 @@
+"""CPU-side check of the block engine for large clusters (cluster_core.cuh,
+compiled for the host with the test-only block/warp emulation) against the
+reference library: bit-exact (timeline exact up to 512 GPUs, 1e-9 relative
+above)."""
+import os
+
+import pytest
+
+from helpers import diff_results, diff_results_relaxed_timeline, emu_run_batch_results
+from oracle import refbind as rb
+from paper_2512_16099_b200.model import FeatureFlags, SchedulerConfig, SimConfig, WorkloadSpec, preset, static_layout_preset
+
+pytestmark = pytest.mark.skipif(not rb.ref_available(), reason="reference library not built")
+
+
+@pytest.fixture
+def block_env(monkeypatch):
+    def set_(force=False, threads=64):
+        if force:
+            monkeypatch.setenv("MSG_EMU_FORCE_BLOCK", "1")
+        else:
+            monkeypatch.delenv("MSG_EMU_FORCE_BLOCK", raising=False)
+        monkeypatch.setenv("MSG_EMU_BLOCK_THREADS", str(threads))
+    return set_
+
+
+def _check(spec, cfg, seeds, relaxed=False):
+    b = rb.ref_generate_batch(spec, seeds)
+    ref = rb.ref_run_batch_results(b, [cfg])
+    got = emu_run_batch_results(b, [cfg])
+    diff = diff_results_relaxed_timeline if relaxed else diff_results
+    bad = [(s, d) for s, r, g in zip(seeds, ref, got) if (d := diff(r, g))]
+    assert not bad, bad[:2]
+
+
+@pytest.mark.parametrize("threads", [32, 64, 96])
+def test_block_engine_on_small_clusters_matches(block_env, threads):
+    block_env(force=True, threads=threads)
+    _check(preset("normal25"), SimConfig(gpu_count=8), [0, 1])
+    c5 = WorkloadSpec(mean_interarrival_s=0.4, median_s=4.0, sigma=1.2, profile_mix=(0.5, 0.3, 0.2, 0.0))
+    _check(c5, SimConfig(gpu_count=8, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                         reconfig_latency_s=0.1), [2])
+    for f in (FeatureFlags(False, False, False), FeatureFlags(True, False, False)):
+        sp = preset("normal25")
+        sp.mean_interarrival_s = 10.0
+        _check(sp, SimConfig(gpu_count=4, sched=SchedulerConfig(features=f, static_layout=static_layout_preset("static-b"))),
+               [3])
+
+
+def test_block_engine_large_clusters(block_env):
+    block_env(force=False, threads=64)
+    sp = preset("normal25")
+    sp.mean_interarrival_s = 25.0 / 12
+    sp.job_count = 400
+    _check(sp, SimConfig(gpu_count=96), [0])
+    churn = WorkloadSpec(mean_interarrival_s=0.04, median_s=4.0, sigma=1.2, job_count=400)
+    _check(churn, SimConfig(gpu_count=50, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                            reconfig_latency_s=0.1), [1])
+
+
+def test_block_engine_relaxed_timeline_above_512_gpus(block_env):
+    block_env(force=False, threads=64)
+    sp = preset("normal25")
+    sp.mean_interarrival_s = 25.0 / 80
+    sp.job_count = 600
+    _check(sp, SimConfig(gpu_count=640), [4], relaxed=True)
