@@ -96,7 +96,7 @@ class Staged:
         _check(lib().msg_time_launch(self.engine._h, self._h, C.byref(ms)), self.engine)
         return ms.value
 
-    def collect(self) -> list:
+    def collect(self) -> "BatchResult":
         r = C.c_void_p()
         _check(lib().msg_collect(self.engine._h, self._h, C.byref(r)), self.engine)
         return _decode(r, self.out_flags)
@@ -155,7 +155,7 @@ class Engine:
     def flush_l2(self):
         _check(lib().msg_engine_flush_l2(self._h), self)
 
-    def run_batch(self, batch: TraceBatch, cfgs: Sequence[SimConfig], out_flags: int = abi.OUT_JOBS) -> list:
+    def run_batch(self, batch: TraceBatch, cfgs: Sequence[SimConfig], out_flags: int = abi.OUT_JOBS) -> "BatchResult":
         """migsched::run over every trace of the batch (sim.cpp:504-507)."""
         pack = ConfigPack(cfgs)
         r = C.c_void_p()
@@ -200,38 +200,64 @@ def _view(ptr, n, dtype, owner):
     return np.asarray(_Mem(ptr, n * dtype.itemsize, owner)).view(dtype)
 
 
-def _decode(r, flags: int) -> list:
-    """Decode a msg_batch_result; per-job rows and events are zero-copy views
-    into the library's result buffers (freed when the last view dies)."""
-    L = lib()
-    owner = _ResultHolder(r)
-    out = []
-    n = L.msg_result_n_traces(r)
-    cnt = C.c_uint64()
-    if n == 0:
-        return out
-    summaries = _view(L.msg_result_summaries(r), n, abi.SUMMARY_DTYPE, owner)
-    offp = C.POINTER(C.c_uint64)()
-    jp = L.msg_result_all_jobs(r, C.byref(offp), C.byref(cnt))
-    jobs_all = offs = None
-    if jp:
-        jobs_all = _view(jp, cnt.value, abi.JOB_DTYPE, owner)
-        offs = np.ctypeslib.as_array(offp, shape=(n + 1,)).copy()
-    status = summaries["status"]
-    for t in range(n):
-        st = int(status[t])
-        msg = L.msg_result_message(r, t).decode() if st != 0 else ""
-        jobs = jobs_all[offs[t]:offs[t + 1]] if jobs_all is not None else None
-        out.append(TraceResult(st, msg, summaries[t], jobs, None, None))
-    if flags & (abi.OUT_EVENTS | abi.OUT_TIMELINE):
-        for t in range(n):
-            if flags & abi.OUT_EVENTS:
-                p = L.msg_result_events(r, t, C.byref(cnt))
-                out[t].events = _view(p, cnt.value, abi.EVENT_DTYPE, owner)
-            if flags & abi.OUT_TIMELINE:
-                p = L.msg_result_timeline(r, t, C.byref(cnt))
-                out[t].frag_timeline = _view(p, cnt.value, abi.TIMELINE_DTYPE, owner)
-    return out
+class BatchResult:
+    """Results of one batch (msg_batch_result), decoded lazily.
+
+    `summaries` (SUMMARY_DTYPE[n]) and `jobs` (JOB_DTYPE, all traces,
+    `job_offsets`) are zero-copy views into the library's buffers; indexing
+    or iterating yields per-trace TraceResult objects shaped like the
+    reference's SimResult."""
+
+    def __init__(self, handle, flags: int):
+        L = lib()
+        self._owner = _ResultHolder(handle)
+        self._h = handle
+        self.flags = flags
+        self.n = int(L.msg_result_n_traces(handle))
+        cnt = C.c_uint64()
+        self.summaries = _view(L.msg_result_summaries(handle), self.n, abi.SUMMARY_DTYPE, self._owner)
+        offp = C.POINTER(C.c_uint64)()
+        jp = L.msg_result_all_jobs(handle, C.byref(offp), C.byref(cnt))
+        self.jobs = self.job_offsets = None
+        if jp:
+            self.jobs = _view(jp, cnt.value, abi.JOB_DTYPE, self._owner)
+            self.job_offsets = np.ctypeslib.as_array(offp, shape=(self.n + 1,)).copy()
+
+    def __len__(self):
+        return self.n
+
+    def __getitem__(self, t):
+        if isinstance(t, slice):
+            return [self[i] for i in range(*t.indices(self.n))]
+        if t < 0:
+            t += self.n
+        if not 0 <= t < self.n:
+            raise IndexError(t)
+        L = lib()
+        cnt = C.c_uint64()
+        summ = self.summaries[t]
+        st = int(summ["status"])
+        msg = L.msg_result_message(self._h, t).decode() if st != 0 else ""
+        jobs = self.jobs[self.job_offsets[t]:self.job_offsets[t + 1]] if self.jobs is not None else None
+        res = TraceResult(st, msg, summ, jobs, None, None)
+        if self.flags & abi.OUT_EVENTS:
+            res.events = _view(L.msg_result_events(self._h, t, C.byref(cnt)), cnt.value, abi.EVENT_DTYPE, self._owner)
+        if self.flags & abi.OUT_TIMELINE:
+            res.frag_timeline = _view(L.msg_result_timeline(self._h, t, C.byref(cnt)), cnt.value,
+                                      abi.TIMELINE_DTYPE, self._owner)
+        return res
+
+    def __iter__(self):
+        for t in range(self.n):
+            yield self[t]
+
+    @property
+    def handler_events(self) -> int:
+        return int(self.summaries["handler_events"].sum())
+
+
+def _decode(r, flags: int) -> BatchResult:
+    return BatchResult(r, flags)
 
 
 _default_engine: Optional[Engine] = None

@@ -55,5 +55,5 @@ def run_shard(spec, cfg, rank: int, traces_per_rank: int, run_fn: Optional[Calla
         from .engine import default_engine
 
         res = default_engine().run_batch(batch, [cfg], 0)
-        return np.array([r.summary for r in res], abi.SUMMARY_DTYPE)
+        return np.array(res.summaries, abi.SUMMARY_DTYPE)
     return run_fn(batch, cfg)

@@ -125,7 +125,7 @@ def test_c2_full_ensemble_summaries(engine):
     cfg = SimConfig(gpu_count=8)
     gpu = engine.run_batch(b, [cfg], 0)
     ref, _ = rb.ref_run_batch_summaries(b, [cfg], threads=0)
-    got = np.array([g.summary for g in gpu])
+    got = gpu.summaries
     for f in ("status", "handler_events", "migration_count", "reconfig_op_count", "dequeue_count",
               "mean_turnaround_s", "workload_makespan_s", "mean_wait_s", "timeline_sum",
               "max_arrival_frag_evals", "max_inter_iter_frag_evals", "max_intra_iter_frag_evals"):
@@ -134,3 +134,44 @@ def test_c2_full_ensemble_summaries(engine):
     assert int(got["handler_events"].sum()) == 1638400
     assert int(got["migration_count"].sum()) == 311361
     assert int(got["reconfig_op_count"].sum()) == 728524
+
+
+def _agg_spec_cfg(entry):
+    import importlib.util
+    import os
+
+    from helpers import GOLDEN
+
+    spec_mod = importlib.util.spec_from_file_location("make_golden", os.path.join(GOLDEN, "make_golden.py"))
+    mg = importlib.util.module_from_spec(spec_mod)
+    spec_mod.loader.exec_module(mg)
+    sp = WorkloadSpec(**entry["spec"])
+    sp.profile_mix = tuple(sp.profile_mix)
+    return sp, mg.cfg_from(entry["cfg"])
+
+
+@pytest.mark.parametrize("name", ["c2_4096", "c5_4096", "c3_ia25_combo0", "c3_ia25_combo1", "c3_ia25_combo2",
+                                  "c3_ia25_combo3"])
+def test_full_size_aggregates_vs_reference_goldens(engine, name):
+    """Full-size ensembles (BASELINE configs C2, C5, a C3 load level) against
+    aggregates produced by the reference library (tests/golden/aggregates.json):
+    counts exact, per-trace means/makespans/timeline digests via exact
+    bit-pattern checksums."""
+    import json
+    import os
+
+    from helpers import GOLDEN
+    from paper_2512_16099_b200.engine import generate_batch
+
+    entry = json.load(open(os.path.join(GOLDEN, "aggregates.json")))[name]
+    sp, cfg = _agg_spec_cfg(entry)
+    lo, hi = entry["seeds"]
+    res = engine.run_batch(generate_batch(sp, lo, hi - lo + 1), [cfg], 0)
+    s = res.summaries
+    assert int(s["handler_events"].sum()) == entry["handler_events"]
+    assert int(s["migration_count"].sum()) == entry["migrations"]
+    assert int(s["reconfig_op_count"].sum()) == entry["reconfig_ops"]
+    assert int(s["dequeue_count"].sum()) == entry["dequeues"]
+    for key, field in (("checksum_turnaround", "mean_turnaround_s"), ("checksum_makespan", "workload_makespan_s"),
+                       ("checksum_timeline", "timeline_sum")):
+        assert int(np.ascontiguousarray(s[field]).view(np.uint64).sum(dtype=np.uint64)) == entry[key], key
