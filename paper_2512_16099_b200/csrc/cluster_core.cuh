@@ -3,18 +3,24 @@
 // reference's discrete-event scheduler (proj/src/sim.cpp:71-410).
 //
 // Same semantics and the same packed-key decisions as the warp engine
-// (engine_core.cuh), with the state moved to global memory (L2-resident:
-// ~64 B per (GPU, start) slot) and block-wide reductions:
-//   * the 8 slots of GPU g are slots 8g..8g+7 of the trace's cluster arena;
-//     per GPU a mask word (busy compute | busy memory | blocked memory |
-//     running count), the idle-exact placement bits and the 4-mask cost id;
-//   * an ACTIVE list holds the slots that carry a timer (running, waiting
-//     for service start, draining), so next-event search, advance_all and
-//     reschedule scan ~R entries, not 8G slots;
+// (engine_core.cuh), laid out for thousands of GPUs:
+//   * per GPU: mask word (busy compute | busy memory | blocked memory |
+//     running count), idle-exact placement bits, 4-mask cost id — in SHARED
+//     memory (9 B/GPU, up to ~24K GPUs), else global;
+//   * per (GPU, start) slot: instance state, profile, creation sequence,
+//     migrations of the bound job, position in the active list — global
+//     (L2-resident);
+//   * the ACTIVE list holds every slot that carries a timer (running, waiting
+//     for service start, draining) with the timer data stored densely by list
+//     index (time, state, job, remaining work, MigrationEnd sequence): the
+//     per-event scans (next event, advance_all, reschedule, plan_inter
+//     sources) are coalesced, indirection-free loops over ~R entries,
+//     unrolled for memory-level parallelism; a migrating job keeps its entry
+//     (only the slot changes);
 //   * GPU-local steps (create_instance, refresh of a GPU word) run on one
 //     thread; plan_intra on warp 0; schedule, plan_inter and the next-event
 //     search are block-wide argmins over packed keys: per-warp REDUX chain,
-//     then one __syncthreads and the same chain over the 32 warp winners.
+//     then one __syncthreads and the same chain over the warp winners.
 // Bit-exact with the reference, except the fragmentation timeline above
 // kExactTimelineGpus GPUs: there the per-sample mean is
 // RN(RN(sum_g k_g / 25200) / G) from the exact integer sum of the per-GPU
@@ -44,17 +50,20 @@ template <bool DETAIL>
 struct ClusterSim {
     BlockScratch* sc;
     const DevTables* tb;
-    // arena views of this trace
+    // per slot
     uint8_t* st;
     uint8_t* prof;
     uint16_t* mig;
     uint32_t* cseq;
-    int32_t* job;
-    uint32_t* mseq;
-    double* rem;
-    double* tkey;
     int32_t* apos;
-    int32_t* act;
+    // per active entry
+    int32_t* aslot;
+    uint8_t* ast;
+    int32_t* ajob;
+    uint32_t* amseq;
+    double* arem;
+    double* atkey;
+    // per GPU
     uint32_t* gw;
     uint32_t* gx;
     uint8_t* gcid;
@@ -71,8 +80,8 @@ struct ClusterSim {
     uint32_t cflags, lazymask;
     double alpha, overlap, latency, inv_g;
     // block-uniform state (every thread holds the same values)
-    unsigned T, W, L, w;  // thread, warp, lane, warps
-    int bph;              // scratch double-buffer parity
+    unsigned T, W, L, w, NT;  // thread, warp, lane, warps, threads
+    int bph;                  // scratch double-buffer parity
     double now, t_prev;
     uint32_t a_idx, a_rank;
     int a_prof;
@@ -158,11 +167,14 @@ struct ClusterSim {
     }
 
     // ---------------------------------------------------------------- setup
-    MSG_DI void setup(const SimArgs& a, const DevTables* tables, BlockScratch* scratch, uint32_t t) {
+    // gpu_smem: 9 B per GPU of dynamic shared memory, or nullptr (global).
+    MSG_DI void setup(const SimArgs& a, const DevTables* tables, BlockScratch* scratch, unsigned char* gpu_smem,
+                      uint32_t t) {
         T = wp::tid();
         L = wp::lane();
         W = T >> 5;
-        w = wp::nthreads() >> 5;
+        NT = wp::nthreads();
+        w = NT >> 5;
         bph = 0;
         sc = scratch;
         tb = tables;
@@ -174,15 +186,22 @@ struct ClusterSim {
         prof = a.c_prof + so;
         mig = a.c_mig + so;
         cseq = a.c_cseq + so;
-        job = a.c_job + so;
-        mseq = a.c_mseq + so;
-        rem = a.c_rem + so;
-        tkey = a.c_tkey + so;
         apos = a.c_apos + so;
-        act = a.c_act + so;
-        gw = a.c_gw + go;
-        gx = a.c_gx + go;
-        gcid = a.c_gcid + go;
+        aslot = a.c_aslot + so;
+        ast = a.c_ast + so;
+        ajob = a.c_ajob + so;
+        amseq = a.c_amseq + so;
+        arem = a.c_arem + so;
+        atkey = a.c_atkey + so;
+        if (gpu_smem) {
+            gw = reinterpret_cast<uint32_t*>(gpu_smem);
+            gx = gw + G;
+            gcid = reinterpret_cast<uint8_t*>(gx + G);
+        } else {
+            gw = a.c_gw + go;
+            gx = a.c_gx + go;
+            gcid = a.c_gcid + go;
+        }
         N = tr.n_jobs;
         arr = a.arrival + tr.job_off;
         svc = a.service + tr.job_off;
@@ -212,15 +231,14 @@ struct ClusterSim {
         max_arr = max_intra = max_inter = 0;
         tl_sum = tl_mean = 0.0;
         tl_dirty = true;
-        const unsigned nt = wp::nthreads();
-        for (uint64_t i = T; i < 8ull * G; i += nt) {
+        for (uint64_t i = T; i < 8ull * G; i += NT) {
             st[i] = ST_EMPTY;
             mig[i] = 0;
             apos[i] = -1;
         }
         // empty GPU: masks 0, cost id of frag 0 (every profile fully feasible)
         const uint8_t empty_id = tb->cost4pair[tb->idealid[0] * 32u + tb->feasid[0]];
-        for (uint64_t g = T; g < (uint64_t)G; g += nt) {
+        for (uint64_t g = T; g < (uint64_t)G; g += NT) {
             gw[g] = 0;
             gx[g] = 0;
             gcid[g] = empty_id;
@@ -275,8 +293,7 @@ struct ClusterSim {
                 k += v == ST_RUN;
             }
         }
-        const unsigned word = bc | (bm << 8) | (km << 16) | (k << 24);
-        gw[g] = word;
+        gw[g] = bc | (bm << 8) | (km << 16) | (k << 24);
         gx[g] = x;
         const unsigned row = (unsigned)wp::popc(bc) * 9u + (unsigned)wp::popc(bm);
         const uint8_t id = tb->cost4pair[tb->idealid[row] * 32u + tb->feasid[km]];
@@ -284,16 +301,29 @@ struct ClusterSim {
         gcid[g] = id;
     }
 
-    // active list (single thread): slots carrying a timer
-    MSG_DI void act_add(int slot) {
-        act[n_act] = slot;
-        apos[slot] = (int32_t)n_act;
+    // ------------------------------------------ active list (single thread)
+    MSG_DI void act_add(uint32_t i, int slot, uint8_t s, int32_t jb, double r, double tk, uint32_t ms) {
+        aslot[i] = slot;
+        ast[i] = s;
+        ajob[i] = jb;
+        arem[i] = r;
+        atkey[i] = tk;
+        amseq[i] = ms;
+        apos[slot] = (int32_t)i;
     }
     MSG_DI void act_remove(int slot, uint32_t n) {  // n = list size before removal
         const int i = apos[slot];
-        const int last = act[n - 1];
-        act[i] = last;
-        apos[last] = i;
+        const uint32_t last = n - 1;
+        if ((uint32_t)i != last) {
+            const int ls = aslot[last];
+            aslot[i] = ls;
+            ast[i] = ast[last];
+            ajob[i] = ajob[last];
+            arem[i] = arem[last];
+            atkey[i] = atkey[last];
+            amseq[i] = amseq[last];
+            apos[ls] = i;
+        }
         apos[slot] = -1;
     }
 
@@ -304,21 +334,20 @@ struct ClusterSim {
         if (!(dt > 0.0)) return;
         if (T < 7) sc->q[T] = wp::ddiv(dt, sc->f[T]);
         wp::bsync();
-        for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
-            const int slot = act[i];
-            if (st[slot] == ST_RUN) rem[slot] = wp::dsub(rem[slot], sc->q[w_k(gw[slot >> 3]) - 1]);
-        }
+#pragma unroll 4
+        for (uint32_t i = T; i < n_act; i += NT)
+            if (ast[i] == ST_RUN) arem[i] = wp::dsub(arem[i], sc->q[w_k(gw[aslot[i] >> 3]) - 1]);
         wp::bsync();
     }
 
     MSG_DI void reschedule() {  // sim.cpp:167-175
         wp::bsync();
-        for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
-            const int slot = act[i];
-            if (st[slot] == ST_RUN) {
-                double r = rem[slot];
+#pragma unroll 4
+        for (uint32_t i = T; i < n_act; i += NT) {
+            if (ast[i] == ST_RUN) {
+                double r = arem[i];
                 if (r < 0.0) r = 0.0;
-                tkey[slot] = wp::dadd(now, wp::dmul(r, sc->f[w_k(gw[slot >> 3]) - 1]));
+                atkey[i] = wp::dadd(now, wp::dmul(r, sc->f[w_k(gw[aslot[i] >> 3]) - 1]));
             }
         }
         wp::bsync();
@@ -350,18 +379,20 @@ struct ClusterSim {
     }
 
     // --------------------------------------------------------- next event
-    MSG_DI int next_event(int& ev_slot) {
+    // Returns the kind (-1 none, 0 completion, 1 migration end, 2 service
+    // start, 3 arrival) and, for slot timers, the active-list index.
+    MSG_DI int next_event(int& ev_i) {
         wp::bsync();
         unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
-        int bsl = -1;
-        for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
-            const int slot = act[i];
-            const uint8_t s = st[slot];
-            const uint64_t tk = time_key(tkey[slot]);
+        int bi = -1;
+#pragma unroll 4
+        for (uint32_t i = T; i < n_act; i += NT) {
+            const uint8_t s = ast[i];
+            const uint64_t tk = time_key(atkey[i]);
             const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;
             const unsigned kind = s == ST_RUN ? 0u : (s == ST_DRAIN ? 1u : 2u);
-            const unsigned tie = (kind << 28) | (unsigned)job[slot];
-            const unsigned ms = s == ST_DRAIN ? mseq[slot] : 0u;
+            const unsigned tie = (kind << 28) | (unsigned)ajob[i];
+            const unsigned ms = s == ST_DRAIN ? amseq[i] : 0u;
             const bool better =
                 hi < bhi || (hi == bhi && (lo < blo || (lo == blo && (tie < btie || (tie == btie && ms < bms)))));
             if (better) {
@@ -369,10 +400,10 @@ struct ClusterSim {
                 blo = lo;
                 btie = tie;
                 bms = ms;
-                bsl = slot;
+                bi = (int)i;
             }
         }
-        block_lexmin(bhi, blo, btie, bms, bsl);
+        block_lexmin(bhi, blo, btie, bms, bi);
         const bool have_arrival = a_idx < N;
         if (bhi == NONE) {
             if (!have_arrival) return -1;
@@ -383,8 +414,8 @@ struct ClusterSim {
             now = a_t;
             return 3;
         }
-        ev_slot = bsl;
-        now = tkey[bsl];
+        ev_i = bi;
+        now = atkey[bi];
         return (int)(btie >> 28);
     }
 
@@ -392,15 +423,13 @@ struct ClusterSim {
     MSG_DI Decision dispatch(int p) {  // scheduler.cpp:47-104
         wp::bsync();
         Decision d;
-        const unsigned smask = startmask_of(p);
         const unsigned n = count_of(p), stride = stride_of(p);
         const unsigned pb = pidx(p, 0);
         const bool dyn = (cflags & CF_DYN) != 0;
         const bool lb = (cflags & CF_LB) != 0;
-        (void)smask;
         uint64_t kmin = ~0ull;
         unsigned nl = 0, nb = 0;
-        for (uint64_t g = T; g < (uint64_t)G; g += wp::nthreads()) {
+        for (uint32_t g = T; g < (uint32_t)G; g += NT) {
             const unsigned wd = gw[g];
             const unsigned ex = gx[g] >> pb;
             const unsigned lazy = (lazymask >> wp::popc(w_bc(wd))) & 1u;
@@ -412,11 +441,11 @@ struct ClusterSim {
                     if (lb) {
                         const unsigned rk = rank2(w_bc(wd) | fpc(p, s), w_bm(wd) | fpm(p, s));
                         key = ((uint64_t)(lazy ^ 1u) << 47) | ((uint64_t)rk << 42) | ((uint64_t)(exact ? 0u : 1u) << 41) |
-                              (g << 3) | (uint64_t)s;
+                              ((uint64_t)g << 3) | (uint64_t)s;
                         nl += lazy;
                         nb += lazy ^ 1u;
                     } else {
-                        key = (g << 3) | (uint64_t)s;
+                        key = ((uint64_t)g << 3) | (uint64_t)s;
                     }
                     kmin = key < kmin ? key : kmin;
                 }
@@ -425,7 +454,11 @@ struct ClusterSim {
         unsigned hi = (unsigned)(kmin >> 32), lo = (unsigned)kmin, z0 = 0, z1 = 0;
         int pay = 0;
         block_lexmin(hi, lo, z0, z1, pay);
-        const unsigned NL = block_sum(nl), NB = block_sum(nb);
+        unsigned NL = 0, NB = 0;
+        if (lb) {
+            NL = block_sum(nl);
+            NB = block_sum(nb);
+        }
         const uint64_t k = ((uint64_t)hi << 32) | lo;
         d.placed = k != ~0ull;
         d.evals = lb ? NL + (NL == 0 ? NB : 0u) : 0u;
@@ -453,8 +486,7 @@ struct ClusterSim {
                 for (int t = 0; t < 8; ++t) {
                     if (st[b + t] == ST_IDLE && (fpm(prof[b + t], t) & fpm(p, s))) {
                         dmask |= 1u << t;
-                        // insertion by creation sequence
-                        int i = nd++;
+                        int i = nd++;  // insertion by creation sequence
                         while (i > 0 && cseq[b + sc->dl_slot[i - 1]] > cseq[b + t]) {
                             sc->dl_slot[i] = sc->dl_slot[i - 1];
                             sc->dl_prof[i] = sc->dl_prof[i - 1];
@@ -501,13 +533,11 @@ struct ClusterSim {
         const double ss = wp::dadd(now, delay);
         const int slot = 8 * g + s;
         if (T == 0) {
-            job[slot] = r;
+            const uint8_t v = delay > 0.0 ? ST_WAIT : ST_RUN;
+            st[slot] = v;
             mig[slot] = 0;
-            rem[slot] = sv;
-            st[slot] = delay > 0.0 ? ST_WAIT : ST_RUN;
-            tkey[slot] = ss;
+            act_add(n_act, slot, v, r, sv, ss, 0);
             jobs[r].sched = ss;
-            act_add(slot);
             refresh_gpu(g);
         }
         ++n_act;
@@ -541,14 +571,17 @@ struct ClusterSim {
     }
 
     // ------------------------------------------------------------ migration
-    MSG_DI void apply_move(int from_slot, int tg, int ts, bool inter) {  // migration.cpp:35-69
+    // apply_move (migration.cpp:35-69): the job keeps its active entry (its
+    // remaining work and timer move with it); with overlap > 0 the source
+    // slot gets a new entry carrying its MigrationEnd timer.
+    MSG_DI void apply_move(int from_slot, int tg, int ts, bool inter) {
         wp::bsync();
         const int fg = from_slot >> 3, fs = from_slot & 7;
         const int q = prof[from_slot];
-        const int32_t r = job[from_slot];
-        const uint8_t jst = st[from_slot];
-        const double jrem = rem[from_slot], jtk = tkey[from_slot];
+        const int ia = apos[from_slot];
+        const int32_t r = ajob[ia];
         const unsigned jmig = mig[from_slot];
+        const uint8_t jst = st[from_slot];
         const unsigned fcb = k2w(gw[fg]), tcb = k2w(gw[tg]);
         wp::bsync();
         if (T == 0) st[from_slot] = ST_DRAIN;  // start_draining
@@ -556,17 +589,14 @@ struct ClusterSim {
         if (T == 0) {
             const int dst = 8 * tg + ts;
             st[dst] = jst;
-            job[dst] = r;
             mig[dst] = (uint16_t)(jmig + 1u);
-            rem[dst] = jrem;
-            tkey[dst] = jtk;
-            act_add(dst);
+            aslot[ia] = dst;  // the job's entry follows it
+            apos[dst] = ia;
+            apos[from_slot] = -1;
             if (overlap <= 0.0) {
                 st[from_slot] = ST_IDLE;
-                act_remove(from_slot, n_act + 1);
             } else {
-                tkey[from_slot] = wp::dadd(now, overlap);
-                mseq[from_slot] = mseq_ctr;
+                act_add(n_act, from_slot, ST_DRAIN, r, 0.0, wp::dadd(now, overlap), mseq_ctr);
             }
             refresh_gpu(fg);
             if (tg != fg) refresh_gpu(tg);
@@ -599,7 +629,7 @@ struct ClusterSim {
                 unsigned kmin = NONE, cnt = 0;
                 if (s == ST_RUN || s == ST_WAIT) {
                     const int q = prof[sl];
-                    const unsigned r = (unsigned)job[sl];
+                    const unsigned r = (unsigned)ajob[apos[sl]];
                     const unsigned ofc = fpc(q, own), ofm = fpm(q, own);
                     const unsigned n = count_of(q), stride = stride_of(q);
                     for (int h = 0; h < 2; ++h) {
@@ -644,27 +674,28 @@ struct ClusterSim {
             const unsigned pl = tb->placeable[km0];
             unsigned bhi = NONE, blo = NONE, z0 = 0, z1 = 0, cnt = 0;
             int bsl = -1;
-            for (uint32_t i = T; i < n_act; i += wp::nthreads()) {
-                const int slot = act[i];
+            for (uint32_t i = T; i < n_act; i += NT) {
+                const uint8_t v = ast[i];
+                if (v != ST_RUN && v != ST_WAIT) continue;
+                const int slot = aslot[i];
                 const int g = slot >> 3, s = slot & 7;
-                const uint8_t v = st[slot];
-                if (g != g0 && (v == ST_RUN || v == ST_WAIT)) {
-                    const unsigned wd = gw[g];
-                    const unsigned src_cs = (unsigned)wp::popc(w_bc(wd));
-                    const int q = prof[slot];
-                    const unsigned cs = cs_of(q);
-                    if (!((lazymask >> src_cs) & 1u) && lazy_cs + cs < src_cs - cs && ((pl >> q) & 1u)) {
-                        const unsigned rk = rank2(w_bc(wd) & ~fpc(q, s), w_bm(wd) & ~fpm(q, s));
-                        // key (cost, gpu, job id): rank:5 | gpu:35 | job:24
-                        const uint64_t key = ((uint64_t)rk << 59) | ((uint64_t)g << 24) | (uint64_t)job[slot];
-                        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-                        if (hi < bhi || (hi == bhi && lo < blo)) {
-                            bhi = hi;
-                            blo = lo;
-                            bsl = slot;
-                        }
-                        ++cnt;
+                if (g == g0) continue;
+                const unsigned wd = gw[g];
+                const unsigned src_cs = (unsigned)wp::popc(w_bc(wd));
+                if ((lazymask >> src_cs) & 1u) continue;  // source must be Busy
+                const int q = prof[slot];
+                const unsigned cs = cs_of(q);
+                if (lazy_cs + cs < src_cs - cs && ((pl >> q) & 1u)) {
+                    const unsigned rk = rank2(w_bc(wd) & ~fpc(q, s), w_bm(wd) & ~fpm(q, s));
+                    // key (cost, gpu, job id): rank:5 | gpu:35 | job:24
+                    const uint64_t key = ((uint64_t)rk << 59) | ((uint64_t)g << 24) | (uint64_t)ajob[i];
+                    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+                    if (hi < bhi || (hi == bhi && lo < blo)) {
+                        bhi = hi;
+                        blo = lo;
+                        bsl = slot;
                     }
+                    ++cnt;
                 }
             }
             block_lexmin(bhi, blo, z0, z1, bsl);
@@ -723,10 +754,11 @@ struct ClusterSim {
         }
     }
 
-    MSG_DI void handle_departure(int slot, bool completion) {
+    MSG_DI void handle_departure(int ia, bool completion) {
         wp::bsync();
+        const int slot = aslot[ia];
         const int g = slot >> 3;
-        const int32_t r = job[slot];
+        const int32_t r = ajob[ia];
         const int m = mig[slot];
         wp::bsync();
         if (T == 0) {
@@ -751,10 +783,12 @@ struct ClusterSim {
         }
     }
 
-    MSG_DI void handle_service_start(int slot) {
+    MSG_DI void handle_service_start(int ia) {
         wp::bsync();
         if (T == 0) {
+            const int slot = aslot[ia];
             st[slot] = ST_RUN;
+            ast[ia] = ST_RUN;  // start_service: arem already holds service_s
             refresh_gpu(slot >> 3);
         }
         tl_dirty = true;
@@ -763,14 +797,14 @@ struct ClusterSim {
 
     MSG_DI void run() {
         for (;;) {
-            int slot = -1;
-            const int kind = next_event(slot);
+            int ia = -1;
+            const int kind = next_event(ia);
             if (kind < 0) break;
             ++n_handler;
             advance_all();
             if (kind == 3) handle_arrival();
-            else if (kind == 2) handle_service_start(slot);
-            else handle_departure(slot, kind == 0);
+            else if (kind == 2) handle_service_start(ia);
+            else handle_departure(ia, kind == 0);
             reschedule();
             sample();
         }
@@ -784,7 +818,7 @@ struct ClusterSim {
         s.pending_rank = -1;
         if (s.status != STATUS_OK) {
             unsigned mn = NONE;
-            for (uint32_t i = q_head + T; i < q_tail; i += wp::nthreads()) {
+            for (uint32_t i = q_head + T; i < q_tail; i += NT) {
                 const unsigned r = (unsigned)queue[i];
                 mn = r < mn ? r : mn;
             }
@@ -849,9 +883,10 @@ struct ClusterSim {
 };
 
 template <bool DETAIL>
-MSG_DI void simulate_large_trace(const SimArgs& a, const DevTables* tables, BlockScratch* sc, uint32_t t) {
+MSG_DI void simulate_large_trace(const SimArgs& a, const DevTables* tables, BlockScratch* sc,
+                                 unsigned char* gpu_smem, uint32_t t) {
     ClusterSim<DETAIL> sim;
-    sim.setup(a, tables, sc, t);
+    sim.setup(a, tables, sc, gpu_smem, t);
     sim.run();
     sim.finish(a.summary + t);
 }

@@ -132,19 +132,25 @@ struct SimArgs {
     const uint32_t* large_idx;
     uint32_t n_large;
     uint32_t reserved;
+    // per slot (8 per GPU)
     uint8_t* c_st;
     uint8_t* c_prof;
     uint16_t* c_mig;
     uint32_t* c_cseq;
-    int32_t* c_job;
-    uint32_t* c_mseq;
-    double* c_rem;
-    double* c_tkey;
-    int32_t* c_apos;
-    int32_t* c_act;
+    int32_t* c_apos;   // slot -> index in the active list, -1
+    // per active-list entry (capacity 8 per GPU): the slot's timer data
+    int32_t* c_aslot;
+    uint8_t* c_ast;
+    int32_t* c_ajob;
+    uint32_t* c_amseq;
+    double* c_arem;
+    double* c_atkey;
+    // per GPU (used only when they do not fit in shared memory)
     uint32_t* c_gw;
     uint32_t* c_gx;
     uint8_t* c_gcid;
+    uint32_t smem_gpus;  // per-GPU arrays live in shared memory for G <= smem_gpus (set by launch_cluster)
+    uint32_t max_gpus;   // largest G among the large traces
 };
 
 // Decision-level kernel arguments (decide.cu): one warp per cluster snapshot

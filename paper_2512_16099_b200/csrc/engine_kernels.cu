@@ -61,21 +61,53 @@ template <bool DETAIL>
 __global__ void __launch_bounds__(kClusterThreads, 1) cluster_kernel(SimArgs a) {
     __shared__ __align__(16) DevTables tb;
     __shared__ BlockScratch sc;
+    extern __shared__ __align__(16) unsigned char gpu_smem[];  // 9 B per GPU when G <= smem_gpus
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tables);
         uint4* dst = reinterpret_cast<uint4*>(&tb);
         for (unsigned i = threadIdx.x; i < sizeof(DevTables) / 16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    simulate_large_trace<DETAIL>(a, &tb, &sc, a.large_idx[blockIdx.x]);
+    const uint32_t t = a.large_idx[blockIdx.x];
+    const bool in_smem = (uint32_t)a.configs[a.traces[t].cfg].G <= a.smem_gpus;
+    simulate_large_trace<DETAIL>(a, &tb, &sc, in_smem ? gpu_smem : nullptr, t);
+}
+
+// Bytes of dynamic shared memory for the per-GPU words of G GPUs.
+static size_t gpu_smem_bytes(uint32_t G) { return ((size_t)G * 9 + 15) & ~(size_t)15; }
+
+template <bool DETAIL>
+static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
+    static int optin = -1;
+    static size_t static_smem = 0;
+    if (optin < 0) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa;
+        if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, cluster_kernel<DETAIL>);
+        if (e != cudaSuccess) return e;
+        static_smem = fa.sharedSizeBytes;
+    }
+    const size_t room = (size_t)optin > static_smem + 1024 ? (size_t)optin - static_smem - 1024 : 0;
+    size_t dyn = 0;
+    a.smem_gpus = 0;
+    if (gpu_smem_bytes(a.max_gpus) <= room) {
+        a.smem_gpus = a.max_gpus;
+        dyn = gpu_smem_bytes(a.max_gpus);
+    }
+    if (dyn > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(cluster_kernel<DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return e;
+    }
+    cluster_kernel<DETAIL><<<a.n_large, kClusterThreads, dyn, stream>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_cluster(const SimArgs& a, cudaStream_t stream) {
     if (!a.n_large) return cudaSuccess;
     const bool detail = (a.out_flags & (OF_EVENTS | OF_TIMELINE)) != 0;
-    if (detail) cluster_kernel<true><<<a.n_large, kClusterThreads, 0, stream>>>(a);
-    else cluster_kernel<false><<<a.n_large, kClusterThreads, 0, stream>>>(a);
-    return cudaGetLastError();
+    return detail ? launch_cluster_t<true>(a, stream) : launch_cluster_t<false>(a, stream);
 }
 
 cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream) {

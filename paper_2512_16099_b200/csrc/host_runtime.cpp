@@ -53,7 +53,9 @@ struct msg_staged {
     std::vector<uint32_t> large_idx;
     uint64_t large_gpus = 0;
     bool any_small = false;
-    DevBuf d_large_idx, c_st, c_prof, c_mig, c_cseq, c_job, c_mseq, c_rem, c_tkey, c_apos, c_act, c_gw, c_gx, c_gcid;
+    DevBuf d_large_idx, c_st, c_prof, c_mig, c_cseq, c_apos, c_aslot, c_ast, c_ajob, c_amseq, c_arem,
+        c_atkey, c_gw, c_gx, c_gcid;
+    uint32_t large_max_g = 0;
     // pinned host mirrors (rank order)
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
@@ -144,6 +146,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     int maxG = 1;
     s->large_idx.clear();
     s->large_gpus = 0;
+    s->large_max_g = 0;
     s->any_small = false;
     for (uint32_t t = 0; t < s->n_in; ++t) {
         const uint32_t ci = b->config_index ? b->config_index[t] : 0;
@@ -160,6 +163,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         if (tr.large) {
             tr.cl_goff = s->large_gpus;
             s->large_gpus += (uint64_t)cfgs[ci].gpu_count;
+            s->large_max_g = std::max(s->large_max_g, (uint32_t)cfgs[ci].gpu_count);
             s->large_idx.push_back((uint32_t)s->traces.size());
         } else {
             s->any_small = true;
@@ -227,12 +231,13 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         CK(s->c_prof.ensure(ns));
         CK(s->c_mig.ensure(ns * 2));
         CK(s->c_cseq.ensure(ns * 4));
-        CK(s->c_job.ensure(ns * 4));
-        CK(s->c_mseq.ensure(ns * 4));
-        CK(s->c_rem.ensure(ns * 8));
-        CK(s->c_tkey.ensure(ns * 8));
         CK(s->c_apos.ensure(ns * 4));
-        CK(s->c_act.ensure(ns * 4));
+        CK(s->c_aslot.ensure(ns * 4));
+        CK(s->c_ast.ensure(ns));
+        CK(s->c_ajob.ensure(ns * 4));
+        CK(s->c_amseq.ensure(ns * 4));
+        CK(s->c_arem.ensure(ns * 8));
+        CK(s->c_atkey.ensure(ns * 8));
         CK(s->c_gw.ensure(ng * 4));
         CK(s->c_gx.ensure(ng * 4));
         CK(s->c_gcid.ensure(ng));
@@ -283,12 +288,14 @@ SimArgs make_args(msg_engine* eng, msg_staged* s) {
         a.c_prof = s->c_prof.as<uint8_t>();
         a.c_mig = s->c_mig.as<uint16_t>();
         a.c_cseq = s->c_cseq.as<uint32_t>();
-        a.c_job = s->c_job.as<int32_t>();
-        a.c_mseq = s->c_mseq.as<uint32_t>();
-        a.c_rem = s->c_rem.as<double>();
-        a.c_tkey = s->c_tkey.as<double>();
         a.c_apos = s->c_apos.as<int32_t>();
-        a.c_act = s->c_act.as<int32_t>();
+        a.c_aslot = s->c_aslot.as<int32_t>();
+        a.c_ast = s->c_ast.as<uint8_t>();
+        a.c_ajob = s->c_ajob.as<int32_t>();
+        a.c_amseq = s->c_amseq.as<uint32_t>();
+        a.c_arem = s->c_arem.as<double>();
+        a.c_atkey = s->c_atkey.as<double>();
+        a.max_gpus = s->large_max_g;
         a.c_gw = s->c_gw.as<uint32_t>();
         a.c_gx = s->c_gx.as<uint32_t>();
         a.c_gcid = s->c_gcid.as<uint8_t>();

@@ -3,8 +3,8 @@
 // schedule() / first_fit_schedule() (scheduler.cpp:47-98) for snapshots of
 // any size: each GPU is one packed 64-bit state word (busy compute, busy
 // memory, blocked memory, 18 idle-exact placement bits; msg_pack_gpu_word).
-// A persistent grid streams 512-word chunks of the snapshots with 128-bit
-// loads (2 words per thread, the next chunk in flight), scores every legal
+// A persistent grid streams 1024-word chunks of the snapshots with 128-bit
+// loads (4 words per thread, the next chunk in flight), scores every legal
 // start of the job's profile — the profile is block-uniform, so the scoring
 // loop is specialised per profile with compile-time footprints — and keeps
 // a 32-bit block-local key [pass:1|cost rank:5|!reused:1|word:11|start:3]
@@ -24,7 +24,7 @@ namespace msgk {
 
 constexpr int kScoreThreads = 256;
 #ifndef MSG_SCORE_WPT
-#define MSG_SCORE_WPT 2
+#define MSG_SCORE_WPT 4
 #endif
 constexpr int kWordsPerThread = MSG_SCORE_WPT;  // 2 or 4 (one or two 128-bit loads)
 constexpr int kChunk = kScoreThreads * kWordsPerThread;  // words per chunk (<= 2048: 11-bit local index)
@@ -81,15 +81,13 @@ struct ChunkData {
     ulonglong2 v[kWordsPerThread / 2];
 };
 
-__device__ __forceinline__ ChunkData load_chunk(const ScoreArgs& a, uint64_t ch, uint64_t chunks_per) {
+__device__ __forceinline__ ChunkData load_chunk(const ScoreArgs& a, uint32_t snap, uint32_t c0) {
     ChunkData d;
-    const uint64_t snap = ch / chunks_per;
-    const uint64_t c0 = (ch % chunks_per) * kChunk;
-    const uint64_t* words = a.words + snap * a.G;
+    const uint64_t* words = a.words + (uint64_t)snap * a.G;
     const unsigned t2 = threadIdx.x * 2u;
 #pragma unroll
     for (int k = 0; k < kWordsPerThread / 2; ++k) {
-        const uint64_t g = c0 + t2 + (unsigned)k * 2 * kScoreThreads;
+        const uint64_t g = (uint64_t)c0 + t2 + (unsigned)k * 2 * kScoreThreads;
         if ((a.G & 1) == 0 && g + 1 < a.G) {
             d.v[k] = __ldcs(reinterpret_cast<const ulonglong2*>(words + g));
         } else {
@@ -137,17 +135,23 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreArgs a) {
         reinterpret_cast<uint4*>(lut)[i] = reinterpret_cast<const uint4*>(a.tables->cost2rank)[i];
     __syncthreads();
     const ScoreCfg c{a.lb, a.dyn, a.lazymask};
-    const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
-    const uint64_t total = chunks_per * a.n;
-    uint64_t ch = blockIdx.x;
+    // chunk ch = snap * chunks_per + j; advanced incrementally (no 64-bit divides)
+    const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
+    const uint32_t total = chunks_per * a.n;
+    uint32_t ch = blockIdx.x;
     if (ch >= total) return;
-    ChunkData cur = load_chunk(a, ch, chunks_per);
+    uint32_t snap = ch / chunks_per, j = ch - snap * chunks_per;
+    const uint32_t step_s = gridDim.x / chunks_per, step_j = gridDim.x - step_s * chunks_per;
+    ChunkData cur = load_chunk(a, snap, j * kChunk);
     for (; ch < total; ch += gridDim.x) {
-        const uint64_t nxt = ch + gridDim.x;
+        uint32_t nsnap = snap + step_s, nj = j + step_j;
+        if (nj >= chunks_per) {
+            nj -= chunks_per;
+            ++nsnap;
+        }
         ChunkData next;
-        if (nxt < total) next = load_chunk(a, nxt, chunks_per);
-        const uint64_t snap = ch / chunks_per;
-        const uint64_t c0 = (ch % chunks_per) * kChunk;
+        if (ch + gridDim.x < total) next = load_chunk(a, nsnap, nj * kChunk);
+        const uint64_t c0 = (uint64_t)j * kChunk;
         switch (a.profile[snap]) {
             case 0: score_chunk<0, LB>(a, c, lut, cur, snap, c0); break;
             case 1: score_chunk<1, LB>(a, c, lut, cur, snap, c0); break;
@@ -157,6 +161,8 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreArgs a) {
             default: score_chunk<5, LB>(a, c, lut, cur, snap, c0); break;
         }
         cur = next;
+        snap = nsnap;
+        j = nj;
     }
 }
 
@@ -178,6 +184,7 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const uint64_t chunks = ((a.G + kChunk - 1) / kChunk) * a.n;
+    if (chunks > 0xFFFFFFFFull) return cudaErrorInvalidValue;
     const uint64_t blocks = std::min<uint64_t>(chunks, (uint64_t)sms * 8);  // 8 x 256 threads per SM
     if (a.lb) score_kernel<true><<<(unsigned)blocks, kScoreThreads, 0, stream>>>(a);
     else score_kernel<false><<<(unsigned)blocks, kScoreThreads, 0, stream>>>(a);

@@ -43,7 +43,7 @@ void run_warp(const SimArgs& a, const DevTables* tb) {
 }
 
 // Block engine (G > 32) on `nt` emulated threads (nt/32 warps + a block barrier).
-void run_block(const SimArgs& a, const DevTables* tb, unsigned nt) {
+void run_block(const SimArgs& a, const DevTables* tb, unsigned nt, unsigned char* gpu_smem) {
     auto sc = std::make_unique<BlockScratch>();
     std::memset(sc.get(), 0xA5, sizeof(BlockScratch));
     wp::EmuBlock block;
@@ -58,7 +58,7 @@ void run_block(const SimArgs& a, const DevTables* tb, unsigned nt) {
             wp::g_lane = t % 32;
             wp::g_tid = t;
             wp::g_phase = 0;
-            simulate_large_trace<true>(a, tb, sc.get(), 0);
+            simulate_large_trace<true>(a, tb, sc.get(), gpu_smem, 0);
         });
     for (auto& x : th) x.join();
 }
@@ -122,9 +122,11 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
     const size_t ns = 8 * (size_t)G;
     std::vector<uint8_t> c_st(ns), c_prof(ns), c_gcid(G);
     std::vector<uint16_t> c_mig(ns);
-    std::vector<uint32_t> c_cseq(ns), c_mseq(ns), c_gw(G), c_gx(G);
-    std::vector<int32_t> c_job(ns), c_apos(ns), c_act(ns);
-    std::vector<double> c_rem(ns), c_tkey(ns);
+    std::vector<uint32_t> c_cseq(ns), c_amseq(ns), c_gw(G), c_gx(G);
+    std::vector<int32_t> c_aslot(ns), c_apos(ns), c_ajob(ns);
+    std::vector<uint8_t> c_ast(ns);
+    std::vector<double> c_arem(ns), c_atkey(ns);
+    std::vector<unsigned char> gpu_smem(9 * (size_t)G + 16, 0xA5);  // stands in for dynamic smem
     uint32_t large_idx = 0;
     const bool block = G > 32 || std::getenv("MSG_EMU_FORCE_BLOCK") != nullptr;
     if (block) {
@@ -136,17 +138,22 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
         a.c_prof = c_prof.data();
         a.c_mig = c_mig.data();
         a.c_cseq = c_cseq.data();
-        a.c_job = c_job.data();
-        a.c_mseq = c_mseq.data();
-        a.c_rem = c_rem.data();
-        a.c_tkey = c_tkey.data();
         a.c_apos = c_apos.data();
-        a.c_act = c_act.data();
+        a.c_aslot = c_aslot.data();
+        a.c_ast = c_ast.data();
+        a.c_ajob = c_ajob.data();
+        a.c_amseq = c_amseq.data();
+        a.c_arem = c_arem.data();
+        a.c_atkey = c_atkey.data();
         a.c_gw = c_gw.data();
         a.c_gx = c_gx.data();
         a.c_gcid = c_gcid.data();
         const char* nt = std::getenv("MSG_EMU_BLOCK_THREADS");
-        run_block(a, &tables, nt ? (unsigned)std::atoi(nt) : 64u);
+        const char* gs = std::getenv("MSG_EMU_GPU_SMEM");  // "0": per-GPU words in global memory
+        const bool smem = !(gs && gs[0] == '0');
+        a.max_gpus = (uint32_t)G;
+        a.smem_gpus = smem ? (uint32_t)G : 0u;
+        run_block(a, &tables, nt ? (unsigned)std::atoi(nt) : 64u, smem ? gpu_smem.data() : nullptr);
     } else if (G <= 4) run_warp<1>(a, &tables);
     else if (G <= 8) run_warp<2>(a, &tables);
     else if (G <= 16) run_warp<4>(a, &tables);

@@ -15,7 +15,8 @@ pytestmark = pytest.mark.skipif(not rb.ref_available(), reason="reference librar
 
 @pytest.fixture
 def block_env(monkeypatch):
-    def set_(force=False, threads=64):
+    def set_(force=False, threads=64, gpu_smem=True):
+        monkeypatch.setenv("MSG_EMU_GPU_SMEM", "1" if gpu_smem else "0")
         if force:
             monkeypatch.setenv("MSG_EMU_FORCE_BLOCK", "1")
         else:
@@ -35,7 +36,7 @@ def _check(spec, cfg, seeds, relaxed=False):
 
 @pytest.mark.parametrize("threads", [32, 64, 96])
 def test_block_engine_on_small_clusters_matches(block_env, threads):
-    block_env(force=True, threads=threads)
+    block_env(force=True, threads=threads, gpu_smem=threads != 64)
     _check(preset("normal25"), SimConfig(gpu_count=8), [0, 1])
     c5 = WorkloadSpec(mean_interarrival_s=0.4, median_s=4.0, sigma=1.2, profile_mix=(0.5, 0.3, 0.2, 0.0))
     _check(c5, SimConfig(gpu_count=8, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
@@ -47,8 +48,9 @@ def test_block_engine_on_small_clusters_matches(block_env, threads):
                [3])
 
 
-def test_block_engine_large_clusters(block_env):
-    block_env(force=False, threads=64)
+@pytest.mark.parametrize("gpu_smem", [True, False])
+def test_block_engine_large_clusters(block_env, gpu_smem):
+    block_env(force=False, threads=64, gpu_smem=gpu_smem)
     sp = preset("normal25")
     sp.mean_interarrival_s = 25.0 / 12
     sp.job_count = 400
