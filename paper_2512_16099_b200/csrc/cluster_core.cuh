@@ -1,37 +1,73 @@
 // cluster_core.cuh — the event loop for LARGE clusters (G > 32 GPUs, up to
-// the 16384-GPU C4 configuration): one thread block replays one trace of the
-// reference's discrete-event scheduler (proj/src/sim.cpp:71-410).
+// the 16384-GPU C4 configuration): one thread-block CLUSTER of S CTAs
+// replays one trace of the reference's discrete-event scheduler
+// (proj/src/sim.cpp:71-410); S = 1 is a single block.
 //
-// Same semantics and the same packed-key decisions as the warp engine
-// (engine_core.cuh), laid out for thousands of GPUs:
+// Sharding.  CTA `sh` (a SHARD) owns the contiguous GPU range
+// [G*sh/S, G*(sh+1)/S) and everything that lives on it:
 //   * per GPU: mask word (busy compute | busy memory | blocked memory |
 //     running count), idle-exact placement bits, 4-mask cost id — in SHARED
-//     memory (9 B/GPU, up to ~24K GPUs), else global;
+//     memory (9 B/GPU), else global;
 //   * per (GPU, start) slot: instance state, profile, creation sequence,
 //     migrations of the bound job, position in the active list — global
 //     (L2-resident);
-//   * the ACTIVE list holds every slot that carries a timer (running, waiting
-//     for service start, draining) with the timer data stored densely by list
-//     index (time, state, job, remaining work, MigrationEnd sequence): the
-//     per-event scans (next event, advance_all, reschedule, plan_inter
-//     sources) are coalesced, indirection-free loops over ~R entries,
-//     unrolled for memory-level parallelism; a migrating job keeps its entry
-//     (only the slot changes);
-//   * GPU-local steps (create_instance, refresh of a GPU word) run on one
-//     thread; plan_intra on warp 0; schedule, plan_inter and the next-event
-//     search are block-wide argmins over packed keys: per-warp REDUX chain,
-//     then one __syncthreads and the same chain over the warp winners.
+//   * the shard's ACTIVE list: every slot of its GPUs that carries a timer
+//     (running, waiting for service start, draining) with the timer data
+//     stored densely by list index (time, state, job, remaining work,
+//     MigrationEnd order): the per-event scans (next event, advance_all,
+//     reschedule, plan_inter sources) are coalesced loops over ~R/S entries;
+//   * the shard's part of the integer fragmentation-cost total.
+// Replicated in every shard (identical, because every input to them is
+// either replicated or exchanged): the clock, the arrival cursor, the FCFS
+// queue, the decision counters.
+//
+// Exchange.  Every decision that spans shards is one EXCHANGE: each shard
+// reduces its own candidates block-wide (per-warp REDUX chain, one
+// __syncthreads, the same chain over the warp winners) into one
+// record (88 B), writes it to its shared memory, and after one cluster barrier
+// warp 0 of every shard reads all S records through distributed shared
+// memory (mapa) and reduces them identically: lexicographic minimum key
+// (with the winner's payload: the migrating job's slot, state, remaining
+// work and timer), sums (candidate counts, cost-total parts) and ORs (the
+// GPU word its owner broadcasts).  Records are double-buffered by round
+// parity, so one barrier per exchange suffices.  Exchanges per handler:
+//   next event (always) · one per placement attempt (arrival, dequeue pass)
+//   · on a completion with migration: one broadcasting the departed GPU's
+//   word (Lazy/Busy) and, if Lazy, one per plan_inter iteration.
+// plan_intra, create_instance and the placement itself are owner-local.
+// Fragmentation-timeline samples are deferred: each shard queues its part
+// of the cost total at the sample point and the next exchange sums them.
+//
+// The MigrationEnd tie order (same job, same time: push order,
+// sim.cpp:49-56) uses the job's migration count at the move, which grows
+// with every move of the job — equivalent to the reference's global push
+// sequence for every comparison that can tie, and shard-independent.
+//
 // Bit-exact with the reference, except the fragmentation timeline above
 // kExactTimelineGpus GPUs: there the per-sample mean is
 // RN(RN(sum_g k_g / 25200) / G) from the exact integer sum of the per-GPU
 // cost numerators instead of the reference's sequential double sum (relative
-// difference <= G * 2^-53, i.e. < 2e-12 at 16384 GPUs; SURVEY §7 hard part 6).
+// difference <= G * 2^-53, i.e. < 2e-12 at 16384 GPUs; SURVEY §7 hard part
+// 6).  S > 1 is used only above that size and without the event log.
 #pragma once
 #include "engine_core.cuh"
 
 namespace msgk {
 
-constexpr int kExactTimelineGpus = 512;
+// One shard's contribution to an exchange (and, after it, the reduction).
+struct XRec {
+    unsigned hi, lo, tie, ms;  // key, lexicographic minimum wins
+    int32_t slot;              // winner payload: global slot
+    int32_t job;               //   job rank
+    uint32_t info;             //   slot state | profile << 8 | job migrations << 16
+    uint32_t w;                // OR: word broadcast by a GPU's owner
+    double rem, tkey;          //   remaining work, timer time
+    uint32_t c[4];             // sums
+    uint32_t mx;               // max
+    uint32_t pad;
+    uint64_t ks[2];            // sums: deferred timeline samples (cost-total parts)
+};
+static_assert(sizeof(XRec) == 88, "exchange record layout");
 
 struct BlockScratch {
     unsigned hi[2][32], lo[2][32], tie[2][32], ms[2][32];
@@ -42,28 +78,30 @@ struct BlockScratch {
     unsigned u[8];     // small broadcasts from one thread / warp 0
     int dl_slot[8];    // create_instance: destroyed starts in creation order
     int dl_prof[8];
-    unsigned long long ksum;  // sum of per-GPU 4-mask cost numerators
+    unsigned long long ksum;  // this shard's sum of per-GPU 4-mask cost numerators
     double tl;
+    XRec xb[2];        // this shard's exchange records (read by the cluster)
+    XRec xr;           // reduced record
 };
 
 template <bool DETAIL>
 struct ClusterSim {
     BlockScratch* sc;
     const DevTables* tb;
-    // per slot
+    // per slot (global slot index 8g + s)
     uint8_t* st;
     uint8_t* prof;
     uint16_t* mig;
     uint32_t* cseq;
     int32_t* apos;
-    // per active entry
+    // per active entry of this shard
     int32_t* aslot;
     uint8_t* ast;
     int32_t* ajob;
     uint32_t* amseq;
     double* arem;
     double* atkey;
-    // per GPU
+    // per owned GPU (index g - g_lo)
     uint32_t* gw;
     uint32_t* gx;
     uint8_t* gcid;
@@ -79,19 +117,27 @@ struct ClusterSim {
     int G;
     uint32_t cflags, lazymask;
     double alpha, overlap, latency, inv_g;
+    // shard geometry
+    unsigned S, sh;
+    int g_lo, g_hi;
     // block-uniform state (every thread holds the same values)
     unsigned T, W, L, w, NT;  // thread, warp, lane, warps, threads
     int bph;                  // scratch double-buffer parity
+    uint32_t xround;          // exchanges so far
     double now, t_prev;
     uint32_t a_idx, a_rank;
     int a_prof;
     double a_t, a_svc;
     uint32_t q_head, q_tail, n_act;
-    uint32_t cseq_ctr, mseq_ctr;
+    uint32_t cseq_ctr;
     uint32_t n_ev, n_handler, n_tl, n_mig, n_reconf, n_enq, n_deq;
     int max_arr, max_intra, max_inter;
     double tl_sum, tl_mean;
     bool tl_dirty;
+    // deferred timeline samples (S > 1)
+    uint32_t npend;
+    double pend_t[2];
+    unsigned long long pend_k[2];
 
     // ------------------------------------------------------------- tables
     MSG_DI unsigned rank2(unsigned bc, unsigned bm) const { return tb->cost2rank[wp::popc(bc) * 256 + bm]; }
@@ -99,6 +145,8 @@ struct ClusterSim {
     MSG_DI static unsigned pidx(int p, int s) {  // idle-exact bit of placement (p, s)
         return ((0x00B74210u >> (4 * p)) & 0xFu) + (unsigned)s / stride_of(p);
     }
+    MSG_DI bool own(int g) const { return g >= g_lo && g < g_hi; }
+    MSG_DI unsigned& W_(int g) { return gw[g - g_lo]; }  // owned GPU's mask word
 
     // ----------------------------------------------------- block reductions
     // Lexicographic (hi, lo, tie, ms) minimum within the warp; every lane
@@ -145,7 +193,68 @@ struct ClusterSim {
         return x;
     }
 
+    // ----------------------------------------------------------- exchange
+    MSG_DI static XRec xnone() {
+        XRec r;
+        r.hi = r.lo = r.tie = r.ms = NONE;
+        r.slot = -1;
+        r.job = -1;
+        r.info = 0;
+        r.w = 0;
+        r.rem = r.tkey = 0.0;
+        r.c[0] = r.c[1] = r.c[2] = r.c[3] = 0;
+        r.mx = 0;
+        r.pad = 0;
+        r.ks[0] = r.ks[1] = 0;
+        return r;
+    }
+    // Cluster-wide reduction of one record per shard (see the header).  The
+    // caller passes a block-uniform record; every thread of every shard
+    // returns the same reduced record.  Deferred timeline samples ride along.
+    MSG_DI void exchange(XRec& r) {
+        if (S == 1) return;
+        r.ks[0] = npend > 0 ? pend_k[0] : 0ull;
+        r.ks[1] = npend > 1 ? pend_k[1] : 0ull;
+        XRec* mine = &sc->xb[xround & 1u];
+        if (T == 0) *mine = r;
+        wp::cluster_sync();
+        if (W == 0) {
+            XRec x = L < S ? *wp::cluster_map(mine, L) : xnone();
+            int pay = (int)L;
+            unsigned hi = x.hi, lo = x.lo, tie = x.tie, ms = x.ms;
+            warp_lexmin(hi, lo, tie, ms, pay);
+            XRec o;
+            o.hi = hi;
+            o.lo = lo;
+            o.tie = tie;
+            o.ms = ms;
+            o.slot = wp::shfl(x.slot, pay);
+            o.job = wp::shfl(x.job, pay);
+            o.info = wp::shfl(x.info, pay);
+            o.rem = wp::shfl(x.rem, pay);
+            o.tkey = wp::shfl(x.tkey, pay);
+            o.w = wp::ror(x.w);
+            for (int k = 0; k < 4; ++k) o.c[k] = wp::radd(x.c[k]);
+            o.mx = wp::rmax(x.mx);
+            o.pad = 0;
+            for (int k = 0; k < 2; ++k) {  // parts < 2^35: 20-bit split keeps the lane sums in 32 bits
+                const unsigned lo20 = wp::radd((unsigned)(x.ks[k] & 0xFFFFFu));
+                const unsigned hi20 = wp::radd((unsigned)(x.ks[k] >> 20));
+                o.ks[k] = ((unsigned long long)hi20 << 20) + lo20;
+            }
+            if (L == 0) sc->xr = o;
+        }
+        wp::bsync();
+        r = sc->xr;
+        ++xround;
+        // deferred timeline samples, in order
+        for (uint32_t i = 0; i < npend; ++i) record_sample(pend_t[i], r.ks[i]);
+        npend = 0;
+    }
+
     // --------------------------------------------------------------- events
+    // Only the shard that owns an event emits (and counts) it; replicated
+    // events belong to shard 0.
     MSG_DI void emit(uint8_t kind, int32_t jb, unsigned gpu, unsigned gpu2, unsigned pr, unsigned start,
                      unsigned start2, unsigned flags, uint64_t aux) {
         if (DETAIL && (oflags & OF_EVENTS) && n_ev < ev_cap && T == 0) {
@@ -167,7 +276,7 @@ struct ClusterSim {
     }
 
     // ---------------------------------------------------------------- setup
-    // gpu_smem: 9 B per GPU of dynamic shared memory, or nullptr (global).
+    // gpu_smem: 9 B per owned GPU of dynamic shared memory, or nullptr (global).
     MSG_DI void setup(const SimArgs& a, const DevTables* tables, BlockScratch* scratch, unsigned char* gpu_smem,
                       uint32_t t) {
         T = wp::tid();
@@ -178,29 +287,37 @@ struct ClusterSim {
         bph = 0;
         sc = scratch;
         tb = tables;
+        S = wp::cluster_size();
+        sh = wp::cluster_rank();
+        xround = 0;
+        npend = 0;
         const DevTrace tr = a.traces[t];
         const DevConfig c = a.configs[tr.cfg];
         G = c.G;
+        g_lo = (int)((uint64_t)G * sh / S);
+        g_hi = (int)((uint64_t)G * (sh + 1) / S);
         const uint64_t go = tr.cl_goff, so = 8 * go;
         st = a.c_st + so;
         prof = a.c_prof + so;
         mig = a.c_mig + so;
         cseq = a.c_cseq + so;
         apos = a.c_apos + so;
-        aslot = a.c_aslot + so;
-        ast = a.c_ast + so;
-        ajob = a.c_ajob + so;
-        amseq = a.c_amseq + so;
-        arem = a.c_arem + so;
-        atkey = a.c_atkey + so;
+        const uint64_t ao = so + 8ull * (uint64_t)g_lo;  // this shard's active-list arena (8 per owned GPU)
+        aslot = a.c_aslot + ao;
+        ast = a.c_ast + ao;
+        ajob = a.c_ajob + ao;
+        amseq = a.c_amseq + ao;
+        arem = a.c_arem + ao;
+        atkey = a.c_atkey + ao;
+        const int ng = g_hi - g_lo;
         if (gpu_smem) {
             gw = reinterpret_cast<uint32_t*>(gpu_smem);
-            gx = gw + G;
-            gcid = reinterpret_cast<uint8_t*>(gx + G);
+            gx = gw + ng;
+            gcid = reinterpret_cast<uint8_t*>(gx + ng);
         } else {
-            gw = a.c_gw + go;
-            gx = a.c_gx + go;
-            gcid = a.c_gcid + go;
+            gw = a.c_gw + go + g_lo;
+            gx = a.c_gx + go + g_lo;
+            gcid = a.c_gcid + go + g_lo;
         }
         N = tr.n_jobs;
         arr = a.arrival + tr.job_off;
@@ -226,36 +343,39 @@ struct ClusterSim {
         a_idx = 0;
         q_head = q_tail = 0;
         n_act = 0;
-        mseq_ctr = 0;
         n_ev = n_handler = n_tl = n_mig = n_reconf = n_enq = n_deq = 0;
         max_arr = max_intra = max_inter = 0;
         tl_sum = tl_mean = 0.0;
         tl_dirty = true;
-        for (uint64_t i = T; i < 8ull * G; i += NT) {
+        for (uint64_t i = 8ull * g_lo + T; i < 8ull * g_hi; i += NT) {
             st[i] = ST_EMPTY;
             mig[i] = 0;
             apos[i] = -1;
         }
         // empty GPU: masks 0, cost id of frag 0 (every profile fully feasible)
         const uint8_t empty_id = tb->cost4pair[tb->idealid[0] * 32u + tb->feasid[0]];
-        for (uint64_t g = T; g < (uint64_t)G; g += NT) {
+        for (int g = (int)T; g < ng; g += (int)NT) {
             gw[g] = 0;
             gx[g] = 0;
             gcid[g] = empty_id;
         }
         if (T < 7) sc->f[T] = wp::dadd(1.0, wp::dmul(alpha, (double)(int)T));  // slowdown(T+1)
-        if (T == 0) sc->ksum = (unsigned long long)tb->cost4k[empty_id] * (unsigned long long)G;
+        if (T == 0) sc->ksum = (unsigned long long)tb->cost4k[empty_id] * (unsigned long long)ng;
         wp::bsync();
-        // static layout (sim.cpp:86-95)
+        // static layout (sim.cpp:86-95), owned instances
         if (T == 0) {
             for (uint32_t k = 0; k < c.n_init; ++k) {
                 const uint32_t v = a.init_slots[c.init_off + k];
                 const int slot = (int)(v & 0xFFFFFFu);
+                if (!own(slot >> 3)) continue;
                 st[slot] = ST_IDLE;
                 prof[slot] = (uint8_t)(v >> 24);
                 cseq[slot] = k;
             }
-            for (uint32_t k = 0; k < c.n_init; ++k) refresh_gpu((int)((a.init_slots[c.init_off + k] & 0xFFFFFFu) >> 3));
+            for (uint32_t k = 0; k < c.n_init; ++k) {
+                const int g = (int)((a.init_slots[c.init_off + k] & 0xFFFFFFu) >> 3);
+                if (own(g)) refresh_gpu(g);
+            }
         }
         cseq_ctr = c.n_init;
         load_arrival();
@@ -274,7 +394,7 @@ struct ClusterSim {
 
     // ------------------------------------------- GPU words (single thread)
     // busy/blocked masks (gpu.cpp:10-48), running count, idle-exact
-    // placements, 4-mask cost id; keeps the integer cost total current.
+    // placements, 4-mask cost id; keeps the shard's integer cost total current.
     MSG_DI void refresh_gpu(int g) {
         unsigned bc = 0, bm = 0, km = 0, k = 0, x = 0;
         for (int s = 0; s < 8; ++s) {
@@ -293,12 +413,13 @@ struct ClusterSim {
                 k += v == ST_RUN;
             }
         }
-        gw[g] = bc | (bm << 8) | (km << 16) | (k << 24);
-        gx[g] = x;
+        const int l = g - g_lo;
+        gw[l] = bc | (bm << 8) | (km << 16) | (k << 24);
+        gx[l] = x;
         const unsigned row = (unsigned)wp::popc(bc) * 9u + (unsigned)wp::popc(bm);
         const uint8_t id = tb->cost4pair[tb->idealid[row] * 32u + tb->feasid[km]];
-        sc->ksum += (unsigned long long)tb->cost4k[id] - (unsigned long long)tb->cost4k[gcid[g]];
-        gcid[g] = id;
+        sc->ksum += (unsigned long long)tb->cost4k[id] - (unsigned long long)tb->cost4k[gcid[l]];
+        gcid[l] = id;
     }
 
     // ------------------------------------------ active list (single thread)
@@ -336,7 +457,7 @@ struct ClusterSim {
         wp::bsync();
 #pragma unroll 4
         for (uint32_t i = T; i < n_act; i += NT)
-            if (ast[i] == ST_RUN) arem[i] = wp::dsub(arem[i], sc->q[w_k(gw[aslot[i] >> 3]) - 1]);
+            if (ast[i] == ST_RUN) arem[i] = wp::dsub(arem[i], sc->q[w_k(W_(aslot[i] >> 3)) - 1]);
         wp::bsync();
     }
 
@@ -347,13 +468,32 @@ struct ClusterSim {
             if (ast[i] == ST_RUN) {
                 double r = arem[i];
                 if (r < 0.0) r = 0.0;
-                atkey[i] = wp::dadd(now, wp::dmul(r, sc->f[w_k(gw[aslot[i] >> 3]) - 1]));
+                atkey[i] = wp::dadd(now, wp::dmul(r, sc->f[w_k(W_(aslot[i] >> 3)) - 1]));
             }
         }
         wp::bsync();
     }
 
+    MSG_DI void record_sample(double t, unsigned long long ktot) {
+        const double tot = wp::ddiv((double)ktot, 25200.0);
+        tl_mean = inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
+        if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && T == 0 && sh == 0) {
+            tl[2 * n_tl] = t;
+            tl[2 * n_tl + 1] = tl_mean;
+        }
+        ++n_tl;
+        tl_sum = wp::dadd(tl_sum, tl_mean);
+    }
+
     MSG_DI void sample() {  // sim.cpp:177-181
+        if (S > 1) {  // deferred: the next exchange sums the shards' parts
+            wp::bsync();
+            pend_t[npend] = now;
+            pend_k[npend] = sc->ksum;
+            ++npend;
+            wp::bsync();
+            return;
+        }
         if (tl_dirty) {
             wp::bsync();
             if (T == 0) {
@@ -380,8 +520,9 @@ struct ClusterSim {
 
     // --------------------------------------------------------- next event
     // Returns the kind (-1 none, 0 completion, 1 migration end, 2 service
-    // start, 3 arrival) and, for slot timers, the active-list index.
-    MSG_DI int next_event(int& ev_i) {
+    // start, 3 arrival); for slot timers `slot` is the global slot and
+    // `ev_i` its index in this shard's active list (-1 on other shards).
+    MSG_DI int next_event(int& slot, int& ev_i) {
         wp::bsync();
         unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
         int bi = -1;
@@ -404,7 +545,29 @@ struct ClusterSim {
             }
         }
         block_lexmin(bhi, blo, btie, bms, bi);
+        double tmin = 0.0;
+        slot = -1;
+        if (bhi != NONE) {
+            tmin = atkey[bi];
+            slot = aslot[bi];
+        }
+        if (S > 1) {
+            XRec r = xnone();
+            r.hi = bhi;
+            r.lo = blo;
+            r.tie = btie;
+            r.ms = bms;
+            r.slot = slot;
+            r.tkey = tmin;
+            exchange(r);
+            bhi = r.hi;
+            blo = r.lo;
+            btie = r.tie;
+            slot = r.slot;
+            tmin = r.tkey;
+        }
         const bool have_arrival = a_idx < N;
+        ev_i = -1;
         if (bhi == NONE) {
             if (!have_arrival) return -1;
             now = a_t;
@@ -414,8 +577,8 @@ struct ClusterSim {
             now = a_t;
             return 3;
         }
-        ev_i = bi;
-        now = atkey[bi];
+        if (own(slot >> 3)) ev_i = apos[slot];
+        now = tmin;
         return (int)(btie >> 28);
     }
 
@@ -429,9 +592,9 @@ struct ClusterSim {
         const bool lb = (cflags & CF_LB) != 0;
         uint64_t kmin = ~0ull;
         unsigned nl = 0, nb = 0;
-        for (uint32_t g = T; g < (uint32_t)G; g += NT) {
-            const unsigned wd = gw[g];
-            const unsigned ex = gx[g] >> pb;
+        for (int g = g_lo + (int)T; g < g_hi; g += (int)NT) {
+            const unsigned wd = gw[g - g_lo];
+            const unsigned ex = gx[g - g_lo] >> pb;
             const unsigned lazy = (lazymask >> wp::popc(w_bc(wd))) & 1u;
             for (unsigned j = 0; j < n; ++j) {
                 const int s = (int)(j * stride);
@@ -459,6 +622,19 @@ struct ClusterSim {
             NL = block_sum(nl);
             NB = block_sum(nb);
         }
+        if (S > 1) {
+            XRec r = xnone();
+            r.hi = hi;
+            r.lo = lo;
+            r.tie = r.ms = 0;
+            r.c[0] = NL;
+            r.c[1] = NB;
+            exchange(r);
+            hi = r.hi;
+            lo = r.lo;
+            NL = r.c[0];
+            NB = r.c[1];
+        }
         const uint64_t k = ((uint64_t)hi << 32) | lo;
         d.placed = k != ~0ull;
         d.evals = lb ? NL + (NL == 0 ? NB : 0u) : 0u;
@@ -467,14 +643,14 @@ struct ClusterSim {
         d.reused = false;
         if (d.placed) {
             if (lb) d.reused = ((k >> 41) & 1u) == 0;
-            else d.reused = (gx[d.g] >> pidx(p, d.s)) & 1u;
+            else if (own(d.g)) d.reused = (gx[d.g - g_lo] >> pidx(p, d.s)) & 1u;
         }
         return d;
     }
 
     // ---------------------------------------------------- create_instance
-    // gpu.cpp:71-101 on one thread; destroyed instances are listed in
-    // creation order for the Reconfig events.
+    // gpu.cpp:71-101 on one thread of the GPU's owner; destroyed instances
+    // are listed in creation order for the Reconfig events.
     MSG_DI CreateRes create(int g, int p, int s) {
         wp::bsync();
         if (T == 0) {
@@ -546,7 +722,9 @@ struct ClusterSim {
         return ss;
     }
 
+    // The decided placement, on the GPU's owner only.
     MSG_DI void place(const Decision& d, int32_t r, int p, double sv, uint8_t kind) {
+        if (!own(d.g)) return;
         const CreateRes cr = create(d.g, p, d.s);
         const unsigned nops = (unsigned)wp::popc(cr.dmask) + (cr.reused ? 0u : 1u);
         const double ss = apply_placement(d.g, d.s, r, sv, nops);
@@ -571,23 +749,24 @@ struct ClusterSim {
     }
 
     // ------------------------------------------------------------ migration
-    // apply_move (migration.cpp:35-69): the job keeps its active entry (its
-    // remaining work and timer move with it); with overlap > 0 the source
-    // slot gets a new entry carrying its MigrationEnd timer.
-    MSG_DI void apply_move(int from_slot, int tg, int ts, bool inter) {
+    // apply_move (migration.cpp:35-69) within one GPU (plan_intra, owner
+    // only): the job keeps its active entry (its remaining work and timer
+    // move with it); with overlap > 0 the source slot gets a new entry
+    // carrying its MigrationEnd timer.
+    MSG_DI void apply_move_intra(int from_slot, int ts) {
         wp::bsync();
-        const int fg = from_slot >> 3, fs = from_slot & 7;
+        const int g = from_slot >> 3, fs = from_slot & 7;
         const int q = prof[from_slot];
         const int ia = apos[from_slot];
         const int32_t r = ajob[ia];
         const unsigned jmig = mig[from_slot];
         const uint8_t jst = st[from_slot];
-        const unsigned fcb = k2w(gw[fg]), tcb = k2w(gw[tg]);
+        const unsigned cb = k2w(W_(g));
         wp::bsync();
         if (T == 0) st[from_slot] = ST_DRAIN;  // start_draining
-        const CreateRes cr = create(tg, q, ts);
+        const CreateRes cr = create(g, q, ts);
         if (T == 0) {
-            const int dst = 8 * tg + ts;
+            const int dst = 8 * g + ts;
             st[dst] = jst;
             mig[dst] = (uint16_t)(jmig + 1u);
             aslot[ia] = dst;  // the job's entry follows it
@@ -596,47 +775,103 @@ struct ClusterSim {
             if (overlap <= 0.0) {
                 st[from_slot] = ST_IDLE;
             } else {
-                act_add(n_act, from_slot, ST_DRAIN, r, 0.0, wp::dadd(now, overlap), mseq_ctr);
+                act_add(n_act, from_slot, ST_DRAIN, r, 0.0, wp::dadd(now, overlap), jmig);
             }
-            refresh_gpu(fg);
-            if (tg != fg) refresh_gpu(tg);
+            refresh_gpu(g);
         }
-        if (overlap > 0.0) {
-            ++mseq_ctr;
+        if (overlap > 0.0) ++n_act;
+        tl_dirty = true;
+        wp::bsync();
+        const unsigned ca = k2w(W_(g));
+        const uint64_t costs = (uint64_t)cb | ((uint64_t)ca << 16) | ((uint64_t)cb << 32) | ((uint64_t)ca << 48);
+        emit(EV_MIGRATION_START, r, (unsigned)g, (unsigned)g, (unsigned)q, (unsigned)fs, (unsigned)ts, 0, costs);
+        ++n_mig;
+        emit_reconfig(g, q, ts, cr);
+        if (overlap <= 0.0) emit(EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
+    }
+
+    // apply_move of plan_inter: the source side on the source GPU's owner,
+    // the destination side on the lazy GPU's owner, from the exchanged
+    // record of the winning source (x).  The job's active entry moves with
+    // it: removed at the source (which, with overlap > 0, gets a draining
+    // entry instead) and re-added at the destination.
+    MSG_DI void apply_move_inter(const XRec& x, int tg, int ts) {
+        wp::bsync();
+        const int from_slot = x.slot;
+        const int fg = from_slot >> 3, fs = from_slot & 7;
+        const uint8_t jst = (uint8_t)(x.info & 0xFFu);
+        const int q = (int)((x.info >> 8) & 0xFFu);
+        const unsigned jmig = x.info >> 16;
+        const int32_t r = x.job;
+        const bool src = own(fg), dst_own = own(tg);
+        unsigned fcb = 0, fca = 0, tcb = 0, tca = 0;
+        if (src) {
+            fcb = k2w(W_(fg));
+            wp::bsync();
+            if (T == 0) {
+                act_remove(from_slot, n_act);
+                if (overlap <= 0.0) {
+                    st[from_slot] = ST_IDLE;
+                } else {
+                    st[from_slot] = ST_DRAIN;
+                    act_add(n_act - 1, from_slot, ST_DRAIN, r, 0.0, wp::dadd(now, overlap), jmig);
+                }
+                refresh_gpu(fg);
+            }
+            if (overlap <= 0.0) --n_act;
+            wp::bsync();
+            fca = k2w(W_(fg));
+        }
+        if (dst_own) {
+            tcb = k2w(W_(tg));
+            const CreateRes cr = create(tg, q, ts);
+            if (T == 0) {
+                const int dst = 8 * tg + ts;
+                st[dst] = jst;
+                mig[dst] = (uint16_t)(jmig + 1u);
+                act_add(n_act, dst, jst, r, x.rem, x.tkey, 0);
+                refresh_gpu(tg);
+            }
             ++n_act;
+            wp::bsync();
+            tca = k2w(W_(tg));
+            if (S == 1) {  // both sides are here: the event log carries all four costs
+                const uint64_t costs =
+                    (uint64_t)fcb | ((uint64_t)fca << 16) | ((uint64_t)tcb << 32) | ((uint64_t)tca << 48);
+                emit(EV_MIGRATION_START, r, (unsigned)fg, (unsigned)tg, (unsigned)q, (unsigned)fs, (unsigned)ts,
+                     EF_INTER, costs);
+            } else {
+                ++n_ev;  // counted; the sharded engine runs without the event log
+            }
+            ++n_mig;
+            emit_reconfig(tg, q, ts, cr);
+            if (overlap <= 0.0) emit(EV_MIGRATION_END, r, (unsigned)fg, 0, 0, 0, 0, 0, 0);
         }
         tl_dirty = true;
         wp::bsync();
-        const unsigned fca = k2w(gw[fg]), tca = k2w(gw[tg]);
-        const uint64_t costs = (uint64_t)fcb | ((uint64_t)fca << 16) | ((uint64_t)tcb << 32) | ((uint64_t)tca << 48);
-        emit(EV_MIGRATION_START, r, (unsigned)fg, (unsigned)tg, (unsigned)q, (unsigned)fs, (unsigned)ts,
-             inter ? EF_INTER : 0, costs);
-        ++n_mig;
-        emit_reconfig(tg, q, ts, cr);
-        if (overlap <= 0.0) emit(EV_MIGRATION_END, r, (unsigned)fg, 0, 0, 0, 0, 0, 0);
     }
 
-    MSG_DI void plan_intra(int g) {  // migration.cpp:71-123, on warp 0
+    MSG_DI void plan_intra(int g) {  // migration.cpp:71-123, on warp 0 of the owner
         for (;;) {
             wp::bsync();
-            const unsigned wd = gw[g];
+            const unsigned wd = W_(g);
             const unsigned bc = w_bc(wd), bm = w_bm(wd), km = w_km(wd);
             const unsigned cur = rank2(bc, bm);
             if (W == 0) {
-                const int own = (int)(L & 7u);
-                const int sl = 8 * g + own;
+                const int own_s = (int)(L & 7u);
+                const int sl = 8 * g + own_s;
                 const uint8_t s = st[sl];
                 unsigned kmin = NONE, cnt = 0;
                 if (s == ST_RUN || s == ST_WAIT) {
                     const int q = prof[sl];
                     const unsigned r = (unsigned)ajob[apos[sl]];
-                    const unsigned ofc = fpc(q, own), ofm = fpm(q, own);
+                    const unsigned ofc = fpc(q, own_s), ofm = fpm(q, own_s);
                     const unsigned n = count_of(q), stride = stride_of(q);
                     for (int h = 0; h < 2; ++h) {
                         const unsigned j = (L >> 3) + 4u * (unsigned)h;
                         if (j < n) {
                             const int t = (int)(j * stride);
-                            if (t != own && !(fpm(q, t) & km)) {
+                            if (t != own_s && !(fpm(q, t) & km)) {
                                 const unsigned rk = rank2((bc & ~ofc) | fpc(q, t), (bm & ~ofm) | fpm(q, t));
                                 const unsigned key = (rk << 27) | (r << 3) | (unsigned)t;
                                 kmin = key < kmin ? key : kmin;
@@ -661,26 +896,28 @@ struct ClusterSim {
             max_intra = max_intra > evals ? max_intra : evals;
             wp::bsync();
             if (best == NONE || (best >> 27) >= cur) break;
-            apply_move(8 * g + from, g, (int)(best & 7u), false);
+            apply_move_intra(8 * g + from, (int)(best & 7u));
         }
     }
 
-    MSG_DI void plan_inter(int g0) {  // migration.cpp:125-210
+    // migration.cpp:125-210.  w0 = the lazy GPU's word, replicated in every
+    // shard (exchanged by on_departure, then updated by every shard with the
+    // same destination choice).
+    MSG_DI void plan_inter(int g0, unsigned w0) {
         for (;;) {
             wp::bsync();
-            const unsigned w0 = gw[g0];
             const unsigned lazy_cs = (unsigned)wp::popc(w_bc(w0));
             const unsigned km0 = w_km(w0);
             const unsigned pl = tb->placeable[km0];
             unsigned bhi = NONE, blo = NONE, z0 = 0, z1 = 0, cnt = 0;
-            int bsl = -1;
+            int bi = -1;
             for (uint32_t i = T; i < n_act; i += NT) {
                 const uint8_t v = ast[i];
                 if (v != ST_RUN && v != ST_WAIT) continue;
                 const int slot = aslot[i];
                 const int g = slot >> 3, s = slot & 7;
                 if (g == g0) continue;
-                const unsigned wd = gw[g];
+                const unsigned wd = W_(g);
                 const unsigned src_cs = (unsigned)wp::popc(w_bc(wd));
                 if ((lazymask >> src_cs) & 1u) continue;  // source must be Busy
                 const int q = prof[slot];
@@ -693,19 +930,32 @@ struct ClusterSim {
                     if (hi < bhi || (hi == bhi && lo < blo)) {
                         bhi = hi;
                         blo = lo;
-                        bsl = slot;
+                        bi = (int)i;
                     }
                     ++cnt;
                 }
             }
-            block_lexmin(bhi, blo, z0, z1, bsl);
-            int evals = (int)block_sum(cnt);
-            if (bhi == NONE) {
+            block_lexmin(bhi, blo, z0, z1, bi);
+            XRec x = xnone();
+            x.c[0] = block_sum(cnt);
+            x.hi = bhi;
+            x.lo = blo;
+            x.tie = x.ms = 0;
+            if (bhi != NONE) {
+                const int slot = aslot[bi];
+                x.slot = slot;
+                x.job = ajob[bi];
+                x.info = (uint32_t)st[slot] | ((uint32_t)prof[slot] << 8) | ((uint32_t)mig[slot] << 16);
+                x.rem = arem[bi];
+                x.tkey = atkey[bi];
+            }
+            exchange(x);
+            int evals = (int)x.c[0];
+            if (x.hi == NONE) {
                 max_inter = max_inter > evals ? max_inter : evals;
                 break;
             }
-            const int from_slot = bsl;
-            const int q = prof[from_slot];
+            const int q = (int)((x.info >> 8) & 0xFFu);
             if (W == 0) {  // destination: minimum (cost, start) on g0, lane = start
                 const bool cand = L < 8 && ((startmask_of(q) >> L) & 1u) && !(fpm(q, (int)L) & km0);
                 const unsigned dk =
@@ -718,17 +968,27 @@ struct ClusterSim {
                 }
             }
             wp::bsync();
-            const unsigned dbest = sc->u[5];
+            const int ts = (int)(sc->u[5] & 7u);
             evals += (int)sc->u[6];
             max_inter = max_inter > evals ? max_inter : evals;
-            apply_move(from_slot, g0, (int)(dbest & 7u), true);
+            apply_move_inter(x, g0, ts);
+            // the lazy GPU's word after create_instance (destroyed instances were idle)
+            const unsigned m = fpm(q, ts);
+            w0 = (w0 | fpc(q, ts) | (m << 8) | (m << 16)) + ((x.info & 0xFFu) == ST_RUN ? (1u << 24) : 0u);
         }
     }
 
     MSG_DI void on_departure(int g) {  // migration.cpp:212-220
         wp::bsync();
-        if ((lazymask >> wp::popc(w_bc(gw[g]))) & 1u) plan_inter(g);
-        else plan_intra(g);
+        unsigned wd = own(g) ? W_(g) : 0u;
+        if (S > 1) {
+            XRec x = xnone();
+            x.w = wd;
+            exchange(x);
+            wd = x.w;
+        }
+        if ((lazymask >> wp::popc(w_bc(wd))) & 1u) plan_inter(g, wd);
+        else if (own(g)) plan_intra(g);
     }
 
     // ------------------------------------------------------------ handlers
@@ -746,35 +1006,36 @@ struct ClusterSim {
             else enq = true;
         }
         if (enq) {
-            emit(EV_ARRIVAL, r, 0, 0, (unsigned)p, 0, 0, 0, 0);
-            if (T == 0) queue[q_tail] = r;
+            if (sh == 0) emit(EV_ARRIVAL, r, 0, 0, (unsigned)p, 0, 0, 0, 0);
+            if (T == 0) queue[q_tail] = r;  // every shard keeps the same queue
             ++q_tail;
-            emit(EV_ENQUEUE, r, 0, 0, 0, 0, 0, 0, 0);
+            if (sh == 0) emit(EV_ENQUEUE, r, 0, 0, 0, 0, 0, 0, 0);
             ++n_enq;
         }
     }
 
-    MSG_DI void handle_departure(int ia, bool completion) {
-        wp::bsync();
-        const int slot = aslot[ia];
+    MSG_DI void handle_departure(int slot, int ia, bool completion) {
         const int g = slot >> 3;
-        const int32_t r = ajob[ia];
-        const int m = mig[slot];
-        wp::bsync();
-        if (T == 0) {
-            st[slot] = ST_IDLE;
-            act_remove(slot, n_act);
-            if (completion) {
-                jobs[r].done = now;
-                jobs[r].gpu = g;
-                jobs[r].mig = m;
+        if (own(g)) {
+            wp::bsync();
+            const int32_t r = ajob[ia];
+            const int m = mig[slot];
+            wp::bsync();
+            if (T == 0) {
+                st[slot] = ST_IDLE;
+                act_remove(slot, n_act);
+                if (completion) {
+                    jobs[r].done = now;
+                    jobs[r].gpu = g;
+                    jobs[r].mig = m;
+                }
+                refresh_gpu(g);
             }
-            refresh_gpu(g);
+            --n_act;
+            tl_dirty = true;
+            wp::bsync();
+            emit(completion ? EV_COMPLETION : EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
         }
-        --n_act;
-        tl_dirty = true;
-        wp::bsync();
-        emit(completion ? EV_COMPLETION : EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
         if (completion) sample();
         const int passes = (completion && (cflags & CF_MIG)) ? 2 : 1;
         for (int pass = 0; pass < passes; ++pass) {
@@ -783,10 +1044,10 @@ struct ClusterSim {
         }
     }
 
-    MSG_DI void handle_service_start(int ia) {
+    MSG_DI void handle_service_start(int slot, int ia) {
+        if (!own(slot >> 3)) return;
         wp::bsync();
         if (T == 0) {
-            const int slot = aslot[ia];
             st[slot] = ST_RUN;
             ast[ia] = ST_RUN;  // start_service: arem already holds service_s
             refresh_gpu(slot >> 3);
@@ -797,25 +1058,40 @@ struct ClusterSim {
 
     MSG_DI void run() {
         for (;;) {
-            int ia = -1;
-            const int kind = next_event(ia);
+            int slot = -1, ia = -1;
+            const int kind = next_event(slot, ia);
             if (kind < 0) break;
             ++n_handler;
             advance_all();
             if (kind == 3) handle_arrival();
-            else if (kind == 2) handle_service_start(ia);
-            else handle_departure(ia, kind == 0);
+            else if (kind == 2) handle_service_start(slot, ia);
+            else handle_departure(slot, ia, kind == 0);
             reschedule();
             sample();
         }
     }
 
-    MSG_DI void finish(DevSummary* out) {  // metrics (sim.cpp:414-502), warp 0
+    MSG_DI void finish(DevSummary* out) {  // metrics (sim.cpp:414-502), warp 0 of shard 0
         wp::bsync();
         DevSummary s;
         s.status = q_head < q_tail ? STATUS_JOBS_PENDING : STATUS_OK;
         s.reserved = 0;
         s.pending_rank = -1;
+        if (S > 1) {  // flush the last samples, sum the owner-counted totals; job rows become visible
+            wp::gfence();
+            XRec x = xnone();
+            x.c[0] = n_mig;
+            x.c[1] = n_reconf;
+            x.c[2] = n_ev;
+            x.mx = (unsigned)max_intra;
+            exchange(x);
+            n_mig = x.c[0];
+            n_reconf = x.c[1];
+            n_ev = x.c[2];
+            max_intra = (int)x.mx;
+            wp::cluster_sync();  // no shard leaves while another may still read its records
+            if (sh != 0) return;
+        }
         if (s.status != STATUS_OK) {
             unsigned mn = NONE;
             for (uint32_t i = q_head + T; i < q_tail; i += NT) {

@@ -17,6 +17,13 @@ enum : uint8_t {
     ST_DRAIN = 4   // draining source replica          (MigrationEnd timer)
 };
 
+// Block engine (cluster_core.cuh): the fragmentation timeline is the
+// reference's sequential double sum up to kExactTimelineGpus GPUs; a trace
+// is split over up to kMaxShards CTAs (one thread-block cluster) only above
+// that size and without the event log.
+constexpr int kExactTimelineGpus = 512;
+constexpr int kMaxShards = 16;
+
 // Feature / output flags.
 enum : uint32_t {
     CF_LB = 1u,      // FeatureFlags::load_balancing
@@ -131,7 +138,7 @@ struct SimArgs {
     // slot (8 * (cl_goff + g) + s), and the list of large traces
     const uint32_t* large_idx;
     uint32_t n_large;
-    uint32_t reserved;
+    uint32_t shards;   // CTAs (GPU-range shards) per large trace: one thread-block cluster
     // per slot (8 per GPU)
     uint8_t* c_st;
     uint8_t* c_prof;

@@ -54,22 +54,26 @@ static cudaError_t launch_sim_t(const SimArgs& a, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-// Block engine for clusters of more than 32 GPUs: one block per trace.
+// Block engine for clusters of more than 32 GPUs: one thread-block cluster
+// of a.shards CTAs per trace (a.shards = 1: one block), each CTA one shard
+// of the trace's GPUs (cluster_core.cuh).
 constexpr int kClusterThreads = 512;
 
 template <bool DETAIL>
 __global__ void __launch_bounds__(kClusterThreads, 1) cluster_kernel(SimArgs a) {
     __shared__ __align__(16) DevTables tb;
     __shared__ BlockScratch sc;
-    extern __shared__ __align__(16) unsigned char gpu_smem[];  // 9 B per GPU when G <= smem_gpus
+    extern __shared__ __align__(16) unsigned char gpu_smem[];  // 9 B per owned GPU when they fit
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tables);
         uint4* dst = reinterpret_cast<uint4*>(&tb);
         for (unsigned i = threadIdx.x; i < sizeof(DevTables) / 16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    const uint32_t t = a.large_idx[blockIdx.x];
-    const bool in_smem = (uint32_t)a.configs[a.traces[t].cfg].G <= a.smem_gpus;
+    const unsigned S = wp::cluster_size();
+    const uint32_t t = a.large_idx[blockIdx.x / S];
+    const uint32_t G = (uint32_t)a.configs[a.traces[t].cfg].G;
+    const bool in_smem = (G + S - 1) / S <= a.smem_gpus;
     simulate_large_trace<DETAIL>(a, &tb, &sc, in_smem ? gpu_smem : nullptr, t);
 }
 
@@ -86,22 +90,42 @@ static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         cudaFuncAttributes fa;
         if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, cluster_kernel<DETAIL>);
+        if (e == cudaSuccess && kMaxShards > 8)
+            e = cudaFuncSetAttribute(cluster_kernel<DETAIL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         static_smem = fa.sharedSizeBytes;
     }
+    const uint32_t S = a.shards < 1 ? 1u : a.shards;
+    if (S > (uint32_t)kMaxShards) return cudaErrorInvalidValue;
+    const uint32_t per = (a.max_gpus + S - 1) / S;  // GPUs per shard (largest trace)
     const size_t room = (size_t)optin > static_smem + 1024 ? (size_t)optin - static_smem - 1024 : 0;
     size_t dyn = 0;
     a.smem_gpus = 0;
-    if (gpu_smem_bytes(a.max_gpus) <= room) {
-        a.smem_gpus = a.max_gpus;
-        dyn = gpu_smem_bytes(a.max_gpus);
+    if (gpu_smem_bytes(per) <= room) {
+        a.smem_gpus = per;
+        dyn = gpu_smem_bytes(per);
     }
     if (dyn > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(cluster_kernel<DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         if (e != cudaSuccess) return e;
     }
-    cluster_kernel<DETAIL><<<a.n_large, kClusterThreads, dyn, stream>>>(a);
-    return cudaGetLastError();
+    if (S == 1) {
+        cluster_kernel<DETAIL><<<a.n_large, kClusterThreads, dyn, stream>>>(a);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.n_large * S);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, cluster_kernel<DETAIL>, a);
 }
 
 cudaError_t launch_cluster(const SimArgs& a, cudaStream_t stream) {

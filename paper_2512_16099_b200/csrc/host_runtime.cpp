@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -56,6 +57,7 @@ struct msg_staged {
     DevBuf d_large_idx, c_st, c_prof, c_mig, c_cseq, c_apos, c_aslot, c_ast, c_ajob, c_amseq, c_arem,
         c_atkey, c_gw, c_gx, c_gcid;
     uint32_t large_max_g = 0;
+    uint32_t large_min_g = 0;
     // pinned host mirrors (rank order)
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
@@ -147,6 +149,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     s->large_idx.clear();
     s->large_gpus = 0;
     s->large_max_g = 0;
+    s->large_min_g = 0;
     s->any_small = false;
     for (uint32_t t = 0; t < s->n_in; ++t) {
         const uint32_t ci = b->config_index ? b->config_index[t] : 0;
@@ -164,6 +167,8 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
             tr.cl_goff = s->large_gpus;
             s->large_gpus += (uint64_t)cfgs[ci].gpu_count;
             s->large_max_g = std::max(s->large_max_g, (uint32_t)cfgs[ci].gpu_count);
+            s->large_min_g = s->large_min_g ? std::min(s->large_min_g, (uint32_t)cfgs[ci].gpu_count)
+                                            : (uint32_t)cfgs[ci].gpu_count;
             s->large_idx.push_back((uint32_t)s->traces.size());
         } else {
             s->any_small = true;
@@ -264,6 +269,21 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     return MSG_OK;
 }
 
+// CTAs per large trace (cluster_core.cuh): >= 1024 GPUs per shard, up to
+// kMaxShards; 1 when any large trace is within the exact-timeline size or
+// the event log is requested.  MSG_SHARDS overrides the count (tuning).
+uint32_t choose_shards(uint32_t min_g, uint32_t out_flags) {
+    if (min_g <= (uint32_t)kExactTimelineGpus || (out_flags & OF_EVENTS)) return 1;
+    uint32_t S = 1;
+    if (const char* e = std::getenv("MSG_SHARDS")) {
+        const int v = std::atoi(e);
+        S = v < 1 ? 1u : std::min<uint32_t>((uint32_t)v, (uint32_t)kMaxShards);
+    } else {
+        while (S < (uint32_t)kMaxShards && min_g / (2 * S) >= 1024) S *= 2;
+    }
+    return std::min(S, min_g);
+}
+
 SimArgs make_args(msg_engine* eng, msg_staged* s) {
     SimArgs a{};
     a.traces = s->d_traces.as<DevTrace>();
@@ -296,6 +316,7 @@ SimArgs make_args(msg_engine* eng, msg_staged* s) {
         a.c_arem = s->c_arem.as<double>();
         a.c_atkey = s->c_atkey.as<double>();
         a.max_gpus = s->large_max_g;
+        a.shards = choose_shards(s->large_min_g, s->out_flags);
         a.c_gw = s->c_gw.as<uint32_t>();
         a.c_gx = s->c_gx.as<uint32_t>();
         a.c_gcid = s->c_gcid.as<uint8_t>();

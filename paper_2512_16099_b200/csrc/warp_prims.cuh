@@ -28,6 +28,7 @@ MSG_DI unsigned ballot(bool p) { return __ballot_sync(0xffffffffu, p); }
 MSG_DI unsigned rmin(unsigned x) { return __reduce_min_sync(0xffffffffu, x); }
 MSG_DI unsigned radd(unsigned x) { return __reduce_add_sync(0xffffffffu, x); }
 MSG_DI unsigned ror(unsigned x) { return __reduce_or_sync(0xffffffffu, x); }
+MSG_DI unsigned rmax(unsigned x) { return __reduce_max_sync(0xffffffffu, x); }
 MSG_DI unsigned shfl(unsigned x, int src) { return __shfl_sync(0xffffffffu, x, src); }
 MSG_DI int shfl(int x, int src) { return __shfl_sync(0xffffffffu, x, src); }
 MSG_DI double shfl(double x, int src) { return __shfl_sync(0xffffffffu, x, src); }
@@ -43,6 +44,29 @@ MSG_DI uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
 MSG_DI void bsync() { __syncthreads(); }
 MSG_DI unsigned tid() { return threadIdx.x; }
 MSG_DI unsigned nthreads() { return blockDim.x; }
+// thread-block cluster (the sharded block engine, cluster_core.cuh): rank
+// and size, a full cluster barrier with release/acquire semantics, and the
+// distributed-shared-memory view of a shared variable in another CTA.
+MSG_DI unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+MSG_DI unsigned cluster_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+MSG_DI void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class T>
+MSG_DI const T* cluster_map(const T* p, unsigned rank) {
+    uint64_t r;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+    return reinterpret_cast<const T*>(r);
+}
+MSG_DI void gfence() { __threadfence(); }
 }  // namespace wp
 
 #else  // host emulation (tests/emu)

@@ -2,6 +2,7 @@
 // (paper_2512_16099_b200/csrc/engine_core.cuh) on 32 host threads per trace,
 // with the product's own staging/decoding (staging.h), and returns results
 // in the ABI record formats so tests can diff them against the reference.
+#include <cstdio>
 #include <cstdlib>
 #include <memory>
 #include <string>
@@ -42,24 +43,38 @@ void run_warp(const SimArgs& a, const DevTables* tb) {
     for (auto& t : lanes) t.join();
 }
 
-// Block engine (G > 32) on `nt` emulated threads (nt/32 warps + a block barrier).
-void run_block(const SimArgs& a, const DevTables* tb, unsigned nt, unsigned char* gpu_smem) {
-    auto sc = std::make_unique<BlockScratch>();
-    std::memset(sc.get(), 0xA5, sizeof(BlockScratch));
-    wp::EmuBlock block;
-    block.n = nt;
+// Block engine (G > 32) on S emulated blocks (one cluster) of `nt` threads
+// each (nt/32 warps + a block barrier; a cluster barrier across blocks).
+void run_block(const SimArgs& a, const DevTables* tb, unsigned nt, unsigned S, bool gpu_smem, int G) {
+    std::vector<std::unique_ptr<BlockScratch>> sc;
+    std::vector<std::unique_ptr<wp::EmuBlock>> blocks;
+    std::vector<std::vector<unsigned char>> smem;
+    wp::EmuCluster cluster;
+    cluster.S = S;
+    cluster.n = S * nt;
     std::vector<std::unique_ptr<wp::EmuWarp>> warps;
-    for (unsigned i = 0; i < nt / 32; ++i) warps.emplace_back(new wp::EmuWarp());
+    for (unsigned b = 0; b < S; ++b) {
+        sc.emplace_back(new BlockScratch());
+        std::memset(sc.back().get(), 0xA5, sizeof(BlockScratch));
+        cluster.base[b] = reinterpret_cast<char*>(sc.back().get());
+        blocks.emplace_back(new wp::EmuBlock());
+        blocks.back()->n = nt;
+        smem.emplace_back(9 * (size_t)((G + S - 1) / S) + 16, 0xA5);  // stands in for dynamic smem
+        for (unsigned i = 0; i < nt / 32; ++i) warps.emplace_back(new wp::EmuWarp());
+    }
     std::vector<std::thread> th;
-    for (unsigned t = 0; t < nt; ++t)
-        th.emplace_back([&, t]() {
-            wp::g_block = &block;
-            wp::g_warp = warps[t / 32].get();
-            wp::g_lane = t % 32;
-            wp::g_tid = t;
-            wp::g_phase = 0;
-            simulate_large_trace<true>(a, tb, sc.get(), gpu_smem, 0);
-        });
+    for (unsigned b = 0; b < S; ++b)
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([&, b, t]() {
+                wp::g_block = blocks[b].get();
+                wp::g_warp = warps[b * (nt / 32) + t / 32].get();
+                wp::g_lane = t % 32;
+                wp::g_tid = t;
+                wp::g_phase = 0;
+                wp::g_cluster = S > 1 ? &cluster : nullptr;
+                wp::g_crank = b;
+                simulate_large_trace<true>(a, tb, sc[b].get(), gpu_smem ? smem[b].data() : nullptr, 0);
+            });
     for (auto& x : th) x.join();
 }
 
@@ -126,7 +141,6 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
     std::vector<int32_t> c_aslot(ns), c_apos(ns), c_ajob(ns);
     std::vector<uint8_t> c_ast(ns);
     std::vector<double> c_arem(ns), c_atkey(ns);
-    std::vector<unsigned char> gpu_smem(9 * (size_t)G + 16, 0xA5);  // stands in for dynamic smem
     uint32_t large_idx = 0;
     const bool block = G > 32 || std::getenv("MSG_EMU_FORCE_BLOCK") != nullptr;
     if (block) {
@@ -150,10 +164,14 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
         a.c_gcid = c_gcid.data();
         const char* nt = std::getenv("MSG_EMU_BLOCK_THREADS");
         const char* gs = std::getenv("MSG_EMU_GPU_SMEM");  // "0": per-GPU words in global memory
+        const char* sh = std::getenv("MSG_EMU_SHARDS");    // thread-block cluster size (shards)
         const bool smem = !(gs && gs[0] == '0');
+        const unsigned S = sh ? (unsigned)std::atoi(sh) : 1u;
+        if (S > 1) a.out_flags &= ~OF_EVENTS;  // the sharded engine runs without the event log
         a.max_gpus = (uint32_t)G;
         a.smem_gpus = smem ? (uint32_t)G : 0u;
-        run_block(a, &tables, nt ? (unsigned)std::atoi(nt) : 64u, smem ? gpu_smem.data() : nullptr);
+        if (std::getenv("MSG_EMU_DEBUG")) std::fprintf(stderr, "emu block engine: S=%u G=%d\n", S, G);
+        run_block(a, &tables, nt ? (unsigned)std::atoi(nt) : 64u, S < 1 ? 1u : S, smem, G);
     } else if (G <= 4) run_warp<1>(a, &tables);
     else if (G <= 8) run_warp<2>(a, &tables);
     else if (G <= 16) run_warp<4>(a, &tables);

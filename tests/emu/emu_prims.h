@@ -36,6 +36,19 @@ struct EmuBlock {
 inline thread_local EmuBlock* g_block = nullptr;
 inline thread_local unsigned g_tid = 0;
 
+// Cluster emulation (sharded block engine): S emulated blocks, a barrier
+// over all their threads, and the base address of each block's scratch so
+// cluster_map can translate a shared-memory pointer to another block's copy.
+struct EmuCluster {
+    std::atomic<unsigned> arrived{0};
+    std::atomic<unsigned> gen{0};
+    unsigned S = 1;
+    unsigned n = 0;  // threads over all blocks
+    char* base[64] = {};
+};
+inline thread_local EmuCluster* g_cluster = nullptr;
+inline thread_local unsigned g_crank = 0;
+
 inline void barrier() {
     EmuWarp* w = g_warp;
     const unsigned g = w->gen.load(std::memory_order_acquire);
@@ -75,6 +88,32 @@ inline void bsync() {
     }
 }
 inline void sync() { barrier(); }
+inline unsigned cluster_rank() { return g_cluster ? g_crank : 0u; }
+inline unsigned cluster_size() { return g_cluster ? g_cluster->S : 1u; }
+inline void cluster_sync() {
+    EmuCluster* c = g_cluster;
+    if (!c) {
+        bsync();
+        return;
+    }
+    const unsigned g = c->gen.load(std::memory_order_acquire);
+    if (c->arrived.fetch_add(1, std::memory_order_acq_rel) == c->n - 1) {
+        c->arrived.store(0, std::memory_order_relaxed);
+        c->gen.fetch_add(1, std::memory_order_release);
+    } else {
+        unsigned spins = 0;
+        while (c->gen.load(std::memory_order_acquire) == g) {
+            if (++spins > 32) std::this_thread::yield();
+        }
+    }
+}
+template <class T>
+inline const T* cluster_map(const T* p, unsigned rank) {
+    if (!g_cluster) return p;
+    const char* me = g_cluster->base[g_crank];
+    return reinterpret_cast<const T*>(g_cluster->base[rank] + (reinterpret_cast<const char*>(p) - me));
+}
+inline void gfence() { std::atomic_thread_fence(std::memory_order_seq_cst); }
 inline unsigned ballot(bool p) {
     const uint64_t* b = exchange(p ? 1u : 0u);
     unsigned m = 0;
@@ -92,6 +131,12 @@ inline unsigned radd(unsigned x) {
     const uint64_t* b = exchange(x);
     unsigned m = 0;
     for (int i = 0; i < 32; ++i) m += (unsigned)b[i];
+    return m;
+}
+inline unsigned rmax(unsigned x) {
+    const uint64_t* b = exchange(x);
+    unsigned m = 0;
+    for (int i = 0; i < 32; ++i) m = (unsigned)b[i] > m ? (unsigned)b[i] : m;
     return m;
 }
 inline unsigned ror(unsigned x) {

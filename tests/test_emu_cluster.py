@@ -25,10 +25,13 @@ def block_env(monkeypatch):
     return set_
 
 
-def _check(spec, cfg, seeds, relaxed=False):
+def _check(spec, cfg, seeds, relaxed=False, no_events=False):
     b = rb.ref_generate_batch(spec, seeds)
     ref = rb.ref_run_batch_results(b, [cfg])
     got = emu_run_batch_results(b, [cfg])
+    if no_events:  # the sharded engine writes no event log
+        for r in got:
+            r.events = None
     diff = diff_results_relaxed_timeline if relaxed else diff_results
     bad = [(s, d) for s, r, g in zip(seeds, ref, got) if (d := diff(r, g))]
     assert not bad, bad[:2]
@@ -66,3 +69,24 @@ def test_block_engine_relaxed_timeline_above_512_gpus(block_env):
     sp.mean_interarrival_s = 25.0 / 80
     sp.job_count = 600
     _check(sp, SimConfig(gpu_count=640), [4], relaxed=True)
+
+
+@pytest.mark.parametrize("shards", [2, 3, 5])
+def test_sharded_block_engine(block_env, monkeypatch, shards):
+    """S CTAs of one thread-block cluster, each owning a GPU range and its
+    active list, exchanging packed keys per decision: identical results to
+    the reference (timeline to 1e-9 above 512 GPUs)."""
+    block_env(force=False, threads=32, gpu_smem=shards != 3)
+    monkeypatch.setenv("MSG_EMU_SHARDS", str(shards))
+    sp = preset("normal25")
+    sp.mean_interarrival_s = 25.0 / 80
+    sp.job_count = 500
+    _check(sp, SimConfig(gpu_count=640), [4], relaxed=True, no_events=True)
+    churn = WorkloadSpec(mean_interarrival_s=0.005, median_s=4.0, sigma=1.2, job_count=500)
+    _check(churn, SimConfig(gpu_count=520, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                            reconfig_latency_s=0.1), [1], relaxed=True, no_events=True)
+    sp2 = preset("long25")
+    sp2.mean_interarrival_s = 25.0 / 100
+    sp2.job_count = 400
+    _check(sp2, SimConfig(gpu_count=700, sched=SchedulerConfig(features=FeatureFlags(True, True, False))), [7],
+           relaxed=True, no_events=True)

@@ -206,10 +206,12 @@ def test_schedule_exhaustive_two_gpus_depth2(d):
     assert got.tobytes() == want.tobytes()
 
 
-@pytest.mark.parametrize("G", [1, 3, 8, 32, 33, 200])
+@pytest.mark.parametrize("G", [1, 3, 8, 32, 33, 200, 1024, 2048, 4099])
 def test_schedule_random_clusters(d, G):
+    """G > 32 goes through the HBM scorer (score.cu): 1024/2048 are whole
+    chunks, 4099 adds a ragged, odd-length tail (scalar loads)."""
     rng = np.random.default_rng(G)
-    n = 150
+    n = 150 if G <= 200 else 24
     snaps = np.stack([random_cluster(rng, G) for _ in range(n)])
     profs = rng.integers(0, 6, n)
     for op in (abi.OP_SCHEDULE, abi.OP_FIRST_FIT, abi.OP_DISPATCH):
