@@ -9,8 +9,9 @@
 //     running count), idle-exact placement bits, 4-mask cost id — in SHARED
 //     memory (9 B/GPU), else global;
 //   * per (GPU, start) slot: instance state, profile, creation sequence,
-//     migrations of the bound job, position in the active list — global
-//     (L2-resident);
+//     migrations of the bound job, position in the active list — in SHARED
+//     memory too when the shard's 105 B/GPU fit (C4 at 16 shards: 105 KiB),
+//     else global (L2-resident);
 //   * the shard's ACTIVE list: every slot of its GPUs that carries a timer
 //     (running, waiting for service start, draining) with the timer data
 //     stored densely by list index (time, state, job, remaining work,
@@ -23,14 +24,16 @@
 //
 // Exchange.  Every decision that spans shards is one EXCHANGE: each shard
 // reduces its own candidates block-wide (per-warp REDUX chain, one
-// __syncthreads, the same chain over the warp winners) into one
-// record (88 B), writes it to its shared memory, and after one cluster barrier
-// warp 0 of every shard reads all S records through distributed shared
-// memory (mapa) and reduces them identically: lexicographic minimum key
+// __syncthreads, the same chain over the warp winners) into one 96-byte
+// record; lane k of warp 0 pushes it into CTA k's shared-memory inbox with
+// st.async (distributed shared memory, completing on CTA k's mbarrier), and
+// once its own barrier has counted all S records, warp 0 of every shard
+// reduces them identically from local shared memory: lexicographic minimum key
 // (with the winner's payload: the migrating job's slot, state, remaining
 // work and timer), sums (candidate counts, cost-total parts) and ORs (the
-// GPU word its owner broadcasts).  Records are double-buffered by round
-// parity, so one barrier per exchange suffices.  Exchanges per handler:
+// GPU word its owner broadcasts).  Inboxes and barriers are
+// double-buffered by round parity; there is no cluster-wide barrier and no
+// global-memory fence on this path.  Exchanges per handler:
 //   next event (always) · one per placement attempt (arrival, dequeue pass)
 //   · on a completion with migration: one broadcasting the departed GPU's
 //   word (Lazy/Busy) and, if Lazy, one per plan_inter iteration.
@@ -48,26 +51,23 @@
 // RN(RN(sum_g k_g / 25200) / G) from the exact integer sum of the per-GPU
 // cost numerators instead of the reference's sequential double sum (relative
 // difference <= G * 2^-53, i.e. < 2e-12 at 16384 GPUs; SURVEY §7 hard part
-// 6).  S > 1 is used only above that size and without the event log.
+// 6).  Sharding (S > 1 or D > 1) is used only above that size and without
+// the event log.
+//
+// Device groups.  The same trace can be split further over D device groups
+// (one cluster each; B200s of one NVLink/NVSwitch domain, or clusters of one
+// GPU): shard gs = dv * S + sh of D * S.  An exchange then has two levels —
+// the cluster level above, giving every CTA of a group the group's record,
+// and one cross-group step in which CTA sh of each group stores that record
+// into the inbox of every group (peer memory over NVLink, 96 B + a stamp
+// written with st.release.sys) and waits on its own inbox stamps
+// (ld.acquire.sys): a device-initiated all-reduce of packed keys per
+// decision, no host round trip and no NCCL call on the path.  Job rows go
+// to group 0's memory; the summary and timeline are written by group 0.
 #pragma once
 #include "engine_core.cuh"
 
 namespace msgk {
-
-// One shard's contribution to an exchange (and, after it, the reduction).
-struct XRec {
-    unsigned hi, lo, tie, ms;  // key, lexicographic minimum wins
-    int32_t slot;              // winner payload: global slot
-    int32_t job;               //   job rank
-    uint32_t info;             //   slot state | profile << 8 | job migrations << 16
-    uint32_t w;                // OR: word broadcast by a GPU's owner
-    double rem, tkey;          //   remaining work, timer time
-    uint32_t c[4];             // sums
-    uint32_t mx;               // max
-    uint32_t pad;
-    uint64_t ks[2];            // sums: deferred timeline samples (cost-total parts)
-};
-static_assert(sizeof(XRec) == 88, "exchange record layout");
 
 struct BlockScratch {
     unsigned hi[2][32], lo[2][32], tie[2][32], ms[2][32];
@@ -80,8 +80,10 @@ struct BlockScratch {
     int dl_prof[8];
     unsigned long long ksum;  // this shard's sum of per-GPU 4-mask cost numerators
     double tl;
-    XRec xb[2];        // this shard's exchange records (read by the cluster)
-    XRec xr;           // reduced record
+    XRec xin[2][kMaxShards];  // records pushed by every shard, by round parity
+    XRec xr;                  // reduced record (within the cluster)
+    XRec xr2;                 // reduced record (across device groups)
+    uint64_t xbar[2];         // mbarriers counting the pushed bytes, by round parity
 };
 
 template <bool DETAIL>
@@ -117,9 +119,11 @@ struct ClusterSim {
     int G;
     uint32_t cflags, lazymask;
     double alpha, overlap, latency, inv_g;
-    // shard geometry
-    unsigned S, sh;
+    // shard geometry: S CTAs per cluster (rank sh), D device groups (this
+    // one dv); global shard gs = dv * S + sh of NS = D * S
+    unsigned S, sh, D, dv, gs, NS, epoch;
     int g_lo, g_hi;
+    XInbox* ib[kMaxDev];
     // block-uniform state (every thread holds the same values)
     unsigned T, W, L, w, NT;  // thread, warp, lane, warps, threads
     int bph;                  // scratch double-buffer parity
@@ -134,7 +138,7 @@ struct ClusterSim {
     int max_arr, max_intra, max_inter;
     double tl_sum, tl_mean;
     bool tl_dirty;
-    // deferred timeline samples (S > 1)
+    // deferred timeline samples (sharded)
     uint32_t npend;
     double pend_t[2];
     unsigned long long pend_k[2];
@@ -206,46 +210,88 @@ struct ClusterSim {
         r.mx = 0;
         r.pad = 0;
         r.ks[0] = r.ks[1] = 0;
+        r.pad2 = 0;
         return r;
     }
+    // Identical reduction of one record per lane (lanes beyond the senders
+    // hold xnone()) in every CTA: lexicographic minimum with the winner's
+    // payload, sums, OR, max.
+    MSG_DI XRec warp_reduce(const XRec& x) {
+        int pay = (int)L;
+        unsigned hi = x.hi, lo = x.lo, tie = x.tie, ms = x.ms;
+        warp_lexmin(hi, lo, tie, ms, pay);
+        XRec o;
+        o.hi = hi;
+        o.lo = lo;
+        o.tie = tie;
+        o.ms = ms;
+        o.slot = wp::shfl(x.slot, pay);
+        o.job = wp::shfl(x.job, pay);
+        o.info = wp::shfl(x.info, pay);
+        o.rem = wp::shfl(x.rem, pay);
+        o.tkey = wp::shfl(x.tkey, pay);
+        o.w = wp::ror(x.w);
+        for (int k = 0; k < 4; ++k) o.c[k] = wp::radd(x.c[k]);
+        o.mx = wp::rmax(x.mx);
+        o.pad = 0;
+        o.pad2 = 0;
+        for (int k = 0; k < 2; ++k) {  // parts < 2^35: 20-bit split keeps the lane sums in 32 bits
+            const unsigned lo20 = wp::radd((unsigned)(x.ks[k] & 0xFFFFFu));
+            const unsigned hi20 = wp::radd((unsigned)(x.ks[k] >> 20));
+            o.ks[k] = ((unsigned long long)hi20 << 20) + lo20;
+        }
+        return o;
+    }
+
     // Cluster-wide reduction of one record per shard (see the header).  The
     // caller passes a block-uniform record; every thread of every shard
     // returns the same reduced record.  Deferred timeline samples ride along.
     MSG_DI void exchange(XRec& r) {
-        if (S == 1) return;
+        if (NS == 1) return;
         r.ks[0] = npend > 0 ? pend_k[0] : 0ull;
         r.ks[1] = npend > 1 ? pend_k[1] : 0ull;
-        XRec* mine = &sc->xb[xround & 1u];
-        if (T == 0) *mine = r;
-        wp::cluster_sync();
-        if (W == 0) {
-            XRec x = L < S ? *wp::cluster_map(mine, L) : xnone();
-            int pay = (int)L;
-            unsigned hi = x.hi, lo = x.lo, tie = x.tie, ms = x.ms;
-            warp_lexmin(hi, lo, tie, ms, pay);
-            XRec o;
-            o.hi = hi;
-            o.lo = lo;
-            o.tie = tie;
-            o.ms = ms;
-            o.slot = wp::shfl(x.slot, pay);
-            o.job = wp::shfl(x.job, pay);
-            o.info = wp::shfl(x.info, pay);
-            o.rem = wp::shfl(x.rem, pay);
-            o.tkey = wp::shfl(x.tkey, pay);
-            o.w = wp::ror(x.w);
-            for (int k = 0; k < 4; ++k) o.c[k] = wp::radd(x.c[k]);
-            o.mx = wp::rmax(x.mx);
-            o.pad = 0;
-            for (int k = 0; k < 2; ++k) {  // parts < 2^35: 20-bit split keeps the lane sums in 32 bits
-                const unsigned lo20 = wp::radd((unsigned)(x.ks[k] & 0xFFFFFu));
-                const unsigned hi20 = wp::radd((unsigned)(x.ks[k] >> 20));
-                o.ks[k] = ((unsigned long long)hi20 << 20) + lo20;
+        const unsigned par = xround & 1u, use = xround >> 1;
+        if (S > 1) {  // level 1: the CTAs of this cluster, over distributed shared memory
+            if (W == 0) {
+                // lane k pushes this shard's record into CTA k's inbox slot [par][sh]
+                if (L == 0) wp::xbar_arm(&sc->xbar[par], S * (unsigned)sizeof(XRec));
+                if (L < S)
+                    wp::xpush(&sc->xin[par][sh], reinterpret_cast<const uint4*>(&r), (int)(sizeof(XRec) / 16), L,
+                              &sc->xbar[par]);
+                wp::xwait(&sc->xbar[par], use, S);
+                const XRec o = warp_reduce(L < S ? sc->xin[par][L] : xnone());
+                if (L == 0) sc->xr = o;
             }
-            if (L == 0) sc->xr = o;
+            wp::bsync();
+            r = sc->xr;
         }
-        wp::bsync();
-        r = sc->xr;
+        if (D > 1) {  // level 2: CTA sh of every device group, over (peer) global memory
+            if (W == 0) {
+                const uint64_t stamp = ((uint64_t)epoch << 32) | (xround + 1u);
+                if (L < D) {  // push the group's record to group L, then its stamp (release)
+                    XInbox* dst = ib[L];
+                    uint4* q = reinterpret_cast<uint4*>(&dst->rec[par][sh][dv]);
+                    const uint4* src = reinterpret_cast<const uint4*>(&r);
+                    for (int i = 0; i < (int)(sizeof(XRec) / 16); ++i) q[i] = src[i];
+                    wp::st_release_sys(&dst->stamp[par][sh][dv], stamp);
+                }
+                XRec x = xnone();
+                if (L < D) {
+                    XInbox* me = ib[dv];
+                    const uint64_t t0 = wp::gtime_ns();
+                    unsigned spins = 0;
+                    while (wp::ld_acquire_sys(&me->stamp[par][sh][L]) != stamp) {
+                        wp::spin_pause();
+                        if ((++spins & 1023u) == 0 && wp::gtime_ns() - t0 > 30000000000ull) wp::fail_stop();
+                    }
+                    x = me->rec[par][sh][L];
+                }
+                const XRec o = warp_reduce(x);
+                if (L == 0) sc->xr2 = o;
+            }
+            wp::bsync();
+            r = sc->xr2;
+        }
         ++xround;
         // deferred timeline samples, in order
         for (uint32_t i = 0; i < npend; ++i) record_sample(pend_t[i], r.ks[i]);
@@ -276,9 +322,11 @@ struct ClusterSim {
     }
 
     // ---------------------------------------------------------------- setup
-    // gpu_smem: 9 B per owned GPU of dynamic shared memory, or nullptr (global).
+    // gpu_smem: dynamic shared memory for the owned GPUs — 9 B per GPU (mask
+    // words, cost ids), plus 96 B per GPU for its 8 slots when slots_smem —
+    // or nullptr (everything global).
     MSG_DI void setup(const SimArgs& a, const DevTables* tables, BlockScratch* scratch, unsigned char* gpu_smem,
-                      uint32_t t) {
+                      bool slots_smem, uint32_t t) {
         T = wp::tid();
         L = wp::lane();
         W = T >> 5;
@@ -289,13 +337,21 @@ struct ClusterSim {
         tb = tables;
         S = wp::cluster_size();
         sh = wp::cluster_rank();
+        D = a.n_dev < 1 ? 1u : a.n_dev;
+        const unsigned vd = a.vdev < 1 ? 1u : a.vdev;
+        dv = a.dev0 + (wp::cluster_id() % vd);
+        gs = dv * S + sh;
+        NS = D * S;
+        epoch = a.epoch;
+        // inbox of group k for this trace: a.inbox[k] holds one XInbox per large trace
+        for (unsigned k = 0; k < D; ++k) ib[k] = reinterpret_cast<XInbox*>(a.inbox[k]) + wp::cluster_id() / vd;
         xround = 0;
         npend = 0;
         const DevTrace tr = a.traces[t];
         const DevConfig c = a.configs[tr.cfg];
         G = c.G;
-        g_lo = (int)((uint64_t)G * sh / S);
-        g_hi = (int)((uint64_t)G * (sh + 1) / S);
+        g_lo = (int)((uint64_t)G * gs / NS);
+        g_hi = (int)((uint64_t)G * (gs + 1) / NS);
         const uint64_t go = tr.cl_goff, so = 8 * go;
         st = a.c_st + so;
         prof = a.c_prof + so;
@@ -311,9 +367,25 @@ struct ClusterSim {
         atkey = a.c_atkey + ao;
         const int ng = g_hi - g_lo;
         if (gpu_smem) {
-            gw = reinterpret_cast<uint32_t*>(gpu_smem);
-            gx = gw + ng;
-            gcid = reinterpret_cast<uint8_t*>(gx + ng);
+            unsigned char* p = gpu_smem;
+            gw = reinterpret_cast<uint32_t*>(p);
+            p += 4 * ng;
+            gx = reinterpret_cast<uint32_t*>(p);
+            p += 4 * ng;
+            if (slots_smem) {  // indexed by global slot: bases offset by the shard's first slot
+                const int s0 = 8 * g_lo;
+                apos = reinterpret_cast<int32_t*>(p) - s0;
+                p += 32 * ng;
+                cseq = reinterpret_cast<uint32_t*>(p) - s0;
+                p += 32 * ng;
+                mig = reinterpret_cast<uint16_t*>(p) - s0;
+                p += 16 * ng;
+                st = p - s0;
+                p += 8 * ng;
+                prof = p - s0;
+                p += 8 * ng;
+            }
+            gcid = p;
         } else {
             gw = a.c_gw + go + g_lo;
             gx = a.c_gx + go + g_lo;
@@ -361,6 +433,13 @@ struct ClusterSim {
         }
         if (T < 7) sc->f[T] = wp::dadd(1.0, wp::dmul(alpha, (double)(int)T));  // slowdown(T+1)
         if (T == 0) sc->ksum = (unsigned long long)tb->cost4k[empty_id] * (unsigned long long)ng;
+        if (S > 1) {  // exchange barriers live before any shard pushes
+            if (T == 0) {
+                wp::xbar_init(&sc->xbar[0]);
+                wp::xbar_init(&sc->xbar[1]);
+            }
+            wp::cluster_sync();
+        }
         wp::bsync();
         // static layout (sim.cpp:86-95), owned instances
         if (T == 0) {
@@ -477,7 +556,7 @@ struct ClusterSim {
     MSG_DI void record_sample(double t, unsigned long long ktot) {
         const double tot = wp::ddiv((double)ktot, 25200.0);
         tl_mean = inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
-        if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && T == 0 && sh == 0) {
+        if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && T == 0 && gs == 0) {
             tl[2 * n_tl] = t;
             tl[2 * n_tl + 1] = tl_mean;
         }
@@ -486,7 +565,7 @@ struct ClusterSim {
     }
 
     MSG_DI void sample() {  // sim.cpp:177-181
-        if (S > 1) {  // deferred: the next exchange sums the shards' parts
+        if (NS > 1) {  // deferred: the next exchange sums the shards' parts
             wp::bsync();
             pend_t[npend] = now;
             pend_k[npend] = sc->ksum;
@@ -551,7 +630,7 @@ struct ClusterSim {
             tmin = atkey[bi];
             slot = aslot[bi];
         }
-        if (S > 1) {
+        if (NS > 1) {
             XRec r = xnone();
             r.hi = bhi;
             r.lo = blo;
@@ -622,7 +701,7 @@ struct ClusterSim {
             NL = block_sum(nl);
             NB = block_sum(nb);
         }
-        if (S > 1) {
+        if (NS > 1) {
             XRec r = xnone();
             r.hi = hi;
             r.lo = lo;
@@ -835,7 +914,7 @@ struct ClusterSim {
             ++n_act;
             wp::bsync();
             tca = k2w(W_(tg));
-            if (S == 1) {  // both sides are here: the event log carries all four costs
+            if (NS == 1) {  // both sides are here: the event log carries all four costs
                 const uint64_t costs =
                     (uint64_t)fcb | ((uint64_t)fca << 16) | ((uint64_t)tcb << 32) | ((uint64_t)tca << 48);
                 emit(EV_MIGRATION_START, r, (unsigned)fg, (unsigned)tg, (unsigned)q, (unsigned)fs, (unsigned)ts,
@@ -981,7 +1060,7 @@ struct ClusterSim {
     MSG_DI void on_departure(int g) {  // migration.cpp:212-220
         wp::bsync();
         unsigned wd = own(g) ? W_(g) : 0u;
-        if (S > 1) {
+        if (NS > 1) {
             XRec x = xnone();
             x.w = wd;
             exchange(x);
@@ -1006,10 +1085,10 @@ struct ClusterSim {
             else enq = true;
         }
         if (enq) {
-            if (sh == 0) emit(EV_ARRIVAL, r, 0, 0, (unsigned)p, 0, 0, 0, 0);
+            if (gs == 0) emit(EV_ARRIVAL, r, 0, 0, (unsigned)p, 0, 0, 0, 0);
             if (T == 0) queue[q_tail] = r;  // every shard keeps the same queue
             ++q_tail;
-            if (sh == 0) emit(EV_ENQUEUE, r, 0, 0, 0, 0, 0, 0, 0);
+            if (gs == 0) emit(EV_ENQUEUE, r, 0, 0, 0, 0, 0, 0, 0);
             ++n_enq;
         }
     }
@@ -1077,8 +1156,9 @@ struct ClusterSim {
         s.status = q_head < q_tail ? STATUS_JOBS_PENDING : STATUS_OK;
         s.reserved = 0;
         s.pending_rank = -1;
-        if (S > 1) {  // flush the last samples, sum the owner-counted totals; job rows become visible
-            wp::gfence();
+        if (NS > 1) {  // flush the last samples, sum the owner-counted totals; job rows become visible
+            if (D > 1) wp::gfence_sys();
+            else wp::gfence();
             XRec x = xnone();
             x.c[0] = n_mig;
             x.c[1] = n_reconf;
@@ -1089,8 +1169,8 @@ struct ClusterSim {
             n_reconf = x.c[1];
             n_ev = x.c[2];
             max_intra = (int)x.mx;
-            wp::cluster_sync();  // no shard leaves while another may still read its records
-            if (sh != 0) return;
+            if (S > 1) wp::cluster_sync();  // no CTA leaves while a push to it may be in flight
+            if (gs != 0) return;
         }
         if (s.status != STATUS_OK) {
             unsigned mn = NONE;
@@ -1160,9 +1240,9 @@ struct ClusterSim {
 
 template <bool DETAIL>
 MSG_DI void simulate_large_trace(const SimArgs& a, const DevTables* tables, BlockScratch* sc,
-                                 unsigned char* gpu_smem, uint32_t t) {
+                                 unsigned char* gpu_smem, bool slots_smem, uint32_t t) {
     ClusterSim<DETAIL> sim;
-    sim.setup(a, tables, sc, gpu_smem, t);
+    sim.setup(a, tables, sc, gpu_smem, slots_smem, t);
     sim.run();
     sim.finish(a.summary + t);
 }

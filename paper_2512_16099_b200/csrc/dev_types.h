@@ -23,6 +23,33 @@ enum : uint8_t {
 // that size and without the event log.
 constexpr int kExactTimelineGpus = 512;
 constexpr int kMaxShards = 16;
+// A trace can also be split over up to kMaxDev device GROUPS (one cluster
+// each): B200s of one box exchanging over NVLink, or clusters of one GPU.
+constexpr int kMaxDev = 8;
+
+// One shard's contribution to an exchange (and, after it, the reduction).
+struct alignas(16) XRec {
+    unsigned hi, lo, tie, ms;  // key, lexicographic minimum wins
+    int32_t slot;              // winner payload: global slot
+    int32_t job;               //   job rank
+    uint32_t info;             //   slot state | profile << 8 | job migrations << 16
+    uint32_t w;                // OR: word broadcast by a GPU's owner
+    double rem, tkey;          //   remaining work, timer time
+    uint32_t c[4];             // sums
+    uint32_t mx;               // max
+    uint32_t pad;
+    uint64_t ks[2];            // sums: deferred timeline samples (cost-total parts)
+    uint64_t pad2;
+};
+static_assert(sizeof(XRec) == 96, "exchange record layout (6 x 16-byte pushes)");
+
+// A device group's inbox for the cross-group exchange: slot [parity][CTA
+// rank][sending group], each validated by a round stamp written with
+// release semantics after the record (peer-mapped across GPUs).
+struct XInbox {
+    XRec rec[2][kMaxShards][kMaxDev];
+    uint64_t stamp[2][kMaxShards][kMaxDev];  // epoch << 32 | round + 1
+};
 
 // Feature / output flags.
 enum : uint32_t {
@@ -157,6 +184,16 @@ struct SimArgs {
     uint32_t* c_gx;
     uint8_t* c_gcid;
     uint32_t smem_gpus;  // per-GPU arrays live in shared memory for G <= smem_gpus (set by launch_cluster)
+    uint32_t smem_slots; // ... and so do the per-slot arrays
+    // device groups (cluster_core.cuh): n_dev groups per trace; this launch
+    // runs groups dev0 .. dev0 + vdev - 1 of every large trace (vdev = n_dev:
+    // all groups on this GPU; vdev = 1: one group per GPU, dev0 = rank).
+    // inbox[k]: group k's exchange inbox (peer-mapped across GPUs).
+    uint32_t n_dev;
+    uint32_t dev0;
+    uint32_t vdev;
+    uint32_t epoch;    // run number of a multi-GPU group (inbox stamps need no reset between runs)
+    void* inbox[kMaxDev];
     uint32_t max_gpus;   // largest G among the large traces
 };
 

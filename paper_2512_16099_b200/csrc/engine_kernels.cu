@@ -71,14 +71,15 @@ __global__ void __launch_bounds__(kClusterThreads, 1) cluster_kernel(SimArgs a) 
     }
     __syncthreads();
     const unsigned S = wp::cluster_size();
-    const uint32_t t = a.large_idx[blockIdx.x / S];
+    const uint32_t t = a.large_idx[wp::cluster_id() / (a.vdev < 1 ? 1u : a.vdev)];
     const uint32_t G = (uint32_t)a.configs[a.traces[t].cfg].G;
     const bool in_smem = (G + S - 1) / S <= a.smem_gpus;
-    simulate_large_trace<DETAIL>(a, &tb, &sc, in_smem ? gpu_smem : nullptr, t);
+    simulate_large_trace<DETAIL>(a, &tb, &sc, in_smem ? gpu_smem : nullptr, in_smem && a.smem_slots, t);
 }
 
-// Bytes of dynamic shared memory for the per-GPU words of G GPUs.
-static size_t gpu_smem_bytes(uint32_t G) { return ((size_t)G * 9 + 15) & ~(size_t)15; }
+// Bytes of dynamic shared memory for the per-GPU words of G GPUs (and their
+// slots: 96 B more per GPU).
+static size_t gpu_smem_bytes(uint32_t G, bool slots) { return ((size_t)G * (slots ? 105 : 9) + 15) & ~(size_t)15; }
 
 template <bool DETAIL>
 static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
@@ -101,20 +102,26 @@ static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
     const size_t room = (size_t)optin > static_smem + 1024 ? (size_t)optin - static_smem - 1024 : 0;
     size_t dyn = 0;
     a.smem_gpus = 0;
-    if (gpu_smem_bytes(per) <= room) {
+    a.smem_slots = 0;
+    if (gpu_smem_bytes(per, true) <= room) {
         a.smem_gpus = per;
-        dyn = gpu_smem_bytes(per);
+        a.smem_slots = 1;
+        dyn = gpu_smem_bytes(per, true);
+    } else if (gpu_smem_bytes(per, false) <= room) {
+        a.smem_gpus = per;
+        dyn = gpu_smem_bytes(per, false);
     }
     if (dyn > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(cluster_kernel<DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         if (e != cudaSuccess) return e;
     }
-    if (S == 1) {
+    const uint32_t groups = a.n_large * (a.vdev < 1 ? 1u : a.vdev);  // clusters in this launch
+    if (S == 1 && groups == a.n_large) {
         cluster_kernel<DETAIL><<<a.n_large, kClusterThreads, dyn, stream>>>(a);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a.n_large * S);
+    cfg.gridDim = dim3(groups * S);
     cfg.blockDim = dim3(kClusterThreads);
     cfg.dynamicSmemBytes = dyn;
     cfg.stream = stream;
@@ -125,6 +132,13 @@ static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (groups > a.n_large) {
+        // device groups on one GPU spin on each other: all must be co-resident
+        int max_clusters = 0;
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&max_clusters, cluster_kernel<DETAIL>, &cfg);
+        if (e != cudaSuccess) return e;
+        if ((uint32_t)max_clusters < groups) return cudaErrorCooperativeLaunchTooLarge;
+    }
     return cudaLaunchKernelEx(&cfg, cluster_kernel<DETAIL>, a);
 }
 

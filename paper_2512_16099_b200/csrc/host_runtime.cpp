@@ -58,12 +58,14 @@ struct msg_staged {
         c_atkey, c_gw, c_gx, c_gcid;
     uint32_t large_max_g = 0;
     uint32_t large_min_g = 0;
+    const PeerBinding* peer = nullptr;  // set by msg_run_peer (host_peer.cpp) for one launch
     // pinned host mirrors (rank order)
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
     // device
     DevBuf d_arrival, d_service, d_profile, d_perm, d_traces, d_configs, d_init, d_tables_unused;
     DevBuf d_queue, d_jobs, d_events, d_timeline, d_summary;
+    DevBuf d_inbox;  // device-group exchange inboxes (MSG_VDEV > 1)
 };
 
 namespace {
@@ -80,15 +82,51 @@ struct PhaseTimer {
 };
 }  // namespace
 
+namespace {
+// Recycled per-job row buffers: a batch result's rows (72 B per job) go back
+// here when the result is freed, so repeated batches of similar size write
+// into already-faulted pages instead of fresh allocations.
+struct RowBuf {
+    std::unique_ptr<msg_job_row[]> p;
+    uint64_t cap = 0;
+};
+std::mutex g_rows_m;
+std::vector<RowBuf> g_rows;
+
+RowBuf take_rows(uint64_t n) {
+    {
+        std::lock_guard<std::mutex> lk(g_rows_m);
+        for (size_t i = 0; i < g_rows.size(); ++i) {
+            if (g_rows[i].cap >= n && g_rows[i].cap <= 2 * n + 1024) {
+                RowBuf b = std::move(g_rows[i]);
+                g_rows.erase(g_rows.begin() + (long)i);
+                return b;
+            }
+        }
+    }
+    RowBuf b;
+    b.cap = std::max<uint64_t>(n, 1);
+    b.p.reset(new msg_job_row[b.cap]);
+    return b;
+}
+
+void give_rows(RowBuf&& b) {
+    if (!b.p) return;
+    std::lock_guard<std::mutex> lk(g_rows_m);
+    if (g_rows.size() < 2) g_rows.push_back(std::move(b));
+}
+}  // namespace
+
 struct msg_batch_result {
     std::vector<msg_trace_summary> summaries;
     std::vector<std::string> messages;
     bool has_jobs = false;
-    std::unique_ptr<msg_job_row[]> jobs;  // all traces, trace-major (filled in parallel, no zero-init pass)
+    RowBuf jobs;  // all traces, trace-major (filled in parallel, no zero-init pass)
     uint64_t n_jobs_all = 0;
     std::vector<uint64_t> job_off;        // n_traces + 1
     std::vector<std::vector<msg_event>> events;
     std::vector<std::vector<msg_timeline_point>> timeline;
+    ~msg_batch_result() { give_rows(std::move(jobs)); }
 };
 
 namespace {
@@ -272,8 +310,23 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
 // CTAs per large trace (cluster_core.cuh): >= 1024 GPUs per shard, up to
 // kMaxShards; 1 when any large trace is within the exact-timeline size or
 // the event log is requested.  MSG_SHARDS overrides the count (tuning).
+bool shardable(uint32_t min_g, uint32_t out_flags) {
+    return min_g > (uint32_t)kExactTimelineGpus && !(out_flags & OF_EVENTS);
+}
+
+// Device groups per large trace on this GPU (MSG_VDEV; default 1): the
+// multi-GPU exchange protocol exercised with all groups on one device.
+uint32_t choose_vdev(uint32_t min_g, uint32_t out_flags, uint32_t shards) {
+    const char* e = std::getenv("MSG_VDEV");
+    if (!e || !shardable(min_g, out_flags)) return 1;
+    const int v = std::atoi(e);
+    uint32_t D = v < 1 ? 1u : std::min<uint32_t>((uint32_t)v, (uint32_t)kMaxDev);
+    while (D > 1 && min_g < D * shards) --D;
+    return D;
+}
+
 uint32_t choose_shards(uint32_t min_g, uint32_t out_flags) {
-    if (min_g <= (uint32_t)kExactTimelineGpus || (out_flags & OF_EVENTS)) return 1;
+    if (!shardable(min_g, out_flags)) return 1;
     uint32_t S = 1;
     if (const char* e = std::getenv("MSG_SHARDS")) {
         const int v = std::atoi(e);
@@ -317,6 +370,8 @@ SimArgs make_args(msg_engine* eng, msg_staged* s) {
         a.c_atkey = s->c_atkey.as<double>();
         a.max_gpus = s->large_max_g;
         a.shards = choose_shards(s->large_min_g, s->out_flags);
+        a.n_dev = a.vdev = choose_vdev(s->large_min_g, s->out_flags, a.shards);
+        a.dev0 = 0;  // inboxes are bound at launch (launch_impl)
         a.c_gw = s->c_gw.as<uint32_t>();
         a.c_gx = s->c_gx.as<uint32_t>();
         a.c_gcid = s->c_gcid.as<uint8_t>();
@@ -326,13 +381,44 @@ SimArgs make_args(msg_engine* eng, msg_staged* s) {
 
 msg_status launch_impl(msg_engine* eng, msg_staged* s) {
     if (s->traces.empty()) return MSG_OK;
-    const SimArgs a = make_args(eng, s);
+    SimArgs a = make_args(eng, s);
+    if (s->peer) {  // one group of a multi-GPU run: this GPU's part of the trace
+        const PeerBinding& pb = *s->peer;
+        a.n_dev = pb.world;
+        a.dev0 = pb.rank;
+        a.vdev = 1;
+        for (uint32_t k = 0; k < pb.world; ++k) a.inbox[k] = pb.inbox[k];
+        a.jobs = static_cast<JobOut*>(pb.jobs);
+        a.summary = static_cast<DevSummary*>(pb.summary);
+        a.timeline = static_cast<double*>(pb.timeline);
+        cudaError_t e = launch_cluster(a, eng->stream);
+        if (e != cudaSuccess) return cuda_fail(eng, e, "launch_cluster (peer)");
+        ++eng->launches;
+        return MSG_OK;
+    }
     if (s->any_small) {
         cudaError_t e = launch_sim(s->spl, a, eng->stream);
         if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim");
         ++eng->launches;
     }
     if (a.n_large) {
+        if (a.n_dev > 1) {
+            const size_t bytes = (size_t)a.n_dev * a.n_large * sizeof(XInbox);
+            CK(s->d_inbox.ensure(bytes));
+            SimArgs b = a;  // one XInbox per (group, large trace); stamps zeroed per launch
+            for (uint32_t k = 0; k < a.n_dev; ++k)
+                b.inbox[k] = static_cast<char*>(s->d_inbox.p) + k * (size_t)a.n_large * sizeof(XInbox);
+            CK(cudaMemsetAsync(s->d_inbox.p, 0, bytes, eng->stream));
+            cudaError_t e = launch_cluster(b, eng->stream);
+            if (e == cudaErrorCooperativeLaunchTooLarge)
+            {
+                eng->last_error = "Unsupported: device groups do not fit co-resident on this GPU";
+                return MSG_ERR_UNSUPPORTED;
+            }
+            if (e != cudaSuccess) return cuda_fail(eng, e, "launch_cluster");
+            ++eng->launches;
+            return MSG_OK;
+        }
         cudaError_t e = launch_cluster(a, eng->stream);
         if (e != cudaSuccess) return cuda_fail(eng, e, "launch_cluster");
         ++eng->launches;
@@ -407,7 +493,7 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
             res->job_off[t + 1] = res->job_off[t] + (rows ? s->traces[d].n_jobs : 0);
         }
         res->n_jobs_all = res->job_off[s->n_in];
-        res->jobs.reset(new msg_job_row[std::max<uint64_t>(res->n_jobs_all, 1)]);
+        res->jobs = take_rows(res->n_jobs_all);
     }
     if (want_ev) res->events.resize(s->n_in);
     if (want_tl) res->timeline.resize(s->n_in);
@@ -453,7 +539,7 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
             return;  // the reference throws: no report, no log
         }
         if (want_jobs) {
-            msg_job_row* rows = res->jobs.get() + res->job_off[t];
+            msg_job_row* rows = res->jobs.p.get() + res->job_off[t];
             for (uint32_t r = 0; r < tr.n_jobs; ++r) {
                 const JobOut& j = hj[tr.job_off + r];
                 msg_job_row& row = rows[r];
@@ -641,7 +727,7 @@ const msg_job_row* msg_result_jobs(const msg_batch_result* r, uint32_t t, uint64
     if (n) *n = 0;
     if (!r || !r->has_jobs || t + 1 >= r->job_off.size()) return nullptr;
     if (n) *n = r->job_off[t + 1] - r->job_off[t];
-    return r->jobs.get() + r->job_off[t];
+    return r->jobs.p.get() + r->job_off[t];
 }
 
 const msg_trace_summary* msg_result_summaries(const msg_batch_result* r) {
@@ -654,7 +740,7 @@ const msg_job_row* msg_result_all_jobs(const msg_batch_result* r, const uint64_t
     if (!r || !r->has_jobs) return nullptr;
     if (offsets) *offsets = r->job_off.data();
     if (n) *n = r->n_jobs_all;
-    return r->jobs.get();
+    return r->jobs.p.get();
 }
 
 const msg_event* msg_result_events(const msg_batch_result* r, uint32_t t, uint64_t* n) {

@@ -5,35 +5,109 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "dev_types.h"
 #include "migsched_b200.h"
 
 namespace msgk {
 
+// Persistent fork-join pool for the host-side staging / decoding loops: the
+// workers are created once (hardware_concurrency - 1) and woken per call, so
+// a batch pays no thread creation.  One parallel region at a time (calls
+// from several host threads serialise on the pool).
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool p;
+        return p;
+    }
+    unsigned size() const { return (unsigned)workers_.size() + 1; }
+    // Runs body() on `n` threads (the caller included) and returns when all finished.
+    template <class B>
+    void run(unsigned n, B&& body) {
+        std::lock_guard<std::mutex> one(region_);
+        n = std::min(n, size());
+        if (n <= 1) {
+            body();
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            body_ = [&body]() { body(); };
+            want_ = n - 1;
+            left_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        body();
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [&] { return left_ == 0; });
+        body_ = nullptr;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+  private:
+    HostPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::function<void()> b;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && want_ > 0); });
+                if (stop_) return;
+                seen = gen_;
+                --want_;
+                b = body_;
+            }
+            b();
+            std::lock_guard<std::mutex> lk(m_);
+            if (--left_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex m_, region_;
+    std::condition_variable cv_, done_;
+    std::function<void()> body_;
+    uint64_t gen_ = 0;
+    unsigned want_ = 0, left_ = 0;
+    bool stop_ = false;
+};
+
 template <class F>
 void parallel_for(uint32_t n, uint32_t min_per_thread, F&& f) {
-    uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
-    uint32_t threads = std::min(hw, std::max(1u, n / std::max(1u, min_per_thread)));
+    HostPool& pool = HostPool::get();
+    const uint32_t threads = std::min(pool.size(), std::max(1u, n / std::max(1u, min_per_thread)));
     if (threads <= 1) {
         for (uint32_t i = 0; i < n; ++i) f(i);
         return;
     }
     std::atomic<uint32_t> next{0};
-    auto worker = [&]() {
+    pool.run(threads, [&]() {
         for (;;) {
             const uint32_t base = next.fetch_add(16);
             if (base >= n) return;
             const uint32_t end = std::min(n, base + 16);
             for (uint32_t i = base; i < end; ++i) f(i);
         }
-    };
-    std::vector<std::thread> pool;
-    for (uint32_t t = 1; t < threads; ++t) pool.emplace_back(worker);
-    worker();
-    for (auto& th : pool) th.join();
+    });
 }
 
 struct DevBuf {
@@ -83,6 +157,18 @@ struct HostBuf {
 }  // namespace msgk
 
 struct msg_staged;
+
+namespace msgk {
+// Device pointers of one multi-GPU launch (host_peer.cpp): every group's
+// inbox (peer-mapped), and group 0's job rows / summary / timeline.
+struct PeerBinding {
+    uint32_t world = 1, rank = 0;
+    void* inbox[kMaxDev] = {};
+    void* jobs = nullptr;
+    void* summary = nullptr;
+    void* timeline = nullptr;
+};
+}  // namespace msgk
 
 struct msg_engine {
     int device = 0;

@@ -34,6 +34,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 #include "decide.h"
 #include "dev_types.h"
@@ -73,13 +75,16 @@ struct Prof {
 //    ADD (an overlapping start is unavailable and masked, so the sum only has
 //    to stay in bounds: 7 * 256 + 255 + 255 < 2304);
 //  avail[p * 256 + km]: bit j set iff start j of profile p is memory-disjoint
-//    from the blocked mask km (gpu.cpp:146-156: availability = disjointness);
+//    from the blocked mask km (gpu.cpp:146-156: availability = disjointness),
+//    and the number of such starts << 8;
 //  bct[p * 128 + busy_c]: 4 * 256 * min(popc(busy_c) + cs_p, 7) | !lazy << 31
-//    (classify, gpu.cpp:168-177, through the host-built lazy mask).
+//    | (lazy ? 16 : 0) (classify, gpu.cpp:168-177, through the host-built lazy
+//    mask; the low field is the shift that files the word's candidate count
+//    under Lazy (high half) or Busy (low half) of a packed counter).
 struct ScoreSmem {
     uint32_t rank26[2304];
     uint32_t bct[6 * 128];
-    uint8_t avail[6 * 256];
+    uint16_t avail[6 * 256];
 };
 
 __device__ __forceinline__ void score_smem_init(ScoreSmem& s, const DevTables* tb, unsigned lazymask) {
@@ -92,20 +97,20 @@ __device__ __forceinline__ void score_smem_init(ScoreSmem& s, const DevTables* t
         unsigned a = 0;
         for (unsigned j = 0; j < n; ++j)
             if (!((((1u << ms) - 1u) << (j * st)) & km)) a |= 1u << j;
-        s.avail[i] = (uint8_t)a;
+        s.avail[i] = (uint16_t)(a | (unsigned)__popc(a) << 8);
     }
     for (unsigned i = threadIdx.x; i < 6 * 128; i += blockDim.x) {
         const unsigned p = i >> 7, pc = (unsigned)__popc(i & 0x7Fu);
         const unsigned cs = (kCsPack >> (4 * p)) & 0xFu;
-        s.bct[i] = (min(pc + cs, 7u) << 10) | ((((lazymask >> pc) & 1u) ^ 1u) << 31);
+        const unsigned lazy = (lazymask >> pc) & 1u;
+        s.bct[i] = (min(pc + cs, 7u) << 10) | ((lazy ^ 1u) << 31) | (lazy << 4);
     }
 }
 
 // Running per-thread state of one item.
 struct ItemAcc {
     unsigned best;   // item-local key minimum
-    unsigned all;    // candidates
-    unsigned lazy;   // candidates on Lazy GPUs
+    unsigned cnt;    // candidates: Lazy << 16 | Busy
     unsigned anyx;   // idle-exact bits of the profile seen in the current chunk
 };
 
@@ -119,8 +124,11 @@ template <int P, bool LB, bool DYN, bool REUSE>
 __device__ __forceinline__ void score_word(const ScoreSmem& sm, uint64_t w, unsigned local, ItemAcc& acc) {
     using Q = Prof<P>;
     const unsigned lo = (unsigned)w;
-    unsigned A = sm.avail[P * 256 + ((lo >> 16) & 0xFFu)];
-    if (!DYN) A &= (unsigned)(w >> (24 + Q::pbase));  // candidate_starts: exact idle instances only
+    unsigned A = sm.avail[P * 256 + ((lo >> 16) & 0xFFu)];  // starts | count << 8
+    if (!DYN) {  // candidate_starts: exact idle instances only
+        A &= (unsigned)(w >> (24 + Q::pbase)) & ((1u << Q::n) - 1u);
+        A |= (unsigned)__popc(A) << 8;
+    }
     if (LB) {
         const unsigned v = sm.bct[P * 128 + (lo & 0x7Fu)];
         // row byte offset | busy_m * 4: the LUT row of popc(busy_c | fc), column busy_m
@@ -141,14 +149,13 @@ __device__ __forceinline__ void score_word(const ScoreSmem& sm, uint64_t w, unsi
                 const unsigned key = rp[Q::fm(j)] | head | (j * Q::stride);
                 acc.best = ((A >> j) & 1u) ? min(acc.best, key) : acc.best;
             }
-            const unsigned c = __popc(A);
-            acc.all += c;
-            acc.lazy += (int)v >= 0 ? c : 0u;
+            acc.cnt += __funnelshift_l(0u, A >> 8, v);  // (A >> 8) << (v & 31)
             if (DYN) acc.anyx |= (unsigned)((w & Q::xmask) >> 24);
         }
     } else if (!REUSE) {
-        const unsigned key = (local << 3) | ((unsigned)(__ffs(A) - 1) * Q::stride);
-        acc.best = A ? min(acc.best, key) : acc.best;
+        const unsigned a7 = A & 0x7Fu;
+        const unsigned key = (local << 3) | ((unsigned)(__ffs(a7) - 1) * Q::stride);
+        acc.best = a7 ? min(acc.best, key) : acc.best;
     }
 }
 
@@ -200,44 +207,13 @@ struct Cursor {
     uint32_t prof;                    // the snapshot's job profile (loaded with the item's first chunk)
 };
 
-// One item: its chunks are scored with the profile's specialised code while
-// the following chunk (possibly the next item's first) is in flight.
-template <int P, bool LB, bool DYN>
-__device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& sm, ChunkData& cur, Cursor& cu,
-                                           uint32_t chunks_per, uint32_t n_items, uint32_t items_per) {
-    ItemAcc acc{0xFFFFFFFFu, 0u, 0u, 0u};
-    const uint32_t snap = cu.snap, first = cu.chunk;
-    for (;;) {
-        // advance the cursor and prefetch
-        Cursor nx = cu;
-        bool more = true;
-        if (++nx.chunk >= nx.end) {
-            nx.item += gridDim.x;
-            more = nx.item < n_items;
-            if (more) {
-                nx.snap = nx.item / items_per;
-                nx.chunk = (nx.item - nx.snap * items_per) * kItemChunks;
-                nx.end = min(nx.chunk + kItemChunks, chunks_per);
-                nx.prof = a.profile[nx.snap];
-            }
-        }
-        ChunkData next;
-        if (more) next = load_chunk(a, nx.snap, (uint64_t)nx.chunk * kChunk);
-        const unsigned base = (cu.chunk - first) * kChunk;
-        acc.anyx = 0;
-        score_chunk<P, LB, DYN, false>(sm, cur, base, acc);
-        if (LB && DYN && __any_sync(0xffffffffu, acc.anyx != 0)) score_chunk<P, LB, DYN, true>(sm, cur, base, acc);
-        const bool done = nx.item != cu.item;
-        cur = next;
-        cu = nx;
-        if (done || !more) break;
-    }
+// End of an item: the warp's minimum key, rebased from the item-local word
+// index to the global GPU index, and its candidate counts, merged into the
+// snapshot's slots with one 64-bit atomicMin / atomicAdd.
+template <bool LB>
+__device__ __forceinline__ void flush_item(const ScoreArgs& a, const ItemAcc& acc, uint32_t snap, uint32_t first) {
     const unsigned best = __reduce_min_sync(0xffffffffu, acc.best);
-    unsigned all = 0, lazy = 0;
-    if (LB) {
-        all = __reduce_add_sync(0xffffffffu, acc.all);
-        lazy = __reduce_add_sync(0xffffffffu, acc.lazy);
-    }
+    const unsigned cnt = LB ? __reduce_add_sync(0xffffffffu, acc.cnt) : 0u;
     if ((threadIdx.x & 31) == 0) {
         if (best != 0xFFFFFFFFu) {
             // item-local [pass|rank|!reused|word|start] -> global [pass|rank|!reused|gpu:32|start]
@@ -245,10 +221,57 @@ __device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& 
             const uint64_t g64 = ((uint64_t)(best >> 25) << 35) | (gpu << 3) | (best & 7u);
             atomicMin(reinterpret_cast<unsigned long long*>(a.out + 2 * snap), (unsigned long long)g64);
         }
-        if (LB && all)
+        if (LB && cnt)
             atomicAdd(reinterpret_cast<unsigned long long*>(a.out + 2 * snap + 1),
-                      ((unsigned long long)lazy << 32) | (all - lazy));
+                      ((unsigned long long)(cnt >> 16) << 32) | (cnt & 0xFFFFu));
     }
+}
+
+// Scores `c` (the cursor's chunk) while the following chunk loads into
+// `n`; advances the cursor; true when the item is finished.
+template <int P, bool LB, bool DYN>
+__device__ __forceinline__ bool score_step(const ScoreArgs& a, const ScoreSmem& sm, const ChunkData& c, ChunkData& n,
+                                           Cursor& cu, ItemAcc& acc, uint32_t first, uint32_t chunks_per,
+                                           uint32_t n_items, uint32_t items_per) {
+    Cursor nx = cu;
+    bool more = true;
+    if (++nx.chunk >= nx.end) {
+        nx.item += gridDim.x;
+        more = nx.item < n_items;
+        if (more) {
+            nx.snap = nx.item / items_per;
+            nx.chunk = (nx.item - nx.snap * items_per) * kItemChunks;
+            nx.end = min(nx.chunk + kItemChunks, chunks_per);
+            nx.prof = a.profile[nx.snap];
+        }
+    }
+    if (more) n = load_chunk(a, nx.snap, (uint64_t)nx.chunk * kChunk);
+    const unsigned base = (cu.chunk - first) * kChunk;
+    acc.anyx = 0;
+    score_chunk<P, LB, DYN, false>(sm, c, base, acc);
+    if (LB && DYN && __any_sync(0xffffffffu, acc.anyx != 0)) score_chunk<P, LB, DYN, true>(sm, c, base, acc);
+    const bool done = nx.item != cu.item || !more;
+    cu = nx;
+    return done;
+}
+
+// One item: its chunks are scored with the profile's specialised code while
+// the following chunk (possibly the next item's first) is in flight.
+template <int P, bool LB, bool DYN>
+__device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& sm, ChunkData& cur, Cursor& cu,
+                                           uint32_t chunks_per, uint32_t n_items, uint32_t items_per) {
+    ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
+    const uint32_t snap = cu.snap, first = cu.chunk;
+    // ping-pong between two register buffers (no copies on the steady path)
+    ChunkData other;
+    for (;;) {
+        if (score_step<P, LB, DYN>(a, sm, cur, other, cu, acc, first, chunks_per, n_items, items_per)) {
+            cur = other;
+            break;
+        }
+        if (score_step<P, LB, DYN>(a, sm, other, cur, cu, acc, first, chunks_per, n_items, items_per)) break;
+    }
+    flush_item<LB>(a, acc, snap, first);
 }
 
 template <bool LB, bool DYN>
@@ -279,6 +302,281 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_kernel(Sc
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant (the default when the snapshot rows are 16-byte aligned:
+// even G, 16-byte aligned words).  One elected thread streams the block's
+// chunk sequence into a kStages-deep ring of shared-memory buffers with 1-D
+// bulk async copies (cp.async.bulk ... mbarrier::complete_tx), so each SM
+// keeps kStages x 8 KiB x blocks of HBM reads in flight without holding them
+// in registers; the block consumes a stage after its mbarrier phase
+// completes (LDS.128 per two words) and hands it back with one
+// __syncthreads.  Per-stage metadata (snapshot, item base, valid words,
+// profile, item end) travels with the copy.
+#ifndef MSG_SCORE_STAGES
+#define MSG_SCORE_STAGES 4
+#endif
+constexpr int kStages = MSG_SCORE_STAGES;
+
+struct StageMeta {
+    uint32_t snap;    // 0xFFFFFFFF: end of the block's sequence
+    uint32_t base;    // item-local index of the chunk's first word
+    uint32_t nvalid;  // words copied (< kChunk only in a snapshot's last chunk)
+    uint32_t prof;    // the snapshot's job profile
+    uint32_t first;   // first chunk of the item
+    uint32_t last;    // chunk ends its item
+    uint32_t pad[2];
+};
+
+// The stage ring lives in dynamic shared memory (beyond the 48 KiB static limit).
+struct TmaSmem {
+    ScoreSmem& t;             // static: the scoring tables
+    uint64_t (*buf)[kChunk];  // [kStages][kChunk]
+    uint64_t* full;           // [kStages]
+    StageMeta* meta;          // [kStages]
+};
+constexpr size_t kTmaDynBytes = sizeof(uint64_t) * kChunk * kStages + 8 * kStages + sizeof(StageMeta) * kStages;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Producer cursor over the block's (item, chunk) sequence (thread 0 only).
+struct Producer {
+    uint32_t item, snap, chunk, first, end, prof;
+    bool done;
+};
+
+__device__ __forceinline__ void prod_start_item(const ScoreArgs& a, Producer& p, uint32_t chunks_per,
+                                                uint32_t items_per, uint32_t n_items) {
+    if (p.item >= n_items) {
+        p.done = true;
+        return;
+    }
+    p.snap = p.item / items_per;
+    p.first = p.chunk = (p.item - p.snap * items_per) * kItemChunks;
+    p.end = min(p.first + kItemChunks, chunks_per);
+    p.prof = a.profile[p.snap];
+}
+
+// Issue the next chunk of the sequence into `stage` (or the end marker).
+__device__ __forceinline__ void prod_issue(const ScoreArgs& a, TmaSmem& sm, Producer& p, int stage,
+                                           uint32_t chunks_per, uint32_t items_per, uint32_t n_items) {
+    StageMeta& m = sm.meta[stage];
+    if (p.done) {
+        m.snap = 0xFFFFFFFFu;
+        mbar_arrive(&sm.full[stage]);
+        return;
+    }
+    const uint64_t c0 = (uint64_t)p.chunk * kChunk;
+    const uint64_t rem = a.G - c0;
+    const uint32_t nvalid = rem < (uint64_t)kChunk ? (uint32_t)rem : (uint32_t)kChunk;
+    m.snap = p.snap;
+    m.base = (p.chunk - p.first) * kChunk;
+    m.nvalid = nvalid;
+    m.prof = p.prof;
+    m.first = p.first;
+    m.last = p.chunk + 1 >= p.end;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage's previous reads precede the copy
+    mbar_arrive_tx(&sm.full[stage], nvalid * 8u);
+    bulk_load(sm.buf[stage], a.words + (uint64_t)p.snap * a.G + c0, nvalid * 8u, &sm.full[stage]);
+    if (++p.chunk >= p.end) {
+        p.item += gridDim.x;
+        prod_start_item(a, p, chunks_per, items_per, n_items);
+    }
+}
+
+template <int P, bool LB, bool DYN, bool REUSE>
+__device__ __forceinline__ void score_stage(const TmaSmem& sm, int stage, const StageMeta& m, ItemAcc& acc) {
+    constexpr uint64_t kFull = 0xFFFF7Full;
+    const ulonglong2* v = reinterpret_cast<const ulonglong2*>(sm.buf[stage]);
+    const unsigned t2 = threadIdx.x * 2u;
+    const bool whole = m.nvalid == (uint32_t)kChunk;
+#pragma unroll
+    for (int k = 0; k < kWordsPerThread / 2; ++k) {
+        const unsigned l = t2 + (unsigned)k * 2 * kScoreThreads;
+        const ulonglong2 x = v[threadIdx.x + (unsigned)k * kScoreThreads];
+        score_word<P, LB, DYN, REUSE>(sm.t, whole || l < m.nvalid ? x.x : kFull, m.base + l, acc);
+        score_word<P, LB, DYN, REUSE>(sm.t, whole || l + 1 < m.nvalid ? x.y : kFull, m.base + l + 1, acc);
+    }
+}
+
+template <int P, bool LB, bool DYN>
+__device__ __forceinline__ void consume_stage(const ScoreArgs& a, const TmaSmem& sm, int stage, const StageMeta& m,
+                                              ItemAcc& acc) {
+    acc.anyx = 0;
+    score_stage<P, LB, DYN, false>(sm, stage, m, acc);
+    if (LB && DYN && __any_sync(0xffffffffu, acc.anyx != 0)) score_stage<P, LB, DYN, true>(sm, stage, m, acc);
+    if (m.last) {
+        flush_item<LB>(a, acc, m.snap, m.first);
+        acc = ItemAcc{0xFFFFFFFFu, 0u, 0u};
+    }
+}
+
+// Pass 1 of load-balanced scoring (scheduler.cpp:47-81 scores Lazy GPUs first
+// and Busy GPUs only when no Lazy GPU has a candidate): only Lazy words are
+// scored.  Each warp classifies its 32 x kWordsPerThread words of the stage
+// with one table lookup each, compacts the Lazy ones into a per-warp index
+// list (ballot + prefix popc), and scores the list with all 32 lanes, so the
+// per-start work is spent on Lazy words only.  Snapshots left without a Lazy
+// candidate are completed by score_busy_kernel (pass 2).
+template <int P, bool DYN>
+__device__ __forceinline__ void consume_lazy(const ScoreArgs& a, const TmaSmem& sm, int stage, const StageMeta& m,
+                                             ItemAcc& acc, uint16_t* wl) {
+    const uint64_t* buf = sm.buf[stage];
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const unsigned wbase = warp * 32u * kWordsPerThread;
+    const unsigned lt = (1u << lane) - 1u;
+    // classify's lazy set is {popc(busy_c) < K} (pc / 7.0 < threshold is monotone in pc)
+    const int K = __popc(a.lazymask & 0xFFu);
+    const bool whole = m.nvalid == (uint32_t)kChunk;
+    unsigned n = 0;
+#pragma unroll
+    for (int k = 0; k < kWordsPerThread; ++k) {
+        const unsigned idx = wbase + (unsigned)k * 32u + lane;
+        const unsigned lo = reinterpret_cast<const uint32_t*>(buf)[2 * idx];
+        const bool lz = (whole || idx < m.nvalid) && __popc(lo & 0x7Fu) < K;
+        const unsigned bal = __ballot_sync(0xffffffffu, lz);
+        if (lz) wl[n + __popc(bal & lt)] = (uint16_t)idx;
+        n += __popc(bal);
+    }
+    __syncwarp();
+    acc.anyx = 0;
+    for (unsigned i = lane; i < n; i += 32) {
+        const unsigned idx = wl[i];
+        score_word<P, true, DYN, false>(sm.t, buf[idx], m.base + idx, acc);
+    }
+    if (DYN && __any_sync(0xffffffffu, acc.anyx != 0)) {
+        for (unsigned i = lane; i < n; i += 32) {
+            const unsigned idx = wl[i];
+            score_word<P, true, DYN, true>(sm.t, buf[idx], m.base + idx, acc);
+        }
+    }
+    __syncwarp();
+    if (m.last) {
+        flush_item<true>(a, acc, m.snap, m.first);
+        acc = ItemAcc{0xFFFFFFFFu, 0u, 0u};
+    }
+}
+
+template <bool LB, bool DYN>
+__global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kernel(ScoreArgs a) {
+    __shared__ __align__(16) ScoreSmem tables;
+    __shared__ uint16_t wlist[kScoreThreads / 32][32 * kWordsPerThread];  // pass 1: Lazy words per warp
+    extern __shared__ __align__(128) unsigned char ring[];
+    TmaSmem sm{tables, reinterpret_cast<uint64_t(*)[kChunk]>(ring),
+               reinterpret_cast<uint64_t*>(ring + sizeof(uint64_t) * kChunk * kStages),
+               reinterpret_cast<StageMeta*>(ring + sizeof(uint64_t) * kChunk * kStages + 8 * kStages)};
+    score_smem_init(sm.t, a.tables, a.lazymask);
+    const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
+    const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
+    const uint32_t n_items = items_per * a.n;
+    Producer p;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&sm.full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        p.item = blockIdx.x;
+        p.done = false;
+        prod_start_item(a, p, chunks_per, items_per, n_items);
+        for (int s = 0; s < kStages; ++s) prod_issue(a, sm, p, s, chunks_per, items_per, n_items);
+    }
+    __syncthreads();
+    ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
+    for (uint32_t n = 0;; ++n) {
+        const int stage = (int)(n % kStages);
+        mbar_wait(&sm.full[stage], (n / kStages) & 1u);
+        const StageMeta m = sm.meta[stage];
+        if (m.snap == 0xFFFFFFFFu) break;
+        uint16_t* wl = wlist[threadIdx.x >> 5];
+        if (LB) {
+            switch (m.prof) {
+                case 0: consume_lazy<0, DYN>(a, sm, stage, m, acc, wl); break;
+                case 1: consume_lazy<1, DYN>(a, sm, stage, m, acc, wl); break;
+                case 2: consume_lazy<2, DYN>(a, sm, stage, m, acc, wl); break;
+                case 3: consume_lazy<3, DYN>(a, sm, stage, m, acc, wl); break;
+                case 4: consume_lazy<4, DYN>(a, sm, stage, m, acc, wl); break;
+                default: consume_lazy<5, DYN>(a, sm, stage, m, acc, wl); break;
+            }
+        } else {
+            switch (m.prof) {
+                case 0: consume_stage<0, LB, DYN>(a, sm, stage, m, acc); break;
+                case 1: consume_stage<1, LB, DYN>(a, sm, stage, m, acc); break;
+                case 2: consume_stage<2, LB, DYN>(a, sm, stage, m, acc); break;
+                case 3: consume_stage<3, LB, DYN>(a, sm, stage, m, acc); break;
+                case 4: consume_stage<4, LB, DYN>(a, sm, stage, m, acc); break;
+                default: consume_stage<5, LB, DYN>(a, sm, stage, m, acc); break;
+            }
+        }
+        __syncthreads();  // every thread is done with the stage
+        if (threadIdx.x == 0) prod_issue(a, sm, p, stage, chunks_per, items_per, n_items);
+    }
+}
+
+// Pass 2 (after score_tma_kernel<true, DYN>): snapshots whose pass 1 found no
+// Lazy candidate are scored again over all words with the full key (Busy
+// GPUs compete; their candidates are counted), exactly as the register path.
+template <bool DYN>
+__global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) {
+    __shared__ __align__(16) ScoreSmem sm;
+    score_smem_init(sm, a.tables, a.lazymask);
+    __syncthreads();
+    const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
+    const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
+    const uint32_t n_items = items_per * a.n;
+    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const uint32_t snap = item / items_per;
+        if ((a.out[2 * snap + 1] >> 32) != 0) continue;  // pass 1 found Lazy candidates
+        const uint32_t first = (item - snap * items_per) * kItemChunks, end = min(first + kItemChunks, chunks_per);
+        ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
+        const unsigned prof = a.profile[snap];
+        for (uint32_t c = first; c < end; ++c) {
+            const ChunkData d = load_chunk(a, snap, (uint64_t)c * kChunk);
+            const unsigned base = (c - first) * kChunk;
+            acc.anyx = 0;
+            switch (prof) {
+                case 0: score_chunk<0, true, DYN, false>(sm, d, base, acc); break;
+                case 1: score_chunk<1, true, DYN, false>(sm, d, base, acc); break;
+                case 2: score_chunk<2, true, DYN, false>(sm, d, base, acc); break;
+                case 3: score_chunk<3, true, DYN, false>(sm, d, base, acc); break;
+                case 4: score_chunk<4, true, DYN, false>(sm, d, base, acc); break;
+                default: score_chunk<5, true, DYN, false>(sm, d, base, acc); break;
+            }
+            if (DYN && __any_sync(0xffffffffu, acc.anyx != 0)) {
+                switch (prof) {
+                    case 0: score_chunk<0, true, DYN, true>(sm, d, base, acc); break;
+                    case 1: score_chunk<1, true, DYN, true>(sm, d, base, acc); break;
+                    case 2: score_chunk<2, true, DYN, true>(sm, d, base, acc); break;
+                    case 3: score_chunk<3, true, DYN, true>(sm, d, base, acc); break;
+                    case 4: score_chunk<4, true, DYN, true>(sm, d, base, acc); break;
+                    default: score_chunk<5, true, DYN, true>(sm, d, base, acc); break;
+                }
+            }
+        }
+        flush_item<true>(a, acc, snap, first);
+    }
+}
+
 __global__ void score_init_kernel(uint64_t* out, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
@@ -290,29 +588,49 @@ __global__ void score_init_kernel(uint64_t* out, uint32_t n) {
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     if (!a.n || !a.G) return cudaSuccess;
     score_init_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(a.out, a.n);
-    static int sms = 0, per_sm[4] = {0, 0, 0, 0};
+    static int sms = 0, per_sm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int dyn = (int)kTmaDynBytes;
+        cudaFuncSetAttribute(score_tma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(score_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(score_tma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(score_tma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], score_kernel<false, false>, kScoreThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], score_kernel<false, true>, kScoreThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], score_kernel<true, false>, kScoreThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[3], score_kernel<true, true>, kScoreThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[4], score_tma_kernel<false, false>, kScoreThreads, dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[5], score_tma_kernel<false, true>, kScoreThreads, dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[6], score_tma_kernel<true, false>, kScoreThreads, dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[7], score_tma_kernel<true, true>, kScoreThreads, dyn);
     }
     const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
     const uint64_t items = ((chunks_per + kItemChunks - 1) / kItemChunks) * a.n;
     if (chunks_per > 0xFFFFFFFFull || items > 0xFFFFFFFFull) return cudaErrorInvalidValue;
+    // bulk copies need 16-byte aligned rows; MSG_SCORE_REG forces the register-streaming kernel
+    static const bool force_reg = std::getenv("MSG_SCORE_REG") != nullptr;
+    const bool tma = !force_reg && (a.G & 1) == 0 && (reinterpret_cast<uintptr_t>(a.words) & 15) == 0;
+    const int v = (tma ? 4 : 0) + (a.lb ? 2 : 0) + (a.dyn ? 1 : 0);
     // persistent grid: exactly the resident blocks (one wave)
-    const int resident = std::max(1, per_sm[(a.lb ? 2 : 0) + (a.dyn ? 1 : 0)]);
-    const uint64_t blocks = std::min<uint64_t>(items, (uint64_t)sms * resident);
+    const uint64_t blocks = std::min<uint64_t>(items, (uint64_t)sms * std::max(1, per_sm[v]));
     const dim3 grid((unsigned)blocks), block(kScoreThreads);
-    if (a.lb) {
-        if (a.dyn) score_kernel<true, true><<<grid, block, 0, stream>>>(a);
-        else score_kernel<true, false><<<grid, block, 0, stream>>>(a);
-    } else {
-        if (a.dyn) score_kernel<false, true><<<grid, block, 0, stream>>>(a);
-        else score_kernel<false, false><<<grid, block, 0, stream>>>(a);
+    switch (v) {
+        case 0: score_kernel<false, false><<<grid, block, 0, stream>>>(a); break;
+        case 1: score_kernel<false, true><<<grid, block, 0, stream>>>(a); break;
+        case 2: score_kernel<true, false><<<grid, block, 0, stream>>>(a); break;
+        case 3: score_kernel<true, true><<<grid, block, 0, stream>>>(a); break;
+        case 4: score_tma_kernel<false, false><<<grid, block, kTmaDynBytes, stream>>>(a); break;
+        case 5: score_tma_kernel<false, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
+        case 6: score_tma_kernel<true, false><<<grid, block, kTmaDynBytes, stream>>>(a); break;
+        default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
+    }
+    if (tma && a.lb) {  // pass 2: snapshots without a Lazy candidate
+        const dim3 g2((unsigned)std::min<uint64_t>(items, (uint64_t)sms * 4));
+        if (a.dyn) score_busy_kernel<true><<<g2, block, 0, stream>>>(a);
+        else score_busy_kernel<false><<<g2, block, 0, stream>>>(a);
     }
     return cudaGetLastError();
 }

@@ -43,27 +43,45 @@ void run_warp(const SimArgs& a, const DevTables* tb) {
     for (auto& t : lanes) t.join();
 }
 
-// Block engine (G > 32) on S emulated blocks (one cluster) of `nt` threads
-// each (nt/32 warps + a block barrier; a cluster barrier across blocks).
-void run_block(const SimArgs& a, const DevTables* tb, unsigned nt, unsigned S, bool gpu_smem, int G) {
+// Block engine (G > 32) on D device groups (MSG_EMU_GROUPS) of S emulated
+// blocks each (one cluster per group) of `nt` threads (nt/32 warps + a block
+// barrier; a cluster barrier across a group's blocks).  Each group gets its
+// own SimArgs like a separate GPU would: its own FCFS queue copy, the shared
+// job rows / summary / timeline of group 0, and the host-memory inboxes of
+// every group.
+void run_block(const SimArgs& a0, const DevTables* tb, unsigned nt, unsigned S, unsigned D, bool gpu_smem,
+               bool slots, int G) {
+    const unsigned NB = S * D;
     std::vector<std::unique_ptr<BlockScratch>> sc;
     std::vector<std::unique_ptr<wp::EmuBlock>> blocks;
     std::vector<std::vector<unsigned char>> smem;
-    wp::EmuCluster cluster;
-    cluster.S = S;
-    cluster.n = S * nt;
+    std::vector<std::unique_ptr<wp::EmuCluster>> clusters;
     std::vector<std::unique_ptr<wp::EmuWarp>> warps;
-    for (unsigned b = 0; b < S; ++b) {
+    std::vector<XInbox> inbox(D);
+    std::memset(inbox.data(), 0, sizeof(XInbox) * D);
+    std::vector<std::vector<int32_t>> queues(D, std::vector<int32_t>(std::max<uint32_t>(a0.traces[0].n_jobs, 1)));
+    std::vector<SimArgs> args(D, a0);
+    for (unsigned d = 0; d < D; ++d) {
+        args[d].n_dev = D;
+        args[d].dev0 = d;
+        args[d].vdev = 1;
+        args[d].queue = d ? queues[d].data() : a0.queue;
+        for (unsigned k = 0; k < D; ++k) args[d].inbox[k] = &inbox[k];
+        clusters.emplace_back(new wp::EmuCluster());
+        clusters.back()->S = S;
+        clusters.back()->n = S * nt;
+    }
+    for (unsigned b = 0; b < NB; ++b) {
         sc.emplace_back(new BlockScratch());
         std::memset(sc.back().get(), 0xA5, sizeof(BlockScratch));
-        cluster.base[b] = reinterpret_cast<char*>(sc.back().get());
+        clusters[b / S]->base[b % S] = reinterpret_cast<char*>(sc.back().get());
         blocks.emplace_back(new wp::EmuBlock());
         blocks.back()->n = nt;
-        smem.emplace_back(9 * (size_t)((G + S - 1) / S) + 16, 0xA5);  // stands in for dynamic smem
+        smem.emplace_back(105 * (size_t)((G + NB - 1) / NB) + 16, 0xA5);  // stands in for dynamic smem
         for (unsigned i = 0; i < nt / 32; ++i) warps.emplace_back(new wp::EmuWarp());
     }
     std::vector<std::thread> th;
-    for (unsigned b = 0; b < S; ++b)
+    for (unsigned b = 0; b < NB; ++b)
         for (unsigned t = 0; t < nt; ++t)
             th.emplace_back([&, b, t]() {
                 wp::g_block = blocks[b].get();
@@ -71,9 +89,10 @@ void run_block(const SimArgs& a, const DevTables* tb, unsigned nt, unsigned S, b
                 wp::g_lane = t % 32;
                 wp::g_tid = t;
                 wp::g_phase = 0;
-                wp::g_cluster = S > 1 ? &cluster : nullptr;
-                wp::g_crank = b;
-                simulate_large_trace<true>(a, tb, sc[b].get(), gpu_smem ? smem[b].data() : nullptr, 0);
+                wp::g_cluster = S > 1 ? clusters[b / S].get() : nullptr;
+                wp::g_crank = b % S;
+                simulate_large_trace<true>(args[b / S], tb, sc[b].get(), gpu_smem ? smem[b].data() : nullptr,
+                                           gpu_smem && slots, 0);
             });
     for (auto& x : th) x.join();
 }
@@ -167,11 +186,15 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
         const char* sh = std::getenv("MSG_EMU_SHARDS");    // thread-block cluster size (shards)
         const bool smem = !(gs && gs[0] == '0');
         const unsigned S = sh ? (unsigned)std::atoi(sh) : 1u;
-        if (S > 1) a.out_flags &= ~OF_EVENTS;  // the sharded engine runs without the event log
+        const char* gr = std::getenv("MSG_EMU_GROUPS");  // device groups
+        const unsigned D = gr ? (unsigned)std::atoi(gr) : 1u;
+        if (S > 1 || D > 1) a.out_flags &= ~OF_EVENTS;  // the sharded engine runs without the event log
         a.max_gpus = (uint32_t)G;
         a.smem_gpus = smem ? (uint32_t)G : 0u;
         if (std::getenv("MSG_EMU_DEBUG")) std::fprintf(stderr, "emu block engine: S=%u G=%d\n", S, G);
-        run_block(a, &tables, nt ? (unsigned)std::atoi(nt) : 64u, S < 1 ? 1u : S, smem, G);
+        const char* ss = std::getenv("MSG_EMU_SLOT_SMEM");  // "0": slots in global memory
+        run_block(a, &tables, nt ? (unsigned)std::atoi(nt) : 64u, S < 1 ? 1u : S, D < 1 ? 1u : D, smem,
+                  !(ss && ss[0] == '0'), G);
     } else if (G <= 4) run_warp<1>(a, &tables);
     else if (G <= 8) run_warp<2>(a, &tables);
     else if (G <= 16) run_warp<4>(a, &tables);

@@ -8,9 +8,15 @@
 // the reference before any GPU time is spent.  Never loaded by the product.
 #pragma once
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <thread>
+
+struct uint4 {
+    unsigned x, y, z, w;
+};
 
 #define MSG_DI inline
 
@@ -90,6 +96,7 @@ inline void bsync() {
 inline void sync() { barrier(); }
 inline unsigned cluster_rank() { return g_cluster ? g_crank : 0u; }
 inline unsigned cluster_size() { return g_cluster ? g_cluster->S : 1u; }
+inline unsigned cluster_id() { return 0u; }  // one cluster per emulated group
 inline void cluster_sync() {
     EmuCluster* c = g_cluster;
     if (!c) {
@@ -114,6 +121,35 @@ inline const T* cluster_map(const T* p, unsigned rank) {
     return reinterpret_cast<const T*>(g_cluster->base[rank] + (reinterpret_cast<const char*>(p) - me));
 }
 inline void gfence() { std::atomic_thread_fence(std::memory_order_seq_cst); }
+inline void gfence_sys() { std::atomic_thread_fence(std::memory_order_seq_cst); }
+inline void st_release_sys(uint64_t* p, uint64_t v) { std::atomic_ref<uint64_t>(*p).store(v, std::memory_order_release); }
+inline uint64_t ld_acquire_sys(const uint64_t* p) {
+    return std::atomic_ref<uint64_t>(*const_cast<uint64_t*>(p)).load(std::memory_order_acquire);
+}
+inline uint64_t gtime_ns() {
+    return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+[[noreturn]] inline void fail_stop() { std::abort(); }
+inline void spin_pause() { std::this_thread::yield(); }
+// Cluster record push (device: st.async + mbarrier complete_tx): copy into
+// the destination block's copy of `dst`, then count one record on its copy
+// of `bar`; xwait spins until the barrier counted `senders` records for this use.
+inline void xbar_init(uint64_t* bar) { std::atomic_ref<uint64_t>(*bar).store(0); }
+inline void xbar_arm(uint64_t*, unsigned) {}
+inline void xpush(void* dst, const uint4* src, int n16, unsigned rank, uint64_t* bar) {
+    std::memcpy(const_cast<void*>(static_cast<const void*>(cluster_map(static_cast<const char*>(dst), rank))), src,
+                16 * (size_t)n16);
+    uint64_t* rb = const_cast<uint64_t*>(cluster_map(bar, rank));
+    std::atomic_ref<uint64_t>(*rb).fetch_add(1, std::memory_order_acq_rel);
+}
+inline void xwait(uint64_t* bar, unsigned use, unsigned senders) {
+    const uint64_t want = (uint64_t)senders * (use + 1);
+    unsigned spins = 0;
+    while (std::atomic_ref<uint64_t>(*bar).load(std::memory_order_acquire) < want)
+        if (++spins > 32) std::this_thread::yield();
+}
 inline unsigned ballot(bool p) {
     const uint64_t* b = exchange(p ? 1u : 0u);
     unsigned m = 0;

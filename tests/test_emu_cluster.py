@@ -78,6 +78,7 @@ def test_sharded_block_engine(block_env, monkeypatch, shards):
     the reference (timeline to 1e-9 above 512 GPUs)."""
     block_env(force=False, threads=32, gpu_smem=shards != 3)
     monkeypatch.setenv("MSG_EMU_SHARDS", str(shards))
+    monkeypatch.setenv("MSG_EMU_SLOT_SMEM", "0" if shards == 2 else "1")  # slots in global / shared memory
     sp = preset("normal25")
     sp.mean_interarrival_s = 25.0 / 80
     sp.job_count = 500
@@ -90,3 +91,20 @@ def test_sharded_block_engine(block_env, monkeypatch, shards):
     sp2.job_count = 400
     _check(sp2, SimConfig(gpu_count=700, sched=SchedulerConfig(features=FeatureFlags(True, True, False))), [7],
            relaxed=True, no_events=True)
+
+
+@pytest.mark.parametrize("groups,shards", [(2, 1), (2, 2), (3, 2), (4, 1)])
+def test_device_groups(block_env, monkeypatch, groups, shards):
+    """The trace split over device groups (one cluster each; GPUs of a box):
+    two-level exchange — DSMEM inside a group, stamped peer-memory inboxes
+    across groups; each group keeps its own queue, job rows go to group 0."""
+    block_env(force=False, threads=32, gpu_smem=True)
+    monkeypatch.setenv("MSG_EMU_SHARDS", str(shards))
+    monkeypatch.setenv("MSG_EMU_GROUPS", str(groups))
+    sp = preset("normal25")
+    sp.mean_interarrival_s = 25.0 / 80
+    sp.job_count = 400
+    _check(sp, SimConfig(gpu_count=640), [5], relaxed=True, no_events=True)
+    churn = WorkloadSpec(mean_interarrival_s=0.005, median_s=4.0, sigma=1.2, job_count=400)
+    _check(churn, SimConfig(gpu_count=520, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                            reconfig_latency_s=0.1), [2], relaxed=True, no_events=True)
