@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--traces", type=int, default=TRACES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--c4-arrivals", type=int, default=20000)
     return ap.parse_args()
 
 
@@ -240,6 +242,72 @@ def scorer_sweep(eng, peaks, peak_kind):
             "workload": f"{B} snapshots x {G} GPUs (8 B words), one arrival each; L2 flushed"}
 
 
+def c4_line(eng, args, rank, world):
+    """C4 (BASELINE.json configs[3]): one 16384-GPU cluster, normal25 at
+    ia = 25/2048 s, seed 0 — a bounded prefix of the 1M-arrival trace.  N=1:
+    the sharded block engine (one thread-block cluster) on this GPU; N>1: the
+    trace split over all ranks' GPUs (device groups exchanging packed keys
+    over peer memory, paper_2512_16099_b200.peer), device time = max over
+    ranks.  The reference needs ~12 h for the full trace, so its
+    single-thread rate on a short prefix of the same trace is set beside it."""
+    import torch
+
+    from paper_2512_16099_b200 import abi
+    from paper_2512_16099_b200.engine import generate_batch
+    from paper_2512_16099_b200.model import SimConfig, preset
+
+    sp = preset("normal25")
+    sp.mean_interarrival_s = 25.0 / 2048
+    sp.job_count = args.c4_arrivals
+    batch = generate_batch(sp, 0, 1)
+    cfg = SimConfig(gpu_count=16384)
+    out = {"workload": f"C4 prefix: 16384-GPU cluster, first {args.c4_arrivals} of 1M arrivals (normal25, "
+                       "ia=25/2048 s, seed 0)", "unit": UNIT}
+    if world == 1:
+        st = eng.stage(batch, [cfg], 0)
+        st.launch()
+        eng.sync()
+        ms = st.time_launch()
+        res = st.collect()[0]
+        ev = int(res.summary["handler_events"])
+        out.update({"value": ev / (ms * 1e-3), "kernel_s": ms * 1e-3, "handler_events": ev, "gpus": 1,
+                    "engine": "sharded block engine, one thread-block cluster", "status": res.code})
+        try:
+            from oracle import refbind
+
+            if refbind.ref_available():
+                n = 200
+                sp.job_count = n
+                b2 = generate_batch(sp, 0, 1)
+                s, secs = refbind.ref_run_batch_summaries(b2, [cfg], threads=1)
+                g = eng.run_batch(b2, [cfg], 0)[0]
+                out["cpu_reference_prefix"] = {
+                    "arrivals": n, "value": float(s["handler_events"][0]) / secs, "cores": 1,
+                    "makespan_equal": g.workload_makespan_s == float(s["workload_makespan_s"][0])}
+        except Exception as e:  # noqa: BLE001
+            out["cpu_reference_prefix"] = f"unavailable: {e}"
+        return out
+    import torch.distributed as dist
+
+    from paper_2512_16099_b200.peer import PeerGroup, torch_allgather
+
+    group = PeerGroup(eng, world, rank, args.c4_arrivals, torch_allgather())
+    group.run(batch, cfg, 0)  # warm-up
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = group.run(batch, cfg, 0)
+    secs = time.perf_counter() - t0
+    t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    group.close()
+    if rank == 0:
+        ev = int(res[0].summary["handler_events"])
+        out.update({"value": ev / float(t.item()), "seconds": float(t.item()), "handler_events": ev, "gpus": world,
+                    "engine": f"device groups over {world} GPUs (peer-memory exchange)", "status": res[0].code})
+    return out
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -371,6 +439,13 @@ def main():
         line["scorer_sweep"] = scorer_sweep(eng, peaks, peak_kind)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(batch, cfg)
+    if not args.no_c4:
+        try:
+            c4 = c4_line(eng, args, rank, world)
+        except Exception as e:  # noqa: BLE001 (reported, the headline line still prints)
+            c4 = {"error": f"{type(e).__name__}: {e}"}
+        if rank == 0:
+            line["c4"] = c4
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

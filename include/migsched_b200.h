@@ -262,6 +262,30 @@ msg_status msg_time_launch(msg_engine* engine, msg_staged* staged, float* ms);
 /* Write a buffer larger than L2 (256 MiB) so the next launch starts cold. */
 msg_status msg_engine_flush_l2(msg_engine* engine);
 
+/* ---- multi-GPU: one large trace split over the B200s of one NVLink /
+ * NVSwitch domain, one process per GPU (configuration C4) ------
+ * Rank r owns a contiguous range of the simulated cluster's GPUs (split
+ * further over the CTAs of one thread-block cluster); every decision is a
+ * device-initiated all-reduce of packed (score, index) keys: each rank's
+ * record is stored into every peer's inbox over NVLink with a release stamp
+ * and read back with acquire loads — no host round trip, no NCCL call on
+ * the path.  Setup: msg_peer_open on every rank; exchange the
+ * msg_peer_handle_size()-byte blobs of msg_peer_export (an all-gather, e.g.
+ * over torch.distributed); msg_peer_connect with all blobs in rank order.
+ * Every rank then calls msg_run_peer with the same single-trace batch and
+ * config (more than 512 GPUs, no event log); the result is returned on rank 0
+ * only (*out stays NULL on the others).  Replaces migsched::run (sim.hpp:114)
+ * for that trace; the fragmentation timeline follows the block engine's
+ * integer-sum rule above 512 GPUs. */
+typedef struct msg_peer msg_peer;
+size_t msg_peer_handle_size(void);
+msg_status msg_peer_open(msg_engine* engine, int32_t world, int32_t rank, uint64_t max_jobs, msg_peer** out);
+msg_status msg_peer_export(msg_peer* peer, void* blob);
+msg_status msg_peer_connect(msg_peer* peer, const void* blobs);
+msg_status msg_run_peer(msg_engine* engine, msg_peer* peer, const msg_trace_batch* batch, const msg_config* cfg,
+                        uint32_t out_flags, msg_batch_result** out);
+void msg_peer_close(msg_peer* peer);
+
 /* ---- result accessors --------------------------------------------------- */
 uint32_t msg_result_n_traces(const msg_batch_result* result);
 const msg_trace_summary* msg_result_summary(const msg_batch_result* result, uint32_t trace);

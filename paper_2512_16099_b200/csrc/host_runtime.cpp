@@ -58,7 +58,8 @@ struct msg_staged {
         c_atkey, c_gw, c_gx, c_gcid;
     uint32_t large_max_g = 0;
     uint32_t large_min_g = 0;
-    const PeerBinding* peer = nullptr;  // set by msg_run_peer (host_peer.cpp) for one launch
+    const PeerBinding* peer = nullptr;  // set by msg_run_peer for one launch
+    bool no_rerun = false;              // multi-GPU run: an output overflow cannot be re-run alone
     // pinned host mirrors (rank order)
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
@@ -388,6 +389,7 @@ msg_status launch_impl(msg_engine* eng, msg_staged* s) {
         a.dev0 = pb.rank;
         a.vdev = 1;
         for (uint32_t k = 0; k < pb.world; ++k) a.inbox[k] = pb.inbox[k];
+        a.epoch = pb.epoch;
         a.jobs = static_cast<JobOut*>(pb.jobs);
         a.summary = static_cast<DevSummary*>(pb.summary);
         a.timeline = static_cast<double*>(pb.timeline);
@@ -440,7 +442,7 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
             overflow |= (s->traces[d].ev_cap && ds[d].n_events > s->traces[d].ev_cap) ||
                         (s->traces[d].tl_cap && ds[d].timeline_samples > s->traces[d].tl_cap);
         if (!overflow) break;
-        if (attempt > 6) {
+        if (attempt > 6 || s->no_rerun) {
             eng->last_error = "Unsupported: event log exceeds the output capacity";
             return MSG_ERR_UNSUPPORTED;
         }
@@ -762,5 +764,149 @@ const char* msg_result_message(const msg_batch_result* r, uint32_t t) {
 }
 
 void msg_result_free(msg_batch_result* r) { delete r; }
+
+}  // extern "C"
+
+// ---- multi-GPU device groups (one process per GPU) --------------------------
+struct msg_peer {
+    int device = 0;
+    uint32_t world = 1, rank = 0;
+    uint64_t max_jobs = 0, max_samples = 0;
+    uint32_t epoch = 0;
+    msgk::DevBuf inbox, jobs, summary, timeline;  // jobs / summary / timeline: rank 0 only
+    void* p_inbox[kMaxDev] = {};
+    void* p_jobs = nullptr;
+    void* p_summary = nullptr;
+    void* p_timeline = nullptr;
+    std::vector<void*> opened;  // IPC mappings to close
+    bool connected = false;
+};
+
+extern "C" {
+
+size_t msg_peer_handle_size(void) { return 4 * sizeof(cudaIpcMemHandle_t); }
+
+msg_status msg_peer_open(msg_engine* eng, int32_t world, int32_t rank, uint64_t max_jobs, msg_peer** out) {
+    if (!eng || !out || world < 1 || world > kMaxDev || rank < 0 || rank >= world) return MSG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    cudaSetDevice(eng->device);
+    auto p = std::make_unique<msg_peer>();
+    p->device = eng->device;
+    p->world = (uint32_t)world;
+    p->rank = (uint32_t)rank;
+    p->max_jobs = std::max<uint64_t>(max_jobs, 1);
+    p->max_samples = 8 * p->max_jobs + 64;  // collect's timeline capacity (tl_per_job = 8)
+    CK(p->inbox.ensure(sizeof(XInbox)));
+    CK(cudaMemset(p->inbox.p, 0, p->inbox.cap));
+    if (rank == 0) {
+        CK(p->jobs.ensure(p->max_jobs * sizeof(JobOut)));
+        CK(p->summary.ensure(sizeof(DevSummary)));
+        CK(p->timeline.ensure(p->max_samples * 2 * sizeof(double)));
+        p->p_jobs = p->jobs.p;
+        p->p_summary = p->summary.p;
+        p->p_timeline = p->timeline.p;
+    }
+    p->p_inbox[rank] = p->inbox.p;
+    *out = p.release();
+    return MSG_OK;
+}
+
+msg_status msg_peer_export(msg_peer* p, void* blob) {
+    if (!p || !blob) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(p->device);
+    cudaIpcMemHandle_t h[4];
+    std::memset(h, 0, sizeof(h));
+    msg_engine* eng = nullptr;  // CK needs the name; errors carry no engine message here
+    CK(cudaIpcGetMemHandle(&h[0], p->inbox.p));
+    if (p->rank == 0) {
+        CK(cudaIpcGetMemHandle(&h[1], p->jobs.p));
+        CK(cudaIpcGetMemHandle(&h[2], p->summary.p));
+        CK(cudaIpcGetMemHandle(&h[3], p->timeline.p));
+    }
+    std::memcpy(blob, h, sizeof(h));
+    return MSG_OK;
+}
+
+msg_status msg_peer_connect(msg_peer* p, const void* blobs) {
+    if (!p || !blobs) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(p->device);
+    msg_engine* eng = nullptr;
+    const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(blobs);
+    auto open = [&](const cudaIpcMemHandle_t& hd, void** ptr) -> cudaError_t {
+        cudaError_t e = cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e == cudaSuccess) p->opened.push_back(*ptr);
+        return e;
+    };
+    for (uint32_t k = 0; k < p->world; ++k)
+        if (k != p->rank) CK(open(h[4 * k], &p->p_inbox[k]));
+    if (p->rank != 0) {
+        CK(open(h[1], &p->p_jobs));
+        CK(open(h[2], &p->p_summary));
+        CK(open(h[3], &p->p_timeline));
+    }
+    p->connected = true;
+    return MSG_OK;
+}
+
+void msg_peer_close(msg_peer* p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    for (void* q : p->opened) cudaIpcCloseMemHandle(q);
+    delete p;
+}
+
+msg_status msg_run_peer(msg_engine* eng, msg_peer* p, const msg_trace_batch* batch, const msg_config* cfg,
+                        uint32_t out_flags, msg_batch_result** out) {
+    if (!eng || !p || !batch || !cfg || !p->connected) return MSG_ERR_INVALID_ARGUMENT;
+    if (out) *out = nullptr;
+    if (batch->n_traces != 1) {
+        eng->last_error = "InvalidArgument: msg_run_peer takes one trace";
+        return MSG_ERR_INVALID_ARGUMENT;
+    }
+    cudaSetDevice(eng->device);
+    if (!eng->cached) eng->cached = new msg_staged();
+    msg_staged* s = eng->cached;
+    s->ev_per_job = 16;
+    s->tl_per_job = 8;
+    msg_status st = stage_impl(eng, batch, cfg, 1, out_flags & ~(uint32_t)MSG_OUT_EVENTS, s);
+    if (st != MSG_OK) return st;
+    if (!s->traces.empty()) {  // (validation is deterministic: every rank agrees)
+        if (s->large_idx.size() != 1 || !shardable(s->large_min_g, s->out_flags)) {
+            eng->last_error = "Unsupported: multi-GPU runs need more than 512 GPUs per cluster";
+            return MSG_ERR_UNSUPPORTED;
+        }
+        if (s->n_jobs > p->max_jobs || s->tl_total > p->max_samples) {
+            eng->last_error = "Unsupported: trace larger than the peer group's capacity";
+            return MSG_ERR_UNSUPPORTED;
+        }
+        PeerBinding pb;
+        pb.world = p->world;
+        pb.rank = p->rank;
+        pb.epoch = ++p->epoch;
+        for (uint32_t k = 0; k < p->world; ++k) pb.inbox[k] = p->p_inbox[k];
+        pb.jobs = p->p_jobs;
+        pb.summary = p->p_summary;
+        pb.timeline = p->p_timeline;
+        s->peer = &pb;
+        st = launch_impl(eng, s);
+        s->peer = nullptr;
+        if (st != MSG_OK) return st;
+        CK(cudaStreamSynchronize(eng->stream));
+        if (p->rank != 0) return MSG_OK;  // results live on rank 0
+        CK(cudaMemcpyAsync(s->d_summary.p, p->p_summary, sizeof(DevSummary), cudaMemcpyDeviceToDevice, eng->stream));
+        if (s->n_jobs)
+            CK(cudaMemcpyAsync(s->d_jobs.p, p->p_jobs, s->n_jobs * sizeof(JobOut), cudaMemcpyDeviceToDevice,
+                               eng->stream));
+        if (s->tl_total)
+            CK(cudaMemcpyAsync(s->d_timeline.p, p->p_timeline, s->tl_total * 2 * sizeof(double),
+                               cudaMemcpyDeviceToDevice, eng->stream));
+    } else if (p->rank != 0) {
+        return MSG_OK;
+    }
+    s->no_rerun = true;
+    st = out ? collect_impl(eng, s, out) : MSG_OK;
+    s->no_rerun = false;
+    return st;
+}
 
 }  // extern "C"

@@ -162,7 +162,7 @@ namespace msgk {
 // Device pointers of one multi-GPU launch (host_peer.cpp): every group's
 // inbox (peer-mapped), and group 0's job rows / summary / timeline.
 struct PeerBinding {
-    uint32_t world = 1, rank = 0;
+    uint32_t world = 1, rank = 0, epoch = 0;
     void* inbox[kMaxDev] = {};
     void* jobs = nullptr;
     void* summary = nullptr;
