@@ -132,8 +132,11 @@ struct msg_batch_result {
 
 namespace {
 
+// defer_arrays: validate, lay out and allocate, copy the per-trace metadata,
+// but leave the job arrays (pinned staging + H2D) to the caller
+// (run_pipelined, chunk by chunk).
 msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
-                      uint32_t flags, msg_staged* s) {
+                      uint32_t flags, msg_staged* s, bool defer_arrays = false) {
     if (!b || (b->n_traces && (!b->offsets || !b->job_id || !b->arrival_s || !b->profile || !b->service_s)) ||
         (n_cfgs == 0 && b->n_traces)) {
         eng->last_error = "InvalidArgument: null batch arrays or no configs";
@@ -249,10 +252,10 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     uint8_t* hp = s->h_profile.as<uint8_t>();
     int64_t* hid = s->h_ids.as<int64_t>();
     uint32_t* hperm = any_perm ? s->h_perm.as<uint32_t>() : nullptr;
-    parallel_for((uint32_t)s->traces.size(), 32, [&](uint32_t d) {
-        stage_trace_arrays(b, s->src_of[d], s->traces[d], ha, hs, hp, hid, hperm);
-    });
-
+    if (!defer_arrays)
+        parallel_for((uint32_t)s->traces.size(), 32, [&](uint32_t d) {
+            stage_trace_arrays(b, s->src_of[d], s->traces[d], ha, hs, hp, hid, hperm);
+        });
     pt.mark("  stage arrays");
     // Device buffers + H2D.
     cudaStream_t st = eng->stream;
@@ -288,7 +291,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         CK(cudaMemcpyAsync(s->d_large_idx.p, s->large_idx.data(), s->large_idx.size() * 4, cudaMemcpyHostToDevice,
                            st));
     }
-    if (njobs) {
+    if (njobs && !defer_arrays) {
         CK(cudaMemcpyAsync(s->d_arrival.p, ha, njobs * sizeof(double), cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(s->d_service.p, hs, njobs * sizeof(double), cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(s->d_profile.p, hp, njobs, cudaMemcpyHostToDevice, st));
@@ -577,6 +580,166 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
     return MSG_OK;
 }
 
+
+// ---- pipelined msg_run_batch for large ensembles ---------------------------
+// Summary / job-row output over many small-cluster traces: the batch is cut
+// into kPipeChunks trace ranges, each on its own stream — host staging of
+// chunk k+1 overlaps the H2D + kernel of chunk k, and the D2H + decode of
+// the first chunks overlap the kernels of the last.  The chunk kernels run
+// concurrently (one warp per trace, latency-bound), so the wall time is
+// close to validation + one chunk's staging + the kernel + one chunk's
+// readback.
+constexpr int kPipeChunks = 4;  // == size of msg_engine::pstream
+
+void fill_summary(msg_trace_summary& o, const DevTrace& tr, const DevSummary& x) {
+    o.status = x.status;
+    o.n_jobs = tr.n_jobs;
+    o.handler_events = x.handler_events;
+    o.n_events = x.n_events;
+    o.timeline_samples = x.timeline_samples;
+    o.migration_count = x.migrations;
+    o.reconfig_op_count = x.reconfig_ops;
+    o.enqueue_count = x.enqueues;
+    o.dequeue_count = x.dequeues;
+    o.max_arrival_frag_evals = x.max_arr;
+    o.max_intra_iter_frag_evals = x.max_intra;
+    o.max_inter_iter_frag_evals = x.max_inter;
+    o.mean_wait_s = x.mean_wait;
+    o.mean_execution_s = x.mean_exec;
+    o.mean_turnaround_s = x.mean_turn;
+    o.workload_makespan_s = x.makespan;
+    o.timeline_sum = x.tl_sum;
+}
+
+msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* s, msg_batch_result** out) {
+    const uint32_t T = (uint32_t)s->traces.size();
+    const bool want_jobs = (s->out_flags & MSG_OUT_JOBS) != 0;
+    for (int k = 0; k < kPipeChunks; ++k) {
+        if (!eng->pstream[k]) CK(cudaStreamCreateWithFlags(&eng->pstream[k], cudaStreamNonBlocking));
+        if (!eng->pevent[k]) CK(cudaEventCreateWithFlags(&eng->pevent[k], cudaEventDisableTiming));
+    }
+    const size_t N = std::max<uint64_t>(s->n_jobs, 1);
+    CK(s->h_summary.ensure(std::max<uint32_t>(T, 1) * sizeof(DevSummary)));
+    if (want_jobs) CK(s->h_jobs.ensure(N * sizeof(JobOut)));
+    double* ha = s->h_arrival.as<double>();
+    double* hs = s->h_service.as<double>();
+    uint8_t* hp = s->h_profile.as<uint8_t>();
+    int64_t* hid = s->h_ids.as<int64_t>();
+    uint32_t* hperm = s->any_perm ? s->h_perm.as<uint32_t>() : nullptr;
+    SimArgs a = make_args(eng, s);
+    uint32_t d0s[kPipeChunks + 1];
+    for (int k = 0; k <= kPipeChunks; ++k) d0s[k] = (uint32_t)((uint64_t)T * k / kPipeChunks);
+    auto joff = [&](uint32_t d) { return d < T ? s->traces[d].job_off : s->n_jobs; };
+    for (int k = 0; k < kPipeChunks; ++k) {
+        const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
+        if (d0 == d1) continue;
+        cudaStream_t st = eng->pstream[k];
+        parallel_for(d1 - d0, 32, [&](uint32_t i) {
+            const uint32_t d = d0 + i;
+            stage_trace_arrays(b, s->src_of[d], s->traces[d], ha, hs, hp, hid, hperm);
+        });
+        const uint64_t j0 = joff(d0), j1 = joff(d1), nj = j1 - j0;
+        if (nj) {
+            CK(cudaMemcpyAsync(s->d_arrival.as<double>() + j0, ha + j0, nj * sizeof(double), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(s->d_service.as<double>() + j0, hs + j0, nj * sizeof(double), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(s->d_profile.as<uint8_t>() + j0, hp + j0, nj, cudaMemcpyHostToDevice, st));
+            if (hperm)
+                CK(cudaMemcpyAsync(s->d_perm.as<uint32_t>() + j0, hperm + j0, nj * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, st));
+        }
+        SimArgs c = a;
+        c.traces = s->d_traces.as<DevTrace>() + d0;
+        c.summary = s->d_summary.as<DevSummary>() + d0;
+        c.n_traces = d1 - d0;
+        cudaError_t e = launch_sim(s->spl, c, st);
+        if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim (pipelined)");
+        ++eng->launches;
+        CK(cudaMemcpyAsync(s->h_summary.as<DevSummary>() + d0, s->d_summary.as<DevSummary>() + d0,
+                           (d1 - d0) * sizeof(DevSummary), cudaMemcpyDeviceToHost, st));
+        if (want_jobs && nj)
+            CK(cudaMemcpyAsync(s->h_jobs.as<JobOut>() + j0, s->d_jobs.as<JobOut>() + j0, nj * sizeof(JobOut),
+                               cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(eng->pevent[k], st));
+    }
+    // Result layout: rows for every valid trace (JobsPending traces are
+    // squeezed out at the end, a rare path).
+    auto res = std::make_unique<msg_batch_result>();
+    res->summaries.resize(s->n_in);
+    res->messages = s->message;
+    std::memset(res->summaries.data(), 0, s->n_in * sizeof(msg_trace_summary));
+    for (uint32_t t = 0; t < s->n_in; ++t) {
+        res->summaries[t].status = s->status[t];
+        res->summaries[t].gpu_count = s->gpu_count[t];
+    }
+    if (want_jobs) {
+        res->has_jobs = true;
+        res->job_off.assign(s->n_in + 1, 0);
+        for (uint32_t t = 0; t < s->n_in; ++t) {
+            const int32_t d = s->dev_index[t];
+            res->job_off[t + 1] = res->job_off[t] + (d >= 0 ? s->traces[d].n_jobs : 0);
+        }
+        res->n_jobs_all = res->job_off[s->n_in];
+        res->jobs = take_rows(res->n_jobs_all);
+    }
+    const DevSummary* ds = s->h_summary.as<DevSummary>();
+    const JobOut* hj = s->h_jobs.as<JobOut>();
+    std::atomic<uint64_t> handler{0};
+    std::atomic<bool> pending{false};
+    for (int k = 0; k < kPipeChunks; ++k) {
+        const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
+        if (d0 == d1) continue;
+        CK(cudaEventSynchronize(eng->pevent[k]));
+        parallel_for(d1 - d0, 64, [&](uint32_t i) {
+            const uint32_t d = d0 + i, t = s->src_of[d];
+            const DevTrace& tr = s->traces[d];
+            const DevSummary& x = ds[d];
+            msg_trace_summary& o = res->summaries[t];
+            fill_summary(o, tr, x);
+            handler += x.handler_events;
+            const int64_t* ids = hid + tr.job_off;
+            if (x.status == MSG_ERR_JOBS_PENDING) {
+                const int64_t jid = x.pending_rank >= 0 ? ids[x.pending_rank] : -1;
+                res->messages[t] = "JobsPending: job " + std::to_string(jid) + " did not complete";
+                pending = true;
+                return;
+            }
+            if (!want_jobs) return;
+            msg_job_row* rows = res->jobs.p.get() + res->job_off[t];
+            for (uint32_t r = 0; r < tr.n_jobs; ++r) {
+                const JobOut& j = hj[tr.job_off + r];
+                msg_job_row& row = rows[r];
+                row.id = ids[r];
+                row.arrival_s = ha[tr.job_off + r];
+                row.scheduled_s = j.sched;
+                row.completed_s = j.done;
+                row.wait_s = row.scheduled_s - row.arrival_s;  // sim.cpp:473-475
+                row.execution_s = row.completed_s - row.scheduled_s;
+                row.turnaround_s = row.wait_s + row.execution_s;
+                row.profile = hp[tr.job_off + r];
+                row.gpu = j.gpu;
+                row.migrations = j.mig;
+                row.reserved0 = 0;
+            }
+        });
+    }
+    if (pending && want_jobs) {  // the reference throws for these traces: drop their rows
+        uint64_t w = 0;
+        std::vector<uint64_t> off(s->n_in + 1, 0);
+        for (uint32_t t = 0; t < s->n_in; ++t) {
+            const uint64_t b0 = res->job_off[t], n = res->job_off[t + 1] - b0;
+            const bool keep = res->summaries[t].status == MSG_OK;
+            if (keep && w != b0) std::memmove(res->jobs.p.get() + w, res->jobs.p.get() + b0, n * sizeof(msg_job_row));
+            w += keep ? n : 0;
+            off[t + 1] = w;
+        }
+        res->job_off = std::move(off);
+        res->n_jobs_all = w;
+    }
+    s->handler_events = handler.load();
+    *out = res.release();
+    return MSG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -626,6 +789,13 @@ void msg_engine_destroy(msg_engine* e) {
     if (e->stream) cudaStreamSynchronize(e->stream);
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
+    for (int k = 0; k < 4; ++k) {
+        if (e->pstream[k]) {
+            cudaStreamSynchronize(e->pstream[k]);
+            cudaStreamDestroy(e->pstream[k]);
+        }
+        if (e->pevent[k]) cudaEventDestroy(e->pevent[k]);
+    }
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
 }
@@ -677,9 +847,22 @@ msg_status msg_run_batch(msg_engine* eng, const msg_trace_batch* batch, const ms
     s->ev_per_job = 16;
     s->tl_per_job = 8;
     PhaseTimer pt;
-    msg_status st = stage_impl(eng, batch, cfgs, n_cfgs, out_flags, s);
-    pt.mark("stage (validate+H2D)");
+    // Large ensembles of small clusters with summary / job-row output run
+    // pipelined (run_pipelined); anything else through stage / launch / collect.
+    const bool pipe = batch && batch->n_traces >= 512 && (out_flags & ~(uint32_t)MSG_OUT_JOBS) == 0 &&
+                      std::getenv("MSG_NO_PIPELINE") == nullptr;
+    msg_status st = stage_impl(eng, batch, cfgs, n_cfgs, out_flags, s, pipe);
     if (st != MSG_OK) return st;
+    if (pipe) {
+        if (s->large_idx.empty()) {
+            st = run_pipelined(eng, batch, s, out);
+            pt.mark("pipelined run");
+            return st;
+        }
+        st = stage_impl(eng, batch, cfgs, n_cfgs, out_flags, s, false);  // large clusters: the plain path
+        if (st != MSG_OK) return st;
+    }
+    pt.mark("stage (validate+H2D)");
     st = launch_impl(eng, s);
     if (st != MSG_OK) return st;
     if (pt.on) {

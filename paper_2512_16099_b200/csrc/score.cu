@@ -42,7 +42,10 @@
 
 namespace msgk {
 
-constexpr int kScoreThreads = 256;
+#ifndef MSG_SCORE_THREADS
+#define MSG_SCORE_THREADS 256
+#endif
+constexpr int kScoreThreads = MSG_SCORE_THREADS;
 #ifndef MSG_SCORE_WPT
 #define MSG_SCORE_WPT 4
 #endif
@@ -537,43 +540,92 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
 // Lazy candidate are scored again over all words with the full key (Busy
 // GPUs compete; their candidates are counted), exactly as the register path.
 template <bool DYN>
+__device__ __forceinline__ void busy_item(const ScoreArgs& a, const ScoreSmem& sm, uint32_t snap, uint32_t first,
+                                          uint32_t end) {
+    ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
+    const unsigned prof = a.profile[snap];
+    for (uint32_t c = first; c < end; ++c) {
+        const ChunkData d = load_chunk(a, snap, (uint64_t)c * kChunk);
+        const unsigned base = (c - first) * kChunk;
+        acc.anyx = 0;
+        switch (prof) {
+            case 0: score_chunk<0, true, DYN, false>(sm, d, base, acc); break;
+            case 1: score_chunk<1, true, DYN, false>(sm, d, base, acc); break;
+            case 2: score_chunk<2, true, DYN, false>(sm, d, base, acc); break;
+            case 3: score_chunk<3, true, DYN, false>(sm, d, base, acc); break;
+            case 4: score_chunk<4, true, DYN, false>(sm, d, base, acc); break;
+            default: score_chunk<5, true, DYN, false>(sm, d, base, acc); break;
+        }
+        if (DYN && __any_sync(0xffffffffu, acc.anyx != 0)) {
+            switch (prof) {
+                case 0: score_chunk<0, true, DYN, true>(sm, d, base, acc); break;
+                case 1: score_chunk<1, true, DYN, true>(sm, d, base, acc); break;
+                case 2: score_chunk<2, true, DYN, true>(sm, d, base, acc); break;
+                case 3: score_chunk<3, true, DYN, true>(sm, d, base, acc); break;
+                case 4: score_chunk<4, true, DYN, true>(sm, d, base, acc); break;
+                default: score_chunk<5, true, DYN, true>(sm, d, base, acc); break;
+            }
+        }
+    }
+    flush_item<true>(a, acc, snap, first);
+}
+
+// Pass 2 (after score_tma_kernel<true, DYN>): snapshots whose pass 1 found no
+// Lazy candidate are scored again over all words with the full key (Busy
+// GPUs compete; their candidates are counted), exactly as the register path.
+// Every block first collects those snapshots from the pass-1 counts with one
+// coalesced sweep (usually none: the kernel then ends after reading 16 B per
+// snapshot), then walks their items grid-stride.
+constexpr int kBusyList = 4096;
+
+template <bool DYN>
 __global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem sm;
+    __shared__ uint32_t list[kBusyList];
+    __shared__ uint32_t wsum[kScoreThreads / 32];
+    __shared__ uint32_t cnt;
+    // Ordered compaction: thread t owns a contiguous run of snapshots, loads
+    // all their pass-1 counts at once, and one block-wide exclusive scan of
+    // the per-thread totals places the entries — every block builds the
+    // same list, with no barrier per snapshot.
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t per = (a.n + blockDim.x - 1) / blockDim.x, s0 = threadIdx.x * per;
+    uint32_t mine = 0;
+    for (uint32_t i = 0; i < per && s0 + i < a.n; ++i) mine += (a.out[2 * (s0 + i) + 1] >> 32) == 0;
+    uint32_t incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t off = incl - mine;
+    for (unsigned w = 0; w < warp; ++w) off += wsum[w];
+    if (threadIdx.x == blockDim.x - 1) cnt = off + mine;
+    for (uint32_t i = 0; i < per && s0 + i < a.n && mine; ++i)
+        if ((a.out[2 * (s0 + i) + 1] >> 32) == 0) {
+            if (off < (uint32_t)kBusyList) list[off] = s0 + i;
+            ++off;
+        }
+    __syncthreads();
+    const uint32_t need = cnt;
+    if (need == 0) return;
     score_smem_init(sm, a.tables, a.lazymask);
     __syncthreads();
     const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
     const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
-    const uint32_t n_items = items_per * a.n;
-    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const uint32_t snap = item / items_per;
-        if ((a.out[2 * snap + 1] >> 32) != 0) continue;  // pass 1 found Lazy candidates
-        const uint32_t first = (item - snap * items_per) * kItemChunks, end = min(first + kItemChunks, chunks_per);
-        ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
-        const unsigned prof = a.profile[snap];
-        for (uint32_t c = first; c < end; ++c) {
-            const ChunkData d = load_chunk(a, snap, (uint64_t)c * kChunk);
-            const unsigned base = (c - first) * kChunk;
-            acc.anyx = 0;
-            switch (prof) {
-                case 0: score_chunk<0, true, DYN, false>(sm, d, base, acc); break;
-                case 1: score_chunk<1, true, DYN, false>(sm, d, base, acc); break;
-                case 2: score_chunk<2, true, DYN, false>(sm, d, base, acc); break;
-                case 3: score_chunk<3, true, DYN, false>(sm, d, base, acc); break;
-                case 4: score_chunk<4, true, DYN, false>(sm, d, base, acc); break;
-                default: score_chunk<5, true, DYN, false>(sm, d, base, acc); break;
-            }
-            if (DYN && __any_sync(0xffffffffu, acc.anyx != 0)) {
-                switch (prof) {
-                    case 0: score_chunk<0, true, DYN, true>(sm, d, base, acc); break;
-                    case 1: score_chunk<1, true, DYN, true>(sm, d, base, acc); break;
-                    case 2: score_chunk<2, true, DYN, true>(sm, d, base, acc); break;
-                    case 3: score_chunk<3, true, DYN, true>(sm, d, base, acc); break;
-                    case 4: score_chunk<4, true, DYN, true>(sm, d, base, acc); break;
-                    default: score_chunk<5, true, DYN, true>(sm, d, base, acc); break;
-                }
-            }
+    if (need <= (uint32_t)kBusyList) {
+        for (uint32_t v = blockIdx.x; v < need * items_per; v += gridDim.x) {
+            const uint32_t j = v / items_per, first = (v - j * items_per) * kItemChunks;
+            busy_item<DYN>(a, sm, list[j], first, min(first + kItemChunks, chunks_per));
         }
-        flush_item<true>(a, acc, snap, first);
+        return;
+    }
+    for (uint32_t item = blockIdx.x; item < items_per * a.n; item += gridDim.x) {  // too many: flag per item
+        const uint32_t snap = item / items_per;
+        if ((a.out[2 * snap + 1] >> 32) != 0) continue;
+        const uint32_t first = (item - snap * items_per) * kItemChunks;
+        busy_item<DYN>(a, sm, snap, first, min(first + kItemChunks, chunks_per));
     }
 }
 

@@ -175,3 +175,39 @@ def test_full_size_aggregates_vs_reference_goldens(engine, name):
     for key, field in (("checksum_turnaround", "mean_turnaround_s"), ("checksum_makespan", "workload_makespan_s"),
                        ("checksum_timeline", "timeline_sum")):
         assert int(np.ascontiguousarray(s[field]).view(np.uint64).sum(dtype=np.uint64)) == entry[key], key
+
+
+def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
+    """msg_run_batch on >= 512 traces with job-row output runs pipelined
+    (four trace chunks on four streams); valid, invalid and JobsPending
+    traces mixed in one batch give the reference's per-trace results and the
+    same bytes as the unpipelined stage / launch / collect path."""
+    from paper_2512_16099_b200.engine import generate_batch
+
+    good = generate_batch(preset("normal25"), 0, 600)
+    traces = []
+    for t in range(good.n_traces):
+        lo, hi = int(good.offsets[t]), int(good.offsets[t + 1])
+        traces.append([Job(int(good.job_id[i]), float(good.arrival_s[i]), int(good.profile[i]),
+                           float(good.service_s[i])) for i in range(lo, hi)])
+    traces[5] = [Job(0, 10.0, 5, 1.0), Job(1, 5.0, 5, 1.0)]  # TraceUnsorted
+    traces[300] = [Job(0, 0.0, 0, 10.0)]  # 1g.5gb on a static 2g-only layout, no repartitioning: JobsPending
+    traces[599] = []
+    cfgs = [SimConfig(gpu_count=8),
+            SimConfig(gpu_count=1, sched=SchedulerConfig(features=FeatureFlags(True, False, True),
+                                                         static_layout=[[(2, 0), (2, 4)]]))]
+    b = TraceBatch.from_traces(traces, config_index=[1 if t == 300 else 0 for t in range(len(traces))])
+    ref = rb.ref_run_batch_results(b, cfgs)
+    piped = engine.run_batch(b, cfgs, abi.OUT_JOBS)
+    monkeypatch.setenv("MSG_NO_PIPELINE", "1")
+    plain = engine.run_batch(b, cfgs, abi.OUT_JOBS)
+    assert piped.summaries.tobytes() == plain.summaries.tobytes()
+    assert piped.jobs.tobytes() == plain.jobs.tobytes()
+    assert np.array_equal(piped.job_offsets, plain.job_offsets)
+    assert piped[300].code == "JobsPending" and piped[5].code == "TraceUnsorted"
+    bad = []
+    for t, (r, g) in enumerate(zip(ref, piped)):
+        r.events = r.frag_timeline = None
+        if d := diff_results(r, g):
+            bad.append((t, d))
+    assert not bad, bad[:3]
