@@ -301,6 +301,24 @@ const msg_trace_summary* msg_result_summaries(const msg_batch_result* result);
 const msg_job_row* msg_result_all_jobs(const msg_batch_result* result, const uint64_t** offsets, uint64_t* n);
 void msg_result_free(msg_batch_result* result);
 
+/* ---- trace ingest: migsched::load_trace (workload.hpp:53,
+ * workload.cpp:151-199).  Reads a JSONL trace file (one {"schema":1,
+ * "job_id", "arrival_s", "profile", "service_s"} object per line; blank lines
+ * skipped) in parallel, with the reference's validation and messages
+ * ("line N: not valid JSON" / "expected an object" / "unsupported schema
+ * version" / "missing or mistyped field" / "times must be non-negative" as
+ * ParseError, unknown profile names as UnknownProfile; the first failing
+ * line wins) and returns the jobs stable-sorted by arrival, ready for a
+ * msg_trace_batch.  `msg` (optional) receives "<Code>: <message>". */
+typedef struct msg_trace_file msg_trace_file;
+msg_status msg_trace_load(const char* path, msg_trace_file** out, char* msg, size_t msg_len);
+uint64_t msg_trace_file_jobs(const msg_trace_file* file);
+const int64_t* msg_trace_file_ids(const msg_trace_file* file);
+const double* msg_trace_file_arrival(const msg_trace_file* file);
+const int32_t* msg_trace_file_profile(const msg_trace_file* file);
+const double* msg_trace_file_service(const msg_trace_file* file);
+void msg_trace_file_free(msg_trace_file* file);
+
 /* ---- workload generation: migsched::generate (workload.hpp:45,
  * workload.cpp:98-127) with the same mt19937_64 inverse-transform sampler, so
  * a seed gives the same trace as the reference.  Host-side (trace staging). */

@@ -498,4 +498,52 @@ int64_t ref_enumerate_states(int depth, int32_t* out, int64_t cap) {
     return n;
 }
 
+// ---- trace files: migsched::load_trace / save_trace (workload.cpp:151-213)
+struct RefTrace {
+    std::vector<Job> jobs;
+    std::string code, message;
+};
+void* ref_load_trace(const char* path) {
+    auto* t = new RefTrace();
+    try {
+        t->jobs = load_trace(path);
+    } catch (const Error& e) {
+        t->code = e.code();
+        t->message = e.what();
+    } catch (const std::exception& e) {  // e.g. nlohmann type_error escaping load_trace
+        t->code = "Exception";
+        t->message = e.what();
+    }
+    return t;
+}
+const char* ref_trace_code(void* h) { return static_cast<RefTrace*>(h)->code.c_str(); }
+const char* ref_trace_message(void* h) { return static_cast<RefTrace*>(h)->message.c_str(); }
+int64_t ref_trace_jobs(void* h) { return (int64_t) static_cast<RefTrace*>(h)->jobs.size(); }
+void ref_trace_get(void* h, int64_t* id, double* arrival, int32_t* profile, double* service) {
+    const auto& j = static_cast<RefTrace*>(h)->jobs;
+    for (size_t i = 0; i < j.size(); ++i) {
+        id[i] = j[i].id;
+        arrival[i] = j[i].arrival_s;
+        profile[i] = (int32_t)j[i].profile;
+        service[i] = j[i].service_s;
+    }
+}
+void ref_trace_free(void* h) { delete static_cast<RefTrace*>(h); }
+int ref_save_trace(const char* path, int64_t n, const int64_t* id, const double* arrival, const int32_t* profile,
+                   const double* service) {
+    std::vector<Job> jobs((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        jobs[(size_t)i].id = id[i];
+        jobs[(size_t)i].arrival_s = arrival[i];
+        jobs[(size_t)i].profile = static_cast<ProfileId>(profile[i]);
+        jobs[(size_t)i].service_s = service[i];
+    }
+    try {
+        save_trace(jobs, path);
+    } catch (const std::exception&) {
+        return 1;
+    }
+    return 0;
+}
+
 }  // extern "C"

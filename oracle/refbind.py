@@ -72,6 +72,17 @@ def ref_lib():
         lib.ref_oracle_run_all.restype = C.c_int
         lib.ref_enumerate_states.restype = C.c_int64
         lib.ref_enumerate_states.argtypes = [C.c_int, C.c_void_p, C.c_int64]
+        lib.ref_load_trace.restype = C.c_void_p
+        lib.ref_load_trace.argtypes = [C.c_char_p]
+        for n in ("ref_trace_code", "ref_trace_message"):
+            getattr(lib, n).restype = C.c_char_p
+            getattr(lib, n).argtypes = [C.c_void_p]
+        lib.ref_trace_jobs.restype = C.c_int64
+        lib.ref_trace_jobs.argtypes = [C.c_void_p]
+        lib.ref_trace_get.argtypes = [C.c_void_p] * 5
+        lib.ref_trace_free.argtypes = [C.c_void_p]
+        lib.ref_save_trace.restype = C.c_int
+        lib.ref_save_trace.argtypes = [C.c_char_p, C.c_int64] + [C.c_void_p] * 4
         _ref = lib
     return _ref
 
@@ -262,3 +273,38 @@ def ref_try_dequeue(slots: np.ndarray, queue, threshold=0.4, lb=True, dyn=True):
     st = lib.ref_try_dequeue(len(slots) // 8, slots.ctypes.data, len(queue), qj.ctypes.data, qp.ctypes.data,
                              C.byref(cfg), placed.ctypes.data, n.ctypes.data)
     return st, [dict(zip(dt.names, (x.item() for x in r))) for r in placed[: int(n[0])]], slots
+
+
+def ref_load_trace(path: str):
+    """migsched::load_trace -> (code, message, ids, arrival, profile, service);
+    code '' on success."""
+    import os
+
+    lib = ref_lib()
+    h = lib.ref_load_trace(os.fsencode(path))
+    try:
+        code = lib.ref_trace_code(h).decode()
+        msg = lib.ref_trace_message(h).decode(errors="replace")
+        n = int(lib.ref_trace_jobs(h))
+        ids = np.zeros(n, np.int64)
+        arr = np.zeros(n, np.float64)
+        prof = np.zeros(n, np.int32)
+        svc = np.zeros(n, np.float64)
+        if n:
+            lib.ref_trace_get(h, ids.ctypes.data, arr.ctypes.data, prof.ctypes.data, svc.ctypes.data)
+    finally:
+        lib.ref_trace_free(h)
+    return code, msg, ids, arr, prof, svc
+
+
+def ref_save_trace(path: str, ids, arrival, profile, service) -> None:
+    """migsched::save_trace (workload.cpp:201-213)."""
+    import os
+
+    ids = np.ascontiguousarray(ids, np.int64)
+    arrival = np.ascontiguousarray(arrival, np.float64)
+    profile = np.ascontiguousarray(profile, np.int32)
+    service = np.ascontiguousarray(service, np.float64)
+    if ref_lib().ref_save_trace(os.fsencode(path), len(ids), ids.ctypes.data, arrival.ctypes.data,
+                                profile.ctypes.data, service.ctypes.data):
+        raise RuntimeError("save_trace failed")

@@ -47,7 +47,7 @@ namespace msgk {
 #endif
 constexpr int kScoreThreads = MSG_SCORE_THREADS;
 #ifndef MSG_SCORE_WPT
-#define MSG_SCORE_WPT 4
+#define MSG_SCORE_WPT 8
 #endif
 #ifndef MSG_SCORE_MINB
 #define MSG_SCORE_MINB 4
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_kernel(Sc
 // __syncthreads.  Per-stage metadata (snapshot, item base, valid words,
 // profile, item end) travels with the copy.
 #ifndef MSG_SCORE_STAGES
-#define MSG_SCORE_STAGES 4
+#define MSG_SCORE_STAGES 2
 #endif
 constexpr int kStages = MSG_SCORE_STAGES;
 

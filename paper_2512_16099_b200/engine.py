@@ -61,6 +61,13 @@ def lib():
         "msg_workload_preset": (C.c_int, [C.c_char_p, vp]),
         "msg_generate": (C.c_int, [vp, vp, vp, vp, vp]),
         "msg_generate_many": (C.c_int, [vp, u64, u32, i32, vp, vp, vp, vp, vp]),
+        "msg_trace_load": (C.c_int, [C.c_char_p, C.POINTER(vp), C.c_char_p, C.c_size_t]),
+        "msg_trace_file_jobs": (u64, [vp]),
+        "msg_trace_file_ids": (vp, [vp]),
+        "msg_trace_file_arrival": (vp, [vp]),
+        "msg_trace_file_profile": (vp, [vp]),
+        "msg_trace_file_service": (vp, [vp]),
+        "msg_trace_file_free": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -290,6 +297,33 @@ def generate(spec: WorkloadSpec):
     s = spec.to_abi()
     _check(lib().msg_generate(C.byref(s), ids.ctypes.data, arr.ctypes.data, prof.ctypes.data, svc.ctypes.data))
     return [Job(int(ids[i]), float(arr[i]), int(prof[i]), float(svc[i])) for i in range(n)]
+
+
+def load_trace(path: str) -> TraceBatch:
+    """migsched::load_trace (workload.cpp:151-199): a JSONL trace file as a
+    one-trace TraceBatch (jobs stable-sorted by arrival).  Raises
+    MigschedError with the reference's code (ParseError, UnknownProfile) and
+    message on a bad file."""
+    L = lib()
+    h = C.c_void_p()
+    msg = C.create_string_buffer(512)
+    st = L.msg_trace_load(os.fsencode(path), C.byref(h), msg, len(msg))
+    if st != 0:
+        text = msg.value.decode(errors="replace")
+        raise MigschedError(abi.STATUS_NAMES.get(st, str(st)), text.split(": ", 1)[-1])
+    try:
+        n = int(L.msg_trace_file_jobs(h))
+
+        def arr(ptr, dt):
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(dt)), shape=(n,)).copy() if n else np.zeros(0, dt)
+
+        ids = arr(L.msg_trace_file_ids(h), C.c_int64)
+        a = arr(L.msg_trace_file_arrival(h), C.c_double)
+        p = arr(L.msg_trace_file_profile(h), C.c_int32)
+        s = arr(L.msg_trace_file_service(h), C.c_double)
+    finally:
+        L.msg_trace_file_free(h)
+    return TraceBatch(np.array([0, n], np.uint64), ids, a, p, s)
 
 
 def generate_batch(spec: WorkloadSpec, seed0: int, n_seeds: int, threads: int = 0) -> TraceBatch:
