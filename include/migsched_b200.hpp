@@ -275,4 +275,26 @@ inline SimResult run(const std::vector<Job>& trace, const SimConfig& cfg) {
     return engine.run(trace, cfg);
 }
 
+// Drop-in for migsched::load_trace(path) (workload.hpp:53): the native
+// parallel JSONL reader, same validation, codes and messages; jobs
+// stable-sorted by arrival.
+inline std::vector<Job> load_trace(const std::string& path) {
+    msg_trace_file* f = nullptr;
+    char msg[512];
+    const msg_status st = msg_trace_load(path.c_str(), &f, msg, sizeof msg);
+    if (st != MSG_OK) {
+        const std::string m(msg), code = msg_status_name(st);
+        throw Error(code, m.size() > code.size() + 2 ? m.substr(code.size() + 2) : m);
+    }
+    const uint64_t n = msg_trace_file_jobs(f);
+    std::vector<Job> jobs(n);
+    const int64_t* id = msg_trace_file_ids(f);
+    const double* a = msg_trace_file_arrival(f);
+    const int32_t* p = msg_trace_file_profile(f);
+    const double* sv = msg_trace_file_service(f);
+    for (uint64_t i = 0; i < n; ++i) jobs[i] = Job{id[i], a[i], static_cast<ProfileId>(p[i]), sv[i]};
+    msg_trace_file_free(f);
+    return jobs;
+}
+
 }  // namespace migsched_b200

@@ -81,6 +81,9 @@ struct BlockScratch {
     unsigned long long ksum;  // this shard's sum of per-GPU 4-mask cost numerators
     double tl;
     XRec xin[2][kMaxShards];  // records pushed by every shard, by round parity
+    XInbox* ib[kMaxDev];      // every device group's inbox for this trace
+    double pend_t[2];         // deferred timeline samples: time, this shard's cost total
+    unsigned long long pend_k[2];
     XRec xr;                  // reduced record (within the cluster)
     XRec xr2;                 // reduced record (across device groups)
     uint64_t xbar[2];         // mbarriers counting the pushed bytes, by round parity
@@ -123,7 +126,6 @@ struct ClusterSim {
     // one dv); global shard gs = dv * S + sh of NS = D * S
     unsigned S, sh, D, dv, gs, NS, epoch;
     int g_lo, g_hi;
-    XInbox* ib[kMaxDev];
     // block-uniform state (every thread holds the same values)
     unsigned T, W, L, w, NT;  // thread, warp, lane, warps, threads
     int bph;                  // scratch double-buffer parity
@@ -140,8 +142,6 @@ struct ClusterSim {
     bool tl_dirty;
     // deferred timeline samples (sharded)
     uint32_t npend;
-    double pend_t[2];
-    unsigned long long pend_k[2];
 
     // ------------------------------------------------------------- tables
     MSG_DI unsigned rank2(unsigned bc, unsigned bm) const { return tb->cost2rank[wp::popc(bc) * 256 + bm]; }
@@ -248,8 +248,8 @@ struct ClusterSim {
     // returns the same reduced record.  Deferred timeline samples ride along.
     MSG_DI void exchange(XRec& r) {
         if (NS == 1) return;
-        r.ks[0] = npend > 0 ? pend_k[0] : 0ull;
-        r.ks[1] = npend > 1 ? pend_k[1] : 0ull;
+        r.ks[0] = npend > 0 ? sc->pend_k[0] : 0ull;
+        r.ks[1] = npend > 1 ? sc->pend_k[1] : 0ull;
         const unsigned par = xround & 1u, use = xround >> 1;
         if (S > 1) {  // level 1: the CTAs of this cluster, over distributed shared memory
             if (W == 0) {
@@ -269,7 +269,7 @@ struct ClusterSim {
             if (W == 0) {
                 const uint64_t stamp = ((uint64_t)epoch << 32) | (xround + 1u);
                 if (L < D) {  // push the group's record to group L, then its stamp (release)
-                    XInbox* dst = ib[L];
+                    XInbox* dst = sc->ib[L];
                     uint4* q = reinterpret_cast<uint4*>(&dst->rec[par][sh][dv]);
                     const uint4* src = reinterpret_cast<const uint4*>(&r);
                     for (int i = 0; i < (int)(sizeof(XRec) / 16); ++i) q[i] = src[i];
@@ -277,7 +277,7 @@ struct ClusterSim {
                 }
                 XRec x = xnone();
                 if (L < D) {
-                    XInbox* me = ib[dv];
+                    XInbox* me = sc->ib[dv];
                     const uint64_t t0 = wp::gtime_ns();
                     unsigned spins = 0;
                     while (wp::ld_acquire_sys(&me->stamp[par][sh][L]) != stamp) {
@@ -294,7 +294,7 @@ struct ClusterSim {
         }
         ++xround;
         // deferred timeline samples, in order
-        for (uint32_t i = 0; i < npend; ++i) record_sample(pend_t[i], r.ks[i]);
+        for (uint32_t i = 0; i < npend; ++i) record_sample(sc->pend_t[i], r.ks[i]);
         npend = 0;
     }
 
@@ -344,7 +344,7 @@ struct ClusterSim {
         NS = D * S;
         epoch = a.epoch;
         // inbox of group k for this trace: a.inbox[k] holds one XInbox per large trace
-        for (unsigned k = 0; k < D; ++k) ib[k] = reinterpret_cast<XInbox*>(a.inbox[k]) + wp::cluster_id() / vd;
+        if (T < D) sc->ib[T] = reinterpret_cast<XInbox*>(a.inbox[T]) + wp::cluster_id() / vd;
         xround = 0;
         npend = 0;
         const DevTrace tr = a.traces[t];
@@ -567,8 +567,10 @@ struct ClusterSim {
     MSG_DI void sample() {  // sim.cpp:177-181
         if (NS > 1) {  // deferred: the next exchange sums the shards' parts
             wp::bsync();
-            pend_t[npend] = now;
-            pend_k[npend] = sc->ksum;
+            if (T == 0) {
+                sc->pend_t[npend] = now;
+                sc->pend_k[npend] = sc->ksum;
+            }
             ++npend;
             wp::bsync();
             return;

@@ -14,6 +14,9 @@ struct ScoreArgs {
     uint64_t G;
     uint32_t n;
     uint32_t lb, dyn, lazymask;
+    // scratch (n + 1 + n words; the first n unused): the count and list of
+    // snapshots pass 1 left without a Lazy candidate (score_list_kernel)
+    uint32_t* scratch;
 };
 
 cudaError_t launch_snapshot(const SnapArgs& a, cudaStream_t stream);

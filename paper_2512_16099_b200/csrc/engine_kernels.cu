@@ -56,11 +56,20 @@ static cudaError_t launch_sim_t(const SimArgs& a, cudaStream_t stream) {
 
 // Block engine for clusters of more than 32 GPUs: one thread-block cluster
 // of a.shards CTAs per trace (a.shards = 1: one block), each CTA one shard
-// of the trace's GPUs (cluster_core.cuh).
-constexpr int kClusterThreads = 512;
+// of the trace's GPUs (cluster_core.cuh).  NT threads per CTA: 512 when a
+// CTA owns thousands of GPUs (S <= 8), 128 at 16 shards, where the
+// per-event chain of block barriers and exchanges dominates the (then
+// small) per-shard scans: C4 at S = 16 runs 1.7x faster with 128 threads
+// than with 512 (profiles/r01).
+#ifndef MSG_CLUSTER_THREADS_WIDE
+#define MSG_CLUSTER_THREADS_WIDE 512
+#endif
+#ifndef MSG_CLUSTER_THREADS_NARROW
+#define MSG_CLUSTER_THREADS_NARROW 128
+#endif
 
-template <bool DETAIL>
-__global__ void __launch_bounds__(kClusterThreads, 1) cluster_kernel(SimArgs a) {
+template <bool DETAIL, int NT>
+__global__ void __launch_bounds__(NT, 1) cluster_kernel(SimArgs a) {
     __shared__ __align__(16) DevTables tb;
     __shared__ BlockScratch sc;
     extern __shared__ __align__(16) unsigned char gpu_smem[];  // 9 B per owned GPU when they fit
@@ -81,7 +90,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) cluster_kernel(SimArgs a) 
 // slots: 96 B more per GPU).
 static size_t gpu_smem_bytes(uint32_t G, bool slots) { return ((size_t)G * (slots ? 105 : 9) + 15) & ~(size_t)15; }
 
-template <bool DETAIL>
+template <bool DETAIL, int NT>
 static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
     static int optin = -1;
     static size_t static_smem = 0;
@@ -90,9 +99,9 @@ static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
         cudaError_t e = cudaGetDevice(&dev);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         cudaFuncAttributes fa;
-        if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, cluster_kernel<DETAIL>);
+        if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, cluster_kernel<DETAIL, NT>);
         if (e == cudaSuccess && kMaxShards > 8)
-            e = cudaFuncSetAttribute(cluster_kernel<DETAIL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            e = cudaFuncSetAttribute(cluster_kernel<DETAIL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         static_smem = fa.sharedSizeBytes;
     }
@@ -112,17 +121,18 @@ static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
         dyn = gpu_smem_bytes(per, false);
     }
     if (dyn > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(cluster_kernel<DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaError_t e =
+            cudaFuncSetAttribute(cluster_kernel<DETAIL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         if (e != cudaSuccess) return e;
     }
     const uint32_t groups = a.n_large * (a.vdev < 1 ? 1u : a.vdev);  // clusters in this launch
     if (S == 1 && groups == a.n_large) {
-        cluster_kernel<DETAIL><<<a.n_large, kClusterThreads, dyn, stream>>>(a);
+        cluster_kernel<DETAIL, NT><<<a.n_large, NT, dyn, stream>>>(a);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(groups * S);
-    cfg.blockDim = dim3(kClusterThreads);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = dyn;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -135,17 +145,20 @@ static cudaError_t launch_cluster_t(SimArgs a, cudaStream_t stream) {
     if (groups > a.n_large) {
         // device groups on one GPU spin on each other: all must be co-resident
         int max_clusters = 0;
-        cudaError_t e = cudaOccupancyMaxActiveClusters(&max_clusters, cluster_kernel<DETAIL>, &cfg);
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&max_clusters, cluster_kernel<DETAIL, NT>, &cfg);
         if (e != cudaSuccess) return e;
         if ((uint32_t)max_clusters < groups) return cudaErrorCooperativeLaunchTooLarge;
     }
-    return cudaLaunchKernelEx(&cfg, cluster_kernel<DETAIL>, a);
+    return cudaLaunchKernelEx(&cfg, cluster_kernel<DETAIL, NT>, a);
 }
 
 cudaError_t launch_cluster(const SimArgs& a, cudaStream_t stream) {
     if (!a.n_large) return cudaSuccess;
     const bool detail = (a.out_flags & (OF_EVENTS | OF_TIMELINE)) != 0;
-    return detail ? launch_cluster_t<true>(a, stream) : launch_cluster_t<false>(a, stream);
+    constexpr int W = MSG_CLUSTER_THREADS_WIDE, N = MSG_CLUSTER_THREADS_NARROW;
+    if (a.shards >= 16)
+        return detail ? launch_cluster_t<true, N>(a, stream) : launch_cluster_t<false, N>(a, stream);
+    return detail ? launch_cluster_t<true, W>(a, stream) : launch_cluster_t<false, W>(a, stream);
 }
 
 cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream) {

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -135,6 +136,22 @@ namespace {
 // defer_arrays: validate, lay out and allocate, copy the per-trace metadata,
 // but leave the job arrays (pinned staging + H2D) to the caller
 // (run_pipelined, chunk by chunk).
+// One per-job row (sim.cpp:467-500 JobRecord fields).
+inline void put_row(msg_job_row* dst, int64_t id, double arrival, const JobOut& j, int32_t profile) {
+    msg_job_row& row = *dst;
+    row.id = id;
+    row.arrival_s = arrival;
+    row.scheduled_s = j.sched;
+    row.completed_s = j.done;
+    row.wait_s = row.scheduled_s - row.arrival_s;  // sim.cpp:473-475
+    row.execution_s = row.completed_s - row.scheduled_s;
+    row.turnaround_s = row.wait_s + row.execution_s;
+    row.profile = profile;
+    row.gpu = j.gpu;
+    row.migrations = j.mig;
+    row.reserved0 = 0;
+}
+
 msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
                       uint32_t flags, msg_staged* s, bool defer_arrays = false) {
     if (!b || (b->n_traces && (!b->offsets || !b->job_id || !b->arrival_s || !b->profile || !b->service_s)) ||
@@ -545,21 +562,8 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
         }
         if (want_jobs) {
             msg_job_row* rows = res->jobs.p.get() + res->job_off[t];
-            for (uint32_t r = 0; r < tr.n_jobs; ++r) {
-                const JobOut& j = hj[tr.job_off + r];
-                msg_job_row& row = rows[r];
-                std::memset(&row, 0, sizeof(row));
-                row.id = ids[r];
-                row.arrival_s = ha[tr.job_off + r];
-                row.scheduled_s = j.sched;
-                row.completed_s = j.done;
-                row.wait_s = row.scheduled_s - row.arrival_s;          // sim.cpp:473-475
-                row.execution_s = row.completed_s - row.scheduled_s;
-                row.turnaround_s = row.wait_s + row.execution_s;
-                row.profile = hp[tr.job_off + r];
-                row.gpu = j.gpu;
-                row.migrations = j.mig;
-            }
+            for (uint32_t r = 0; r < tr.n_jobs; ++r)
+                put_row(rows + r, ids[r], ha[tr.job_off + r], hj[tr.job_off + r], hp[tr.job_off + r]);
         }
         if (want_ev) {
             auto& evs = res->events[t];
@@ -614,6 +618,7 @@ void fill_summary(msg_trace_summary& o, const DevTrace& tr, const DevSummary& x)
 msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* s, msg_batch_result** out) {
     const uint32_t T = (uint32_t)s->traces.size();
     const bool want_jobs = (s->out_flags & MSG_OUT_JOBS) != 0;
+    PhaseTimer pt;
     for (int k = 0; k < kPipeChunks; ++k) {
         if (!eng->pstream[k]) CK(cudaStreamCreateWithFlags(&eng->pstream[k], cudaStreamNonBlocking));
         if (!eng->pevent[k]) CK(cudaEventCreateWithFlags(&eng->pevent[k], cudaEventDisableTiming));
@@ -660,6 +665,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             CK(cudaMemcpyAsync(s->h_jobs.as<JobOut>() + j0, s->d_jobs.as<JobOut>() + j0, nj * sizeof(JobOut),
                                cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(eng->pevent[k], st));
+        pt.mark("  chunk staged+enqueued");
     }
     // Result layout: rows for every valid trace (JobsPending traces are
     // squeezed out at the end, a rare path).
@@ -689,6 +695,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
         if (d0 == d1) continue;
         CK(cudaEventSynchronize(eng->pevent[k]));
+        pt.mark("  chunk kernel+D2H done");
         parallel_for(d1 - d0, 64, [&](uint32_t i) {
             const uint32_t d = d0 + i, t = s->src_of[d];
             const DevTrace& tr = s->traces[d];
@@ -705,22 +712,10 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             }
             if (!want_jobs) return;
             msg_job_row* rows = res->jobs.p.get() + res->job_off[t];
-            for (uint32_t r = 0; r < tr.n_jobs; ++r) {
-                const JobOut& j = hj[tr.job_off + r];
-                msg_job_row& row = rows[r];
-                row.id = ids[r];
-                row.arrival_s = ha[tr.job_off + r];
-                row.scheduled_s = j.sched;
-                row.completed_s = j.done;
-                row.wait_s = row.scheduled_s - row.arrival_s;  // sim.cpp:473-475
-                row.execution_s = row.completed_s - row.scheduled_s;
-                row.turnaround_s = row.wait_s + row.execution_s;
-                row.profile = hp[tr.job_off + r];
-                row.gpu = j.gpu;
-                row.migrations = j.mig;
-                row.reserved0 = 0;
-            }
+            for (uint32_t r = 0; r < tr.n_jobs; ++r)
+                put_row(rows + r, ids[r], ha[tr.job_off + r], hj[tr.job_off + r], hp[tr.job_off + r]);
         });
+        pt.mark("  chunk decoded");
     }
     if (pending && want_jobs) {  // the reference throws for these traces: drop their rows
         uint64_t w = 0;

@@ -573,23 +573,32 @@ __device__ __forceinline__ void busy_item(const ScoreArgs& a, const ScoreSmem& s
 // Pass 2 (after score_tma_kernel<true, DYN>): snapshots whose pass 1 found no
 // Lazy candidate are scored again over all words with the full key (Busy
 // GPUs compete; their candidates are counted), exactly as the register path.
-// Every block first collects those snapshots from the pass-1 counts with one
-// coalesced sweep (usually none: the kernel then ends after reading 16 B per
-// snapshot), then walks their items grid-stride.
-constexpr int kBusyList = 4096;
+// score_list_kernel lists them between the passes, so with none listed this
+// kernel reads one word and ends.
 
 template <bool DYN>
 __global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem sm;
-    __shared__ uint32_t list[kBusyList];
-    __shared__ uint32_t wsum[kScoreThreads / 32];
-    __shared__ uint32_t cnt;
-    // Ordered compaction: thread t owns a contiguous run of snapshots, loads
-    // all their pass-1 counts at once, and one block-wide exclusive scan of
-    // the per-thread totals places the entries — every block builds the
-    // same list, with no barrier per snapshot.
+    const uint32_t* list = a.scratch + a.n + 1;  // score_list_kernel
+    const uint32_t need = *(volatile const uint32_t*)(a.scratch + a.n);
+    if (need == 0) return;
+    score_smem_init(sm, a.tables, a.lazymask);
+    __syncthreads();
+    const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
+    const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
+    for (uint64_t v = blockIdx.x; v < (uint64_t)need * items_per; v += gridDim.x) {
+        const uint32_t j = (uint32_t)(v / items_per), first = (uint32_t)(v - (uint64_t)j * items_per) * kItemChunks;
+        busy_item<DYN>(a, sm, list[j], first, min(first + kItemChunks, chunks_per));
+    }
+}
+
+// Between the passes: one block lists, in snapshot order, the snapshots
+// pass 1 left without a Lazy candidate (scratch[n] = count, then the list).
+constexpr int kListThreads = 1024;
+__global__ void __launch_bounds__(kListThreads) score_list_kernel(ScoreArgs a) {
+    __shared__ uint32_t wsum[kListThreads / 32];
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t per = (a.n + blockDim.x - 1) / blockDim.x, s0 = threadIdx.x * per;
+    const uint32_t per = (a.n + kListThreads - 1) / kListThreads, s0 = threadIdx.x * per;
     uint32_t mine = 0;
     for (uint32_t i = 0; i < per && s0 + i < a.n; ++i) mine += (a.out[2 * (s0 + i) + 1] >> 32) == 0;
     uint32_t incl = mine;
@@ -601,32 +610,10 @@ __global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) 
     __syncthreads();
     uint32_t off = incl - mine;
     for (unsigned w = 0; w < warp; ++w) off += wsum[w];
-    if (threadIdx.x == blockDim.x - 1) cnt = off + mine;
+    uint32_t* list = a.scratch + a.n + 1;
     for (uint32_t i = 0; i < per && s0 + i < a.n && mine; ++i)
-        if ((a.out[2 * (s0 + i) + 1] >> 32) == 0) {
-            if (off < (uint32_t)kBusyList) list[off] = s0 + i;
-            ++off;
-        }
-    __syncthreads();
-    const uint32_t need = cnt;
-    if (need == 0) return;
-    score_smem_init(sm, a.tables, a.lazymask);
-    __syncthreads();
-    const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
-    const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
-    if (need <= (uint32_t)kBusyList) {
-        for (uint32_t v = blockIdx.x; v < need * items_per; v += gridDim.x) {
-            const uint32_t j = v / items_per, first = (v - j * items_per) * kItemChunks;
-            busy_item<DYN>(a, sm, list[j], first, min(first + kItemChunks, chunks_per));
-        }
-        return;
-    }
-    for (uint32_t item = blockIdx.x; item < items_per * a.n; item += gridDim.x) {  // too many: flag per item
-        const uint32_t snap = item / items_per;
-        if ((a.out[2 * snap + 1] >> 32) != 0) continue;
-        const uint32_t first = (item - snap * items_per) * kItemChunks;
-        busy_item<DYN>(a, sm, snap, first, min(first + kItemChunks, chunks_per));
-    }
+        if ((a.out[2 * (s0 + i) + 1] >> 32) == 0) list[off++] = s0 + i;
+    if (threadIdx.x == kListThreads - 1) a.scratch[a.n] = off;
 }
 
 __global__ void score_init_kernel(uint64_t* out, uint32_t n) {
@@ -680,6 +667,7 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
     }
     if (tma && a.lb) {  // pass 2: snapshots without a Lazy candidate
+        score_list_kernel<<<1, kListThreads, 0, stream>>>(a);
         const dim3 g2((unsigned)std::min<uint64_t>(items, (uint64_t)sms * 4));
         if (a.dyn) score_busy_kernel<true><<<g2, block, 0, stream>>>(a);
         else score_busy_kernel<false><<<g2, block, 0, stream>>>(a);
