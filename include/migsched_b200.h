@@ -319,6 +319,25 @@ const int32_t* msg_trace_file_profile(const msg_trace_file* file);
 const double* msg_trace_file_service(const msg_trace_file* file);
 void msg_trace_file_free(msg_trace_file* file);
 
+/* ---- report emission: the reference's output files (reports.cpp:14-116)
+ * byte for byte, formatted in parallel on the host — events.jsonl
+ * (events_to_jsonl), report.json (report_to_json, needs the summary, the
+ * config and the per-job rows), report.csv (report_to_csv) and
+ * fragcost_timeline.csv (frag_timeline_to_csv), from the records of one
+ * trace (msg_result_events / _jobs / _timeline / _summary).  The text is
+ * library-allocated (NUL-terminated, *len bytes); free it with
+ * msg_text_free. */
+typedef enum msg_text_kind {
+    MSG_TEXT_EVENTS_JSONL = 0,
+    MSG_TEXT_REPORT_JSON = 1,
+    MSG_TEXT_REPORT_CSV = 2,
+    MSG_TEXT_TIMELINE_CSV = 3
+} msg_text_kind;
+msg_status msg_format_text(int32_t kind, const msg_trace_summary* summary, const msg_config* cfg,
+                           const msg_event* events, uint64_t n_events, const msg_job_row* jobs, uint64_t n_jobs,
+                           const msg_timeline_point* timeline, uint64_t n_timeline, char** text, size_t* len);
+void msg_text_free(char* text);
+
 /* ---- workload generation: migsched::generate (workload.hpp:45,
  * workload.cpp:98-127) with the same mt19937_64 inverse-transform sampler, so
  * a seed gives the same trace as the reference.  Host-side (trace staging). */

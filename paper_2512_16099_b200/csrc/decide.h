@@ -17,9 +17,11 @@ struct ScoreArgs {
     // scratch (n + 1 + n words; the first n unused): the count and list of
     // snapshots pass 1 left without a Lazy candidate (score_list_kernel)
     uint32_t* scratch;
+    uint64_t* items;  // TMA path: 2 words per item (score_items_bytes)
 };
 
 cudaError_t launch_snapshot(const SnapArgs& a, cudaStream_t stream);
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream);
+size_t score_items_bytes(uint32_t n, uint64_t G);
 
 }  // namespace msgk

@@ -57,15 +57,15 @@ static cudaError_t launch_sim_t(const SimArgs& a, cudaStream_t stream) {
 // Block engine for clusters of more than 32 GPUs: one thread-block cluster
 // of a.shards CTAs per trace (a.shards = 1: one block), each CTA one shard
 // of the trace's GPUs (cluster_core.cuh).  NT threads per CTA: 512 when a
-// CTA owns thousands of GPUs (S <= 8), 128 at 16 shards, where the
+// CTA owns thousands of GPUs (S <= 8), 256 at 16 shards, where the
 // per-event chain of block barriers and exchanges dominates the (then
-// small) per-shard scans: C4 at S = 16 runs 1.7x faster with 128 threads
+// small) per-shard scans: C4 at S = 16 runs 2.2x faster with 256 threads
 // than with 512 (profiles/r01).
 #ifndef MSG_CLUSTER_THREADS_WIDE
 #define MSG_CLUSTER_THREADS_WIDE 512
 #endif
 #ifndef MSG_CLUSTER_THREADS_NARROW
-#define MSG_CLUSTER_THREADS_NARROW 128
+#define MSG_CLUSTER_THREADS_NARROW 256
 #endif
 
 template <bool DETAIL, int NT>

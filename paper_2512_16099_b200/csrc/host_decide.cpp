@@ -129,6 +129,8 @@ msg_status msg_score_device(msg_engine* eng, uint32_t n, int64_t G, const uint64
     a.lazymask = lazymask_of(cfg->threshold);
     CK(eng->dscr[7].ensure((2 * (size_t)n + 1) * sizeof(uint32_t)));
     a.scratch = eng->dscr[7].as<uint32_t>();
+    CK(eng->dscr[8].ensure(std::max<size_t>(score_items_bytes(n, (uint64_t)G), 16)));
+    a.items = eng->dscr[8].as<uint64_t>();
     cudaError_t e = launch_score(a, eng->stream);
     if (e != cudaSuccess) return cuda_fail(eng, e, "launch_score");
     ++eng->launches;

@@ -258,6 +258,21 @@ __device__ __forceinline__ bool score_step(const ScoreArgs& a, const ScoreSmem& 
     return done;
 }
 
+// TMA path: the end of an item reduces each warp's key and counts into the
+// block's per-warp slots (double-buffered by stage parity); thread 0 folds
+// them after the stage barrier into the item's own output slot — no
+// atomics, no output initialisation (score_reduce_kernel merges the items).
+struct WarpPart {
+    unsigned best, cnt;
+};
+
+template <bool LB>
+__device__ __forceinline__ void stash_item(const ItemAcc& acc, WarpPart* wpart) {
+    const unsigned best = __reduce_min_sync(0xffffffffu, acc.best);
+    const unsigned cnt = LB ? __reduce_add_sync(0xffffffffu, acc.cnt) : 0u;
+    if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = WarpPart{best, cnt};
+}
+
 // One item: its chunks are scored with the profile's specialised code while
 // the following chunk (possibly the next item's first) is in flight.
 template <int P, bool LB, bool DYN>
@@ -278,7 +293,7 @@ __device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& 
 }
 
 template <bool LB, bool DYN>
-__global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem sm;
     score_smem_init(sm, a.tables, a.lazymask);
     __syncthreads();
@@ -426,13 +441,13 @@ __device__ __forceinline__ void score_stage(const TmaSmem& sm, int stage, const 
 }
 
 template <int P, bool LB, bool DYN>
-__device__ __forceinline__ void consume_stage(const ScoreArgs& a, const TmaSmem& sm, int stage, const StageMeta& m,
-                                              ItemAcc& acc) {
+__device__ __forceinline__ void consume_stage(const TmaSmem& sm, int stage, const StageMeta& m, ItemAcc& acc,
+                                              WarpPart* wpart) {
     acc.anyx = 0;
     score_stage<P, LB, DYN, false>(sm, stage, m, acc);
     if (LB && DYN && __any_sync(0xffffffffu, acc.anyx != 0)) score_stage<P, LB, DYN, true>(sm, stage, m, acc);
     if (m.last) {
-        flush_item<LB>(a, acc, m.snap, m.first);
+        stash_item<LB>(acc, wpart);
         acc = ItemAcc{0xFFFFFFFFu, 0u, 0u};
     }
 }
@@ -446,7 +461,7 @@ __device__ __forceinline__ void consume_stage(const ScoreArgs& a, const TmaSmem&
 // candidate are completed by score_busy_kernel (pass 2).
 template <int P, bool DYN>
 __device__ __forceinline__ void consume_lazy(const ScoreArgs& a, const TmaSmem& sm, int stage, const StageMeta& m,
-                                             ItemAcc& acc, uint16_t* wl) {
+                                             ItemAcc& acc, uint16_t* wl, WarpPart* wpart) {
     const uint64_t* buf = sm.buf[stage];
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const unsigned wbase = warp * 32u * kWordsPerThread;
@@ -478,7 +493,7 @@ __device__ __forceinline__ void consume_lazy(const ScoreArgs& a, const TmaSmem& 
     }
     __syncwarp();
     if (m.last) {
-        flush_item<true>(a, acc, m.snap, m.first);
+        stash_item<true>(acc, wpart);
         acc = ItemAcc{0xFFFFFFFFu, 0u, 0u};
     }
 }
@@ -487,6 +502,7 @@ template <bool LB, bool DYN>
 __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem tables;
     __shared__ uint16_t wlist[kScoreThreads / 32][32 * kWordsPerThread];  // pass 1: Lazy words per warp
+    __shared__ WarpPart wpart[2][kScoreThreads / 32];                     // item ends, by stage parity
     extern __shared__ __align__(128) unsigned char ring[];
     TmaSmem sm{tables, reinterpret_cast<uint64_t(*)[kChunk]>(ring),
                reinterpret_cast<uint64_t*>(ring + sizeof(uint64_t) * kChunk * kStages),
@@ -496,6 +512,7 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
     const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
     const uint32_t n_items = items_per * a.n;
     Producer p;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.scratch[a.n] = 0;  // pass-2 list length
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&sm.full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -512,27 +529,45 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
         const StageMeta m = sm.meta[stage];
         if (m.snap == 0xFFFFFFFFu) break;
         uint16_t* wl = wlist[threadIdx.x >> 5];
+        WarpPart* wp = wpart[n & 1u];
         if (LB) {
             switch (m.prof) {
-                case 0: consume_lazy<0, DYN>(a, sm, stage, m, acc, wl); break;
-                case 1: consume_lazy<1, DYN>(a, sm, stage, m, acc, wl); break;
-                case 2: consume_lazy<2, DYN>(a, sm, stage, m, acc, wl); break;
-                case 3: consume_lazy<3, DYN>(a, sm, stage, m, acc, wl); break;
-                case 4: consume_lazy<4, DYN>(a, sm, stage, m, acc, wl); break;
-                default: consume_lazy<5, DYN>(a, sm, stage, m, acc, wl); break;
+                case 0: consume_lazy<0, DYN>(a, sm, stage, m, acc, wl, wp); break;
+                case 1: consume_lazy<1, DYN>(a, sm, stage, m, acc, wl, wp); break;
+                case 2: consume_lazy<2, DYN>(a, sm, stage, m, acc, wl, wp); break;
+                case 3: consume_lazy<3, DYN>(a, sm, stage, m, acc, wl, wp); break;
+                case 4: consume_lazy<4, DYN>(a, sm, stage, m, acc, wl, wp); break;
+                default: consume_lazy<5, DYN>(a, sm, stage, m, acc, wl, wp); break;
             }
         } else {
             switch (m.prof) {
-                case 0: consume_stage<0, LB, DYN>(a, sm, stage, m, acc); break;
-                case 1: consume_stage<1, LB, DYN>(a, sm, stage, m, acc); break;
-                case 2: consume_stage<2, LB, DYN>(a, sm, stage, m, acc); break;
-                case 3: consume_stage<3, LB, DYN>(a, sm, stage, m, acc); break;
-                case 4: consume_stage<4, LB, DYN>(a, sm, stage, m, acc); break;
-                default: consume_stage<5, LB, DYN>(a, sm, stage, m, acc); break;
+                case 0: consume_stage<0, LB, DYN>(sm, stage, m, acc, wp); break;
+                case 1: consume_stage<1, LB, DYN>(sm, stage, m, acc, wp); break;
+                case 2: consume_stage<2, LB, DYN>(sm, stage, m, acc, wp); break;
+                case 3: consume_stage<3, LB, DYN>(sm, stage, m, acc, wp); break;
+                case 4: consume_stage<4, LB, DYN>(sm, stage, m, acc, wp); break;
+                default: consume_stage<5, LB, DYN>(sm, stage, m, acc, wp); break;
             }
         }
         __syncthreads();  // every thread is done with the stage
-        if (threadIdx.x == 0) prod_issue(a, sm, p, stage, chunks_per, items_per, n_items);
+        if (threadIdx.x == 0) {
+            prod_issue(a, sm, p, stage, chunks_per, items_per, n_items);
+            if (m.last) {  // the item's result: min key (rebased to the global GPU index), counts
+                unsigned best = 0xFFFFFFFFu, cnt = 0;
+                for (int w = 0; w < kScoreThreads / 32; ++w) {
+                    best = min(best, wp[w].best);
+                    cnt += wp[w].cnt;
+                }
+                uint64_t g64 = ~0ull;
+                if (best != 0xFFFFFFFFu) {
+                    const uint64_t gpu = (uint64_t)m.first * kChunk + ((best >> 3) & ((1u << 22) - 1u));
+                    g64 = ((uint64_t)(best >> 25) << 35) | (gpu << 3) | (best & 7u);
+                }
+                uint64_t* it = a.items + 2 * ((uint64_t)m.snap * items_per + m.first / kItemChunks);
+                it[0] = g64;
+                it[1] = ((uint64_t)(cnt >> 16) << 32) | (cnt & 0xFFFFu);
+            }
+        }
     }
 }
 
@@ -573,13 +608,13 @@ __device__ __forceinline__ void busy_item(const ScoreArgs& a, const ScoreSmem& s
 // Pass 2 (after score_tma_kernel<true, DYN>): snapshots whose pass 1 found no
 // Lazy candidate are scored again over all words with the full key (Busy
 // GPUs compete; their candidates are counted), exactly as the register path.
-// score_list_kernel lists them between the passes, so with none listed this
-// kernel reads one word and ends.
+// score_reduce_kernel lists them between the passes, so with none listed
+// this kernel reads one word and ends.
 
 template <bool DYN>
 __global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem sm;
-    const uint32_t* list = a.scratch + a.n + 1;  // score_list_kernel
+    const uint32_t* list = a.scratch + a.n + 1;  // score_reduce_kernel
     const uint32_t need = *(volatile const uint32_t*)(a.scratch + a.n);
     if (need == 0) return;
     score_smem_init(sm, a.tables, a.lazymask);
@@ -592,28 +627,22 @@ __global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) 
     }
 }
 
-// Between the passes: one block lists, in snapshot order, the snapshots
-// pass 1 left without a Lazy candidate (scratch[n] = count, then the list).
-constexpr int kListThreads = 1024;
-__global__ void __launch_bounds__(kListThreads) score_list_kernel(ScoreArgs a) {
-    __shared__ uint32_t wsum[kListThreads / 32];
-    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t per = (a.n + kListThreads - 1) / kListThreads, s0 = threadIdx.x * per;
-    uint32_t mine = 0;
-    for (uint32_t i = 0; i < per && s0 + i < a.n; ++i) mine += (a.out[2 * (s0 + i) + 1] >> 32) == 0;
-    uint32_t incl = mine;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if ((int)lane >= o) incl += v;
+// After pass 1 (TMA path): each snapshot's items merge into its output —
+// minimum key, summed counts — and, with load balancing, the snapshots left
+// without a Lazy candidate are listed for pass 2 (scratch[n] = count, then
+// the list; the order is irrelevant, every pass-2 block reads the same list).
+__global__ void score_reduce_kernel(ScoreArgs a, uint32_t items_per) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= a.n) return;
+    uint64_t best = ~0ull, cnt = 0;
+    const uint64_t* it = a.items + 2 * (uint64_t)s * items_per;
+    for (uint32_t i = 0; i < items_per; ++i) {
+        best = it[2 * i] < best ? it[2 * i] : best;
+        cnt += it[2 * i + 1];
     }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    uint32_t off = incl - mine;
-    for (unsigned w = 0; w < warp; ++w) off += wsum[w];
-    uint32_t* list = a.scratch + a.n + 1;
-    for (uint32_t i = 0; i < per && s0 + i < a.n && mine; ++i)
-        if ((a.out[2 * (s0 + i) + 1] >> 32) == 0) list[off++] = s0 + i;
-    if (threadIdx.x == kListThreads - 1) a.scratch[a.n] = off;
+    a.out[2 * s] = best;
+    a.out[2 * s + 1] = cnt;
+    if (a.lb && (cnt >> 32) == 0) a.scratch[a.n + 1 + atomicAdd(&a.scratch[a.n], 1u)] = s;
 }
 
 __global__ void score_init_kernel(uint64_t* out, uint32_t n) {
@@ -624,9 +653,13 @@ __global__ void score_init_kernel(uint64_t* out, uint32_t n) {
     }
 }
 
+size_t score_items_bytes(uint32_t n, uint64_t G) {
+    const uint64_t chunks_per = (G + kChunk - 1) / kChunk;
+    return (size_t)n * ((chunks_per + kItemChunks - 1) / kItemChunks) * 2 * sizeof(uint64_t);
+}
+
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     if (!a.n || !a.G) return cudaSuccess;
-    score_init_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(a.out, a.n);
     static int sms = 0, per_sm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (!sms) {
         int dev = 0;
@@ -656,6 +689,7 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     // persistent grid: exactly the resident blocks (one wave)
     const uint64_t blocks = std::min<uint64_t>(items, (uint64_t)sms * std::max(1, per_sm[v]));
     const dim3 grid((unsigned)blocks), block(kScoreThreads);
+    if (!tma) score_init_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(a.out, a.n);  // register path: atomics
     switch (v) {
         case 0: score_kernel<false, false><<<grid, block, 0, stream>>>(a); break;
         case 1: score_kernel<false, true><<<grid, block, 0, stream>>>(a); break;
@@ -666,8 +700,8 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         case 6: score_tma_kernel<true, false><<<grid, block, kTmaDynBytes, stream>>>(a); break;
         default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
     }
+    if (tma) score_reduce_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(a, (uint32_t)(items / a.n));
     if (tma && a.lb) {  // pass 2: snapshots without a Lazy candidate
-        score_list_kernel<<<1, kListThreads, 0, stream>>>(a);
         const dim3 g2((unsigned)std::min<uint64_t>(items, (uint64_t)sms * 4));
         if (a.dyn) score_busy_kernel<true><<<g2, block, 0, stream>>>(a);
         else score_busy_kernel<false><<<g2, block, 0, stream>>>(a);

@@ -62,6 +62,9 @@ def lib():
         "msg_generate": (C.c_int, [vp, vp, vp, vp, vp]),
         "msg_generate_many": (C.c_int, [vp, u64, u32, i32, vp, vp, vp, vp, vp]),
         "msg_trace_load": (C.c_int, [C.c_char_p, C.POINTER(vp), C.c_char_p, C.c_size_t]),
+        "msg_format_text": (C.c_int, [C.c_int32, vp, vp, vp, u64, vp, u64, vp, u64, C.POINTER(vp),
+                                      C.POINTER(C.c_size_t)]),
+        "msg_text_free": (None, [vp]),
         "msg_trace_file_jobs": (u64, [vp]),
         "msg_trace_file_ids": (vp, [vp]),
         "msg_trace_file_arrival": (vp, [vp]),
@@ -297,6 +300,31 @@ def generate(spec: WorkloadSpec):
     s = spec.to_abi()
     _check(lib().msg_generate(C.byref(s), ids.ctypes.data, arr.ctypes.data, prof.ctypes.data, svc.ctypes.data))
     return [Job(int(ids[i]), float(arr[i]), int(prof[i]), float(svc[i])) for i in range(n)]
+
+
+TEXT_KINDS = {"events.jsonl": 0, "report.json": 1, "report.csv": 2, "fragcost_timeline.csv": 3}
+
+
+def format_text(kind: str, res: TraceResult, cfg: Optional[SimConfig] = None) -> str:
+    """reports.cpp serializers over one TraceResult (see TraceResult.text)."""
+    L = lib()
+    k = TEXT_KINDS[kind]
+
+    def ptr(a):
+        return (a.ctypes.data if a is not None and len(a) else None), (len(a) if a is not None else 0)
+
+    ev, nev = ptr(res.events)
+    jb, njb = ptr(res.per_job)
+    tl, ntl = ptr(res.frag_timeline)
+    summ = np.ascontiguousarray(np.array([res.summary], abi.SUMMARY_DTYPE))
+    pack = ConfigPack([cfg]) if cfg is not None else None
+    cptr = C.addressof(pack.c[0]) if pack is not None else None
+    out, n = C.c_void_p(), C.c_size_t()
+    _check(L.msg_format_text(k, summ.ctypes.data, cptr, ev, nev, jb, njb, tl, ntl, C.byref(out), C.byref(n)))
+    try:
+        return C.string_at(out, n.value).decode()
+    finally:
+        L.msg_text_free(out)
 
 
 def load_trace(path: str) -> TraceBatch:

@@ -44,6 +44,15 @@ class TraceResult:
     def code(self) -> str:
         return abi.STATUS_NAMES.get(self.status, "Unknown")
 
+    def text(self, kind: str, cfg=None) -> str:
+        """The reference CLI's output file for this result, byte for byte
+        (reports.cpp:14-116): kind in {"events.jsonl", "report.json",
+        "report.csv", "fragcost_timeline.csv"}; report.json needs the
+        SimConfig.  Formatted natively and in parallel (msg_format_text)."""
+        from .engine import format_text
+
+        return format_text(kind, self, cfg)
+
     def raise_for_status(self) -> "TraceResult":
         if self.status != 0:
             raise MigschedError(self.code, self.message)

@@ -211,3 +211,21 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
         if d := diff_results(r, g):
             bad.append((t, d))
     assert not bad, bad[:3]
+
+
+def test_report_files_from_gpu_results_match_reference(engine):
+    """§8f row 1: the reference CLI's files (events.jsonl, report.json,
+    report.csv, fragcost_timeline.csv) formatted natively from the GPU
+    engine's results equal the reference serializers' bytes."""
+    kinds = ("events.jsonl", "report.json", "report.csv", "fragcost_timeline.csv")
+    for spec, cfg, seeds in ((preset("normal25"), SimConfig(gpu_count=8), [0, 7]),
+                             (WorkloadSpec(mean_interarrival_s=0.4, median_s=4.0, sigma=1.2,
+                                           profile_mix=(0.5, 0.3, 0.2, 0.0)),
+                              SimConfig(gpu_count=8, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                                        reconfig_latency_s=0.1), [3])):
+        b = rb.ref_generate_batch(spec, seeds)
+        ref = rb.ref_run_batch_results(b, [cfg], texts=True)
+        gpu = engine.run_batch(b, [cfg], ALL)
+        for r, g in zip(ref, gpu):
+            for kind, want in zip(kinds, r.texts):
+                assert g.text(kind, cfg) == want, kind
