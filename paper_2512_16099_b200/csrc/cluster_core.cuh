@@ -34,9 +34,11 @@
 // GPU word its owner broadcasts).  Inboxes and barriers are
 // double-buffered by round parity; there is no cluster-wide barrier and no
 // global-memory fence on this path.  Exchanges per handler:
-//   next event (always) · one per placement attempt (arrival, dequeue pass)
-//   · on a completion with migration: one broadcasting the departed GPU's
-//   word (Lazy/Busy) and, if Lazy, one per plan_inter iteration.
+//   next event (always; its record also carries the winning slot's GPU word,
+//   which every shard then follows through the dequeue pass to classify a
+//   completed job's GPU without an exchange) · one per placement attempt
+//   (arrival, dequeue pass) · on a completion with migration onto a Lazy
+//   GPU, one per plan_inter iteration.
 // plan_intra, create_instance and the placement itself are owner-local.
 // Fragmentation-timeline samples are deferred: each shard queues its part
 // of the cost total at the sample point and the next exchange sums them.
@@ -142,6 +144,15 @@ struct ClusterSim {
     bool tl_dirty;
     // deferred timeline samples (sharded)
     uint32_t npend;
+    // sharded: the GPU word of the last completion's GPU, tracked by every
+    // shard (from the next-event record, then through the placements of the
+    // dequeue pass), so on_departure needs no exchange to classify it
+    int dep_g;
+    unsigned dep_w;
+    // sharded: the pending arrival's decision, searched in the next-event exchange
+    bool spec;
+    uint64_t spec_key;
+    unsigned spec_nl, spec_nb;
 
     // ------------------------------------------------------------- tables
     MSG_DI unsigned rank2(unsigned bc, unsigned bm) const { return tb->cost2rank[wp::popc(bc) * 256 + bm]; }
@@ -210,7 +221,7 @@ struct ClusterSim {
         r.mx = 0;
         r.pad = 0;
         r.ks[0] = r.ks[1] = 0;
-        r.pad2 = 0;
+        r.pad2 = ~0ull;
         return r;
     }
     // Identical reduction of one record per lane (lanes beyond the senders
@@ -234,7 +245,11 @@ struct ClusterSim {
         for (int k = 0; k < 4; ++k) o.c[k] = wp::radd(x.c[k]);
         o.mx = wp::rmax(x.mx);
         o.pad = 0;
-        o.pad2 = 0;
+        {  // pad2: a second 64-bit minimum (the speculative arrival decision key)
+            const unsigned h = wp::rmin((unsigned)(x.pad2 >> 32));
+            const unsigned l = wp::rmin((unsigned)(x.pad2 >> 32) == h ? (unsigned)x.pad2 : NONE);
+            o.pad2 = ((uint64_t)h << 32) | l;
+        }
         for (int k = 0; k < 2; ++k) {  // parts < 2^35: 20-bit split keeps the lane sums in 32 bits
             const unsigned lo20 = wp::radd((unsigned)(x.ks[k] & 0xFFFFFu));
             const unsigned hi20 = wp::radd((unsigned)(x.ks[k] >> 20));
@@ -347,6 +362,9 @@ struct ClusterSim {
         if (T < D) sc->ib[T] = reinterpret_cast<XInbox*>(a.inbox[T]) + wp::cluster_id() / vd;
         xround = 0;
         npend = 0;
+        dep_g = -1;
+        dep_w = 0;
+        spec = false;
         const DevTrace tr = a.traces[t];
         const DevConfig c = a.configs[tr.cfg];
         G = c.G;
@@ -628,24 +646,42 @@ struct ClusterSim {
         block_lexmin(bhi, blo, btie, bms, bi);
         double tmin = 0.0;
         slot = -1;
+        unsigned winfo = 0;
         if (bhi != NONE) {
             tmin = atkey[bi];
             slot = aslot[bi];
+            winfo = (W_(slot >> 3) & 0x0FFFFFFFu) | ((unsigned)prof[slot] << 28);  // GPU word | slot profile
         }
         if (NS > 1) {
             XRec r = xnone();
+            // The pending arrival's placement search rides in the same
+            // exchange when it would dispatch at once (empty queue): the
+            // masks it reads do not change before handle_arrival.
+            spec = a_idx < N && q_head == q_tail;
+            if (spec) {
+                uint64_t k;
+                local_dispatch(a_prof, k, r.c[0], r.c[1]);
+                r.pad2 = k;
+            }
             r.hi = bhi;
             r.lo = blo;
             r.tie = btie;
             r.ms = bms;
             r.slot = slot;
             r.tkey = tmin;
+            r.info = winfo;
             exchange(r);
+            if (spec) {
+                spec_key = r.pad2;
+                spec_nl = r.c[0];
+                spec_nb = r.c[1];
+            }
             bhi = r.hi;
             blo = r.lo;
             btie = r.tie;
             slot = r.slot;
             tmin = r.tkey;
+            winfo = r.info;
         }
         const bool have_arrival = a_idx < N;
         ev_i = -1;
@@ -660,13 +696,20 @@ struct ClusterSim {
         }
         if (own(slot >> 3)) ev_i = apos[slot];
         now = tmin;
+        if ((btie >> 28) == 0u) {  // a completion: its GPU's word once the slot is idle (gpu.cpp:113-125)
+            const int q = (int)(winfo >> 28), s0 = slot & 7;
+            const unsigned m = fpm(q, s0);
+            dep_g = slot >> 3;
+            dep_w = (winfo & ~(fpc(q, s0) | (m << 8) | (m << 16))) & 0x00FFFFFFu;
+        }
         return (int)(btie >> 28);
     }
 
     // ------------------------------------------------------------ schedule
-    MSG_DI Decision dispatch(int p) {  // scheduler.cpp:47-104
+    // This shard's candidates for a job of profile p (scheduler.cpp:47-104):
+    // the block-wide minimum packed key and the Lazy / Busy candidate counts.
+    MSG_DI void local_dispatch(int p, uint64_t& key, unsigned& NL, unsigned& NB) {
         wp::bsync();
-        Decision d;
         const unsigned n = count_of(p), stride = stride_of(p);
         const unsigned pb = pidx(p, 0);
         const bool dyn = (cflags & CF_DYN) != 0;
@@ -681,42 +724,35 @@ struct ClusterSim {
                 const int s = (int)(j * stride);
                 const bool exact = (ex >> j) & 1u;
                 if ((dyn || exact) && !(fpm(p, s) & w_km(wd))) {
-                    uint64_t key;
+                    uint64_t k;
                     if (lb) {
                         const unsigned rk = rank2(w_bc(wd) | fpc(p, s), w_bm(wd) | fpm(p, s));
-                        key = ((uint64_t)(lazy ^ 1u) << 47) | ((uint64_t)rk << 42) | ((uint64_t)(exact ? 0u : 1u) << 41) |
-                              ((uint64_t)g << 3) | (uint64_t)s;
+                        k = ((uint64_t)(lazy ^ 1u) << 47) | ((uint64_t)rk << 42) | ((uint64_t)(exact ? 0u : 1u) << 41) |
+                            ((uint64_t)g << 3) | (uint64_t)s;
                         nl += lazy;
                         nb += lazy ^ 1u;
                     } else {
-                        key = ((uint64_t)g << 3) | (uint64_t)s;
+                        k = ((uint64_t)g << 3) | (uint64_t)s;
                     }
-                    kmin = key < kmin ? key : kmin;
+                    kmin = k < kmin ? k : kmin;
                 }
             }
         }
         unsigned hi = (unsigned)(kmin >> 32), lo = (unsigned)kmin, z0 = 0, z1 = 0;
         int pay = 0;
         block_lexmin(hi, lo, z0, z1, pay);
-        unsigned NL = 0, NB = 0;
+        NL = NB = 0;
         if (lb) {
             NL = block_sum(nl);
             NB = block_sum(nb);
         }
-        if (NS > 1) {
-            XRec r = xnone();
-            r.hi = hi;
-            r.lo = lo;
-            r.tie = r.ms = 0;
-            r.c[0] = NL;
-            r.c[1] = NB;
-            exchange(r);
-            hi = r.hi;
-            lo = r.lo;
-            NL = r.c[0];
-            NB = r.c[1];
-        }
-        const uint64_t k = ((uint64_t)hi << 32) | lo;
+        key = ((uint64_t)hi << 32) | lo;
+    }
+
+    // The decision from the global minimum key and counts.
+    MSG_DI Decision decide(int p, uint64_t k, unsigned NL, unsigned NB) {
+        const bool lb = (cflags & CF_LB) != 0;
+        Decision d;
         d.placed = k != ~0ull;
         d.evals = lb ? NL + (NL == 0 ? NB : 0u) : 0u;
         d.g = (int)((k >> 3) & 0x3FFFFFFFFull);
@@ -727,6 +763,25 @@ struct ClusterSim {
             else if (own(d.g)) d.reused = (gx[d.g - g_lo] >> pidx(p, d.s)) & 1u;
         }
         return d;
+    }
+
+    MSG_DI Decision dispatch(int p) {  // scheduler.cpp:47-104
+        uint64_t k;
+        unsigned NL, NB;
+        local_dispatch(p, k, NL, NB);
+        if (NS > 1) {
+            XRec r = xnone();
+            r.hi = (unsigned)(k >> 32);
+            r.lo = (unsigned)k;
+            r.tie = r.ms = 0;
+            r.c[0] = NL;
+            r.c[1] = NB;
+            exchange(r);
+            k = ((uint64_t)r.hi << 32) | r.lo;
+            NL = r.c[0];
+            NB = r.c[1];
+        }
+        return decide(p, k, NL, NB);
     }
 
     // ---------------------------------------------------- create_instance
@@ -805,6 +860,10 @@ struct ClusterSim {
 
     // The decided placement, on the GPU's owner only.
     MSG_DI void place(const Decision& d, int32_t r, int p, double sv, uint8_t kind) {
+        if (d.g == dep_g) {  // every shard follows the departed GPU's masks (create_instance never
+            const unsigned m = fpm(p, d.s);  // touches busy masks of other instances)
+            dep_w |= fpc(p, d.s) | (m << 8) | (m << 16);
+        }
         if (!own(d.g)) return;
         const CreateRes cr = create(d.g, p, d.s);
         const unsigned nops = (unsigned)wp::popc(cr.dmask) + (cr.reused ? 0u : 1u);
@@ -1061,13 +1120,9 @@ struct ClusterSim {
 
     MSG_DI void on_departure(int g) {  // migration.cpp:212-220
         wp::bsync();
-        unsigned wd = own(g) ? W_(g) : 0u;
-        if (NS > 1) {
-            XRec x = xnone();
-            x.w = wd;
-            exchange(x);
-            wd = x.w;
-        }
+        // sharded: every shard tracked g's masks since the completion (the
+        // running count, not needed here, is left out)
+        const unsigned wd = NS > 1 ? dep_w : W_(g);
         if ((lazymask >> wp::popc(w_bc(wd))) & 1u) plan_inter(g, wd);
         else if (own(g)) plan_intra(g);
     }
@@ -1081,7 +1136,7 @@ struct ClusterSim {
         load_arrival();
         bool enq = q_head < q_tail;
         if (!enq) {
-            const Decision d = dispatch(p);
+            const Decision d = spec ? decide(p, spec_key, spec_nl, spec_nb) : dispatch(p);
             max_arr = max_arr > (int)d.evals ? max_arr : (int)d.evals;
             if (d.placed) place(d, r, p, sv, EV_ARRIVAL);
             else enq = true;

@@ -39,7 +39,7 @@ struct alignas(16) XRec {
     uint32_t mx;               // max
     uint32_t pad;
     uint64_t ks[2];            // sums: deferred timeline samples (cost-total parts)
-    uint64_t pad2;
+    uint64_t pad2;             // second minimum: the pending arrival's placement key (next-event exchange)
 };
 static_assert(sizeof(XRec) == 96, "exchange record layout (6 x 16-byte pushes)");
 
