@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -544,6 +545,49 @@ int ref_save_trace(const char* path, int64_t n, const int64_t* id, const double*
         return 1;
     }
     return 0;
+}
+
+// ---- the CLI's ablation (tools/migsched.cpp:64-99, reports.cpp:137-168) on
+// the reference library, for the CLI parity test: writes ablation.json and
+// the table (NUL-terminated, truncated to the buffer sizes); 0 on success.
+int ref_ablation(const msg_trace_batch* batch, const msg_config* base, char* json, size_t jlen, char* table,
+                 size_t tlen) {
+    try {
+        const std::vector<Job> trace = to_trace(batch, 0);
+        const SimConfig cfg0 = to_sim_config(*base);
+        struct Step {
+            const char* name;
+            FeatureFlags features;
+        };
+        const Step steps[] = {{"baseline", {false, false, false}},
+                              {"lb", {true, false, false}},
+                              {"lb+dyn", {true, true, false}},
+                              {"lb+dyn+migr", {true, true, true}}};
+        std::vector<AblationRow> rows;
+        double base_turn = 0.0;
+        for (const Step& st : steps) {
+            SimConfig cfg = cfg0;
+            cfg.sched.features = st.features;
+            if (!cfg.sched.features.dynamic_partitioning && !cfg.sched.static_layout)
+                cfg.sched.static_layout = static_layout_preset("static-a");
+            const SimResult r = run(trace, cfg);
+            AblationRow row;
+            row.name = st.name;
+            row.features = st.features;
+            row.mean_turnaround_s = r.report.mean_turnaround_s;
+            row.mean_wait_s = r.report.mean_wait_s;
+            row.mean_execution_s = r.report.mean_execution_s;
+            row.workload_makespan_s = r.report.workload_makespan_s;
+            if (rows.empty()) base_turn = row.mean_turnaround_s;
+            row.normalized_turnaround = base_turn > 0.0 ? row.mean_turnaround_s / base_turn : 1.0;
+            rows.push_back(row);
+        }
+        std::snprintf(json, jlen, "%s", ablation_to_json(rows).c_str());
+        std::snprintf(table, tlen, "%s", ablation_to_table(rows).c_str());
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
 }
 
 }  // extern "C"

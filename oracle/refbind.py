@@ -308,3 +308,18 @@ def ref_save_trace(path: str, ids, arrival, profile, service) -> None:
     if ref_lib().ref_save_trace(os.fsencode(path), len(ids), ids.ctypes.data, arrival.ctypes.data,
                                 profile.ctypes.data, service.ctypes.data):
         raise RuntimeError("save_trace failed")
+
+
+def ref_ablation(batch: TraceBatch, cfg: SimConfig):
+    """The reference CLI's ablate (tools/migsched.cpp:64-99) on the
+    reference library: (ablation.json text, table text)."""
+    lib = ref_lib()
+    f = lib.ref_ablation
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t]
+    pack = ConfigPack([cfg])
+    js = C.create_string_buffer(1 << 16)
+    tb = C.create_string_buffer(1 << 12)
+    if f(C.addressof(batch._c), C.addressof(pack.c[0]), js, len(js), tb, len(tb)):
+        raise RuntimeError("reference ablation failed")
+    return js.value.decode(), tb.value.decode()
