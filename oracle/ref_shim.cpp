@@ -14,6 +14,7 @@
 #include <cstring>
 #include <deque>
 #include <map>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -588,6 +589,58 @@ int ref_ablation(const msg_trace_batch* batch, const msg_config* base, char* jso
     } catch (const std::exception&) {
         return 1;
     }
+}
+
+// ---- brute-force scheduler oracle over clusters of enumerated states
+// (oracle.cpp:233-296, check_cluster_against_search): for every cluster of
+// G states (indices into enumerate_states(depth)) and every profile, the
+// placement the exact-fraction search picks — Lazy GPUs first (threshold
+// 0.4), per GPU best_placement_search (lower start on ties), then the
+// lowest cost, lower GPU on ties; (-1, -1) when nothing fits.  Threaded.
+void ref_oracle_clusters(int depth, int G, const int32_t* idx, int64_t n, int32_t* out_gpu, int32_t* out_start,
+                         int threads) {
+    const auto states = oracle::enumerate_states(depth);
+    std::vector<int> used(states.size(), 0);
+    for (size_t i = 0; i < states.size(); ++i)
+        for (const auto& u : states[i].busy) used[i] += profiles()[(size_t)u.profile_index].compute_slices;
+    // per state and profile: the best single-GPU placement (start, cost)
+    std::vector<std::optional<oracle::BestPlacement>> best(states.size() * kProfileCount);
+    for (size_t i = 0; i < states.size(); ++i)
+        for (int p = 0; p < kProfileCount; ++p)
+            best[i * kProfileCount + p] = oracle::best_placement_search(states[i], profiles()[(size_t)p]);
+    std::atomic<int64_t> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const int64_t c0 = next.fetch_add(256);
+            if (c0 >= n) return;
+            for (int64_t c = c0; c < std::min<int64_t>(n, c0 + 256); ++c) {
+                for (int p = 0; p < kProfileCount; ++p) {
+                    int bg = -1, bs = -1;
+                    double bc = 0.0;
+                    for (int pass = 0; pass < 2 && bg < 0; ++pass) {
+                        for (int g = 0; g < G; ++g) {
+                            const int st = idx[c * G + g];
+                            const bool lazy = used[(size_t)st] / 7.0 < 0.4;
+                            if ((pass == 0) != lazy) continue;
+                            const auto& b = best[(size_t)st * kProfileCount + p];
+                            if (b && (bg < 0 || b->cost < bc)) {
+                                bg = g;
+                                bs = b->start;
+                                bc = b->cost;
+                            }
+                        }
+                    }
+                    out_gpu[c * kProfileCount + p] = bg;
+                    out_start[c * kProfileCount + p] = bs;
+                }
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    const int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
 }
 
 }  // extern "C"

@@ -323,3 +323,19 @@ def ref_ablation(batch: TraceBatch, cfg: SimConfig):
     if f(C.addressof(batch._c), C.addressof(pack.c[0]), js, len(js), tb, len(tb)):
         raise RuntimeError("reference ablation failed")
     return js.value.decode(), tb.value.decode()
+
+
+def ref_oracle_clusters(depth: int, clusters: np.ndarray, threads: int = 0):
+    """Brute-force scheduler oracle (oracle.cpp:233-296) for clusters given as
+    rows of state indices into enumerate_states(depth): expected (gpu, start)
+    per cluster and profile, shape (n, 6) each; -1 when nothing fits."""
+    lib = ref_lib()
+    f = lib.ref_oracle_clusters
+    f.restype = None
+    f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]
+    idx = np.ascontiguousarray(clusters, np.int32)
+    n, G = idx.shape
+    g = np.zeros((n, 6), np.int32)
+    s = np.zeros((n, 6), np.int32)
+    f(depth, G, idx.ctypes.data, n, g.ctypes.data, s.ctypes.data, threads)
+    return g, s

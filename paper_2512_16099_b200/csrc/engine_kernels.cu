@@ -21,7 +21,7 @@ constexpr int kWarpsPerBlock = MSG_SIM_WPB;
 
 template <int SPL, bool DETAIL>
 #ifndef MSG_SIM_MINB
-#define MSG_SIM_MINB 8
+#define MSG_SIM_MINB 7
 #endif
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, MSG_SIM_MINB) sim_kernel(SimArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
