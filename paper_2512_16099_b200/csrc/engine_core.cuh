@@ -77,6 +77,7 @@ struct WarpSmem {
     double rem[NS];    // RunJob::remaining_work (WAIT: service demand)
     double tkey[NS];   // timer time of the slot
     double gcost[NG];  // frag_cost(gpu) for the timeline (4-mask form)
+    double tlp[NG + 2];  // timeline prefix sums: tlp[g] = ((c0 + c1) + ...) + c(g-1), reference order
     int32_t job[NS];   // bound job rank (RUN/WAIT) or migrating job (DRAIN)
     uint32_t cseq[NS]; // instance creation order (vector order, gpu.cpp:88-111)
     uint32_t mseq[NS]; // MigrationEnd push sequence
@@ -137,7 +138,7 @@ struct TraceSim {
     uint32_t n_plan_iter;
     bool snap_mode;
     double tl_sum, tl_mean;
-    bool tl_dirty;
+    unsigned tl_from;  // first GPU whose cost changed since the last timeline sum (G: none)
     // RunJob::last_update of EVERY running job equals the time of the last
     // handler: advance_all stamps all of them, start_service stamps `now`,
     // moves carry it (sim.cpp:153-165,212-218).  So dt is warp-uniform.
@@ -217,7 +218,7 @@ struct TraceSim {
         snap_mode = false;
         tl_sum = 0.0;
         tl_mean = 0.0;
-        tl_dirty = true;
+        tl_from = 0;
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
@@ -284,7 +285,7 @@ struct TraceSim {
         n_plan_iter = 0;
         snap_mode = true;
         tl_sum = tl_mean = 0.0;
-        tl_dirty = true;
+        tl_from = 0;
         const size_t base = (size_t)i * (size_t)G * 8;
         unsigned maxseq = 0;
         bool any = false;
@@ -357,11 +358,14 @@ struct TraceSim {
             }
         }
         const unsigned w = wp::ror(c) | (wp::radd(r) << 24);
+        const double nc = cost4w(w), oc = sm->gcost[g];
+        wp::sync();
         if (L == 0) {
             sm->gw[g] = w;
-            sm->gcost[g] = cost4w(w);
+            sm->gcost[g] = nc;
         }
-        tl_dirty = true;
+        // only a changed cost re-opens the timeline sum, from this GPU on
+        if (wp::dbits(nc) != wp::dbits(oc) && (unsigned)g < tl_from) tl_from = (unsigned)g;
         wp::sync();
         return w;
     }
@@ -415,13 +419,19 @@ struct TraceSim {
     }
 
     // sample_timeline (sim.cpp:177-181): sequential sum in GPU order / G.
+    // The running prefix sums are kept, so after a change on GPU g only the
+    // tail g .. G-1 of the chain is re-added (same additions, same order).
     MSG_DI void sample() {
-        if (tl_dirty) {
+        if (tl_from < (unsigned)G) {
             wp::sync();
-            double tot = 0.0;
-            for (int g = 0; g < G; ++g) tot = wp::dadd(tot, sm->gcost[g]);
+            double tot = tl_from ? sm->tlp[tl_from] : 0.0;
+            for (int g = (int)tl_from; g < G; ++g) {
+                tot = wp::dadd(tot, sm->gcost[g]);
+                if (L == 0) sm->tlp[g + 1] = tot;
+            }
             tl_mean = inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
-            tl_dirty = false;
+            tl_from = (unsigned)G;
+            wp::sync();
         }
         if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && L == 0) {
             tl[2 * n_tl] = now;
