@@ -280,20 +280,21 @@ __device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& 
                                            uint32_t chunks_per, uint32_t n_items, uint32_t items_per) {
     ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
     const uint32_t snap = cu.snap, first = cu.chunk;
-    // ping-pong between two register buffers (no copies on the steady path)
-    ChunkData other;
-    for (;;) {
-        if (score_step<P, LB, DYN>(a, sm, cur, other, cu, acc, first, chunks_per, n_items, items_per)) {
-            cur = other;
-            break;
-        }
-        if (score_step<P, LB, DYN>(a, sm, other, cur, cu, acc, first, chunks_per, n_items, items_per)) break;
+    for (;;) {  // the following chunk loads while this one is scored
+        ChunkData next;
+        const bool done = score_step<P, LB, DYN>(a, sm, cur, next, cu, acc, first, chunks_per, n_items, items_per);
+        cur = next;
+        if (done) break;
     }
     flush_item<LB>(a, acc, snap, first);
 }
 
+// Register-streaming path: the fallback when the snapshot rows are not
+// 16-byte aligned (odd G or an unaligned words pointer) — one pass with the
+// full key, words in registers (the profile-specialised unrolled code needs
+// the whole register file: one block per SM, no spills).
 template <bool LB, bool DYN>
-__global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem sm;
     score_smem_init(sm, a.tables, a.lazymask);
     __syncthreads();
