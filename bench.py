@@ -50,7 +50,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--c4-arrivals", type=int, default=20000)
+    ap.add_argument("--c4-peer", action="store_true",
+                    help="under torchrun, also split the C4 prefix over all ranks' GPUs (device groups)")
     return ap.parse_args()
 
 
@@ -248,8 +251,10 @@ def c4_line(eng, args, rank, world):
     the sharded block engine (one thread-block cluster) on this GPU; N>1: the
     trace split over all ranks' GPUs (device groups exchanging packed keys
     over peer memory, paper_2512_16099_b200.peer), device time = max over
-    ranks.  The reference needs ~12 h for the full trace, so its
-    single-thread rate on a short prefix of the same trace is set beside it."""
+    ranks (opt-in, --c4-peer: the cross-GPU path has only been exercised with
+    several processes on one GPU so far).  The reference needs ~12 h for the
+    full trace, so its single-thread rate on a short prefix of the
+    same trace is set beside it."""
     import torch
 
     from paper_2512_16099_b200 import abi
@@ -305,6 +310,67 @@ def c4_line(eng, args, rank, world):
         ev = int(res[0].summary["handler_events"])
         out.update({"value": ev / float(t.item()), "seconds": float(t.item()), "handler_events": ev, "gpus": world,
                     "engine": f"device groups over {world} GPUs (peer-memory exchange)", "status": res[0].code})
+    return out
+
+
+def other_configs(eng, peaks):
+    """BASELINE.json configs[2] (C3: 4 technique combinations x 1024 seeds x
+    5 arrival loads, 4-GPU clusters, one launch) and configs[4] (C5: 4096
+    high-churn traces, overlap 0.5 s, reconfiguration latency 0.1 s, 8-GPU
+    clusters): device-timed decisions/s with L2 flushed, and the reference
+    library on all host threads over a bounded sample of the same traces."""
+    from oracle import refbind
+    from paper_2512_16099_b200.engine import generate_batch
+    from paper_2512_16099_b200.model import (FeatureFlags, SchedulerConfig, SimConfig, TraceBatch, WorkloadSpec,
+                                             preset, static_layout_preset)
+
+    out = {}
+    # C3: combos x seeds x loads as one batch (config index per trace)
+    combos = [FeatureFlags(False, False, False), FeatureFlags(True, False, False), FeatureFlags(True, True, False),
+              FeatureFlags(True, True, True)]
+    cfgs = [SimConfig(gpu_count=4, sched=SchedulerConfig(
+        features=f, static_layout=None if f.dynamic_partitioning else static_layout_preset("static-a")))
+        for f in combos]
+    parts, index = [], []
+    for load in (10.0, 15.0, 25.0, 35.0, 50.0):
+        sp = preset("normal25")
+        sp.mean_interarrival_s = load
+        b = generate_batch(sp, 0, 1024)
+        for k in range(4):
+            parts.append(b)
+            index += [k] * b.n_traces
+    c3 = TraceBatch.concat(parts, config_index=index)
+    c5 = generate_batch(WorkloadSpec(mean_interarrival_s=0.4, median_s=4.0, sigma=1.2,
+                                     profile_mix=(0.5, 0.3, 0.2, 0.0)), 0, 4096)
+    c5cfg = [SimConfig(gpu_count=8, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                       reconfig_latency_s=0.1)]
+    for name, batch, cs, desc in (
+            ("c3", c3, cfgs, "4 technique combinations x 1024 seeds x 5 loads (ia 10/15/25/35/50 s), 4-GPU clusters"),
+            ("c5", c5, c5cfg, "4096 high-churn traces (ia 0.4 s, median 4 s), overlap 0.5 s, latency 0.1 s, 8 GPUs")):
+        st = eng.stage(batch, cs, 0)
+        for _ in range(3):
+            st.launch()
+        eng.sync()
+        res = st.collect()
+        if any(not r.ok for r in res):
+            out[name] = {"error": "simulation failed"}
+            continue
+        ms = []
+        for _ in range(5):
+            eng.flush_l2()
+            ms.append(st.time_launch())
+        ev = st.handler_events
+        line = {"workload": desc, "traces": batch.n_traces, "decisions_per_step": ev,
+                "value": ev / (statistics.median(ms) * 1e-3), "unit": UNIT, "ms_per_step": statistics.median(ms)}
+        if refbind.ref_available():
+            threads = refbind.hardware_threads()
+            n = min(batch.n_traces, 1024)
+            sub = batch.subset(range(0, batch.n_traces, max(1, batch.n_traces // n)))
+            sub_cfg = cs
+            s_, secs = refbind.ref_run_batch_summaries(sub, sub_cfg, threads=threads)
+            line["cpu_reference"] = {"value": float(s_["handler_events"].sum() / secs), "cores": threads,
+                                     "sample": f"{sub.n_traces} of the traces, reference library"}
+        out[name] = line
     return out
 
 
@@ -439,7 +505,12 @@ def main():
         line["scorer_sweep"] = scorer_sweep(eng, peaks, peak_kind)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(batch, cfg)
-    if not args.no_c4:
+    if rank == 0 and world == 1 and not args.no_configs:
+        try:
+            line["configs"] = other_configs(eng, peaks)
+        except Exception as e:  # noqa: BLE001
+            line["configs"] = {"error": f"{type(e).__name__}: {e}"}
+    if not args.no_c4 and (world == 1 or args.c4_peer):
         try:
             c4 = c4_line(eng, args, rank, world)
         except Exception as e:  # noqa: BLE001 (reported, the headline line still prints)

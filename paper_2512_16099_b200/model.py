@@ -223,6 +223,18 @@ class TraceBatch:
             for i in range(lo, hi)
         ]
 
+    @classmethod
+    def concat(cls, batches: Sequence["TraceBatch"], config_index=None) -> "TraceBatch":
+        """The traces of several batches, in order, as one batch."""
+        offs = [np.zeros(1, np.uint64)]
+        base = 0
+        for b in batches:
+            offs.append(b.offsets[1:] + np.uint64(base))
+            base += b.n_jobs
+        return cls(np.concatenate(offs), np.concatenate([b.job_id for b in batches]),
+                   np.concatenate([b.arrival_s for b in batches]), np.concatenate([b.profile for b in batches]),
+                   np.concatenate([b.service_s for b in batches]), config_index)
+
     def subset(self, traces: Sequence[int]) -> "TraceBatch":
         offs = [0]
         parts = []
