@@ -416,6 +416,14 @@ msg_status msg_schedule_batch(msg_engine* engine, int32_t op, uint32_t n, int32_
  * the profile table).  msg_pack_gpu_word builds it from 8 slots. */
 uint64_t msg_pack_gpu_word(const msg_instance* slots8);
 
+/* frag_cost(gpu) (frag.hpp:40-51, frag.cpp:60-65) for n GPU snapshots of 8
+ * slots each: the exact cost as a numerator over 25200 (every reachable cost
+ * is k/25200) and as the reference's double (k / 25200.0 rounds
+ * like its num/den).  Idle instances do not count; draining ones block
+ * memory.  Either output may be NULL. */
+msg_status msg_frag_cost_batch(msg_engine* engine, uint32_t n, const msg_instance* slots, int32_t* numer_25200,
+                               double* cost);
+
 /* Batched scorer over large clusters (SURVEY §8d roofline path): n
  * snapshots × gpu_count packed words (device pointers, resident in HBM), one
  * job profile per snapshot (device).  d_out (device) receives 2 u64 per

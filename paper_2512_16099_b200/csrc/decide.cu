@@ -45,6 +45,27 @@ static cudaError_t launch_snap_t(const SnapArgs& a, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+// frag_cost (frag.cpp:60-65) of n GPUs from their packed words: the 4-mask
+// cost (busy masks drive the ideal counts, blocked memory the feasible
+// ones) through the exact tables — numerator over 25200 and the double.
+__global__ void frag_cost_kernel(const DevTables* tb, const uint64_t* words, uint32_t n, int32_t* num,
+                                 double* cost) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned w = (unsigned)words[i];
+    const unsigned row = (unsigned)__popc(w & 0x7Fu) * 9u + (unsigned)__popc((w >> 8) & 0xFFu);
+    const unsigned id = tb->cost4pair[tb->idealid[row] * 32u + tb->feasid[(w >> 16) & 0xFFu]];
+    if (num) num[i] = (int32_t)tb->cost4k[id];
+    if (cost) cost[i] = tb->cost4val[id];
+}
+
+cudaError_t launch_frag_cost(const DevTables* tb, const uint64_t* words, uint32_t n, int32_t* num, double* cost,
+                             cudaStream_t stream) {
+    if (!n) return cudaSuccess;
+    frag_cost_kernel<<<(n + 255) / 256, 256, 0, stream>>>(tb, words, n, num, cost);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_snapshot(const SnapArgs& a, cudaStream_t stream) {
     const int G = a.G;
     if (G <= 4) return launch_snap_t<1>(a, stream);

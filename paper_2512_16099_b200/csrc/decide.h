@@ -23,5 +23,7 @@ struct ScoreArgs {
 cudaError_t launch_snapshot(const SnapArgs& a, cudaStream_t stream);
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream);
 size_t score_items_bytes(uint32_t n, uint64_t G);
+cudaError_t launch_frag_cost(const DevTables* tb, const uint64_t* words, uint32_t n, int32_t* num, double* cost,
+                             cudaStream_t stream);
 
 }  // namespace msgk

@@ -137,6 +137,33 @@ msg_status msg_score_device(msg_engine* eng, uint32_t n, int64_t G, const uint64
     return MSG_OK;
 }
 
+// frag_cost(gpu) (frag.cpp:60-65) for n GPU snapshots of 8 slots each.
+msg_status msg_frag_cost_batch(msg_engine* eng, uint32_t n, const msg_instance* slots, int32_t* numer,
+                               double* cost) {
+    if (!eng || (n && !slots)) return MSG_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(eng->device);
+    if (!n) return MSG_OK;
+    std::string err;
+    std::vector<uint64_t> words(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        msg_status e = check_gpu(slots + (size_t)i * 8, &err);
+        if (e != MSG_OK) return fail(eng, e, err);
+        words[i] = msg_pack_gpu_word(slots + (size_t)i * 8);
+    }
+    CK(eng->dscr[9].ensure((size_t)n * 8));
+    CK(eng->dscr[10].ensure((size_t)n * 4));
+    CK(eng->dscr[11].ensure((size_t)n * 8));
+    CK(cudaMemcpyAsync(eng->dscr[9].p, words.data(), (size_t)n * 8, cudaMemcpyHostToDevice, eng->stream));
+    cudaError_t e = launch_frag_cost(eng->tables.as<DevTables>(), eng->dscr[9].as<uint64_t>(), n,
+                                     eng->dscr[10].as<int32_t>(), eng->dscr[11].as<double>(), eng->stream);
+    if (e != cudaSuccess) return cuda_fail(eng, e, "launch_frag_cost");
+    ++eng->launches;
+    if (numer) CK(cudaMemcpyAsync(numer, eng->dscr[10].p, (size_t)n * 4, cudaMemcpyDeviceToHost, eng->stream));
+    if (cost) CK(cudaMemcpyAsync(cost, eng->dscr[11].p, (size_t)n * 8, cudaMemcpyDeviceToHost, eng->stream));
+    CK(cudaStreamSynchronize(eng->stream));
+    return MSG_OK;
+}
+
 msg_status msg_time_score_device(msg_engine* eng, uint32_t n, int64_t G, const uint64_t* d_words,
                                  const uint8_t* d_profile, const msg_sched_config* cfg, uint64_t* d_out, float* ms) {
     if (!eng || !ms) return MSG_ERR_INVALID_ARGUMENT;

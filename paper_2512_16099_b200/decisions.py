@@ -34,6 +34,7 @@ def _bind():
         ("msg_plan_batch", C.c_int, [vp, i32, u32, i32, vp, vp, C.c_double, i32, C.c_double, u32, vp, vp]),
         ("msg_try_dequeue_batch", C.c_int, [vp, u32, i32, vp, vp, vp, vp, vp, vp, vp]),
         ("msg_pack_gpu_word", C.c_uint64, [vp]),
+        ("msg_frag_cost_batch", C.c_int, [vp, u32, vp, vp, vp]),
         ("msg_score_device", C.c_int, [vp, u32, C.c_int64, vp, vp, vp, vp]),
         ("msg_time_score_device", C.c_int, [vp, u32, C.c_int64, vp, vp, vp, vp, C.POINTER(C.c_float)]),
     ):
@@ -276,6 +277,24 @@ def try_dequeue(queue: list, cluster: Cluster, cfg: SchedulerConfig) -> list:
     k = int(n_placed[0])
     del queue[:k]
     return [dict(zip(DEQUEUE_DTYPE.names, (x.item() for x in row))) for row in placed[:k]]
+
+
+def frag_cost_batch(slots: np.ndarray, engine=None):
+    """frag_cost(gpu) (frag.cpp:60-65) of n GPU snapshots (slots shape (n, 8)
+    INSTANCE_DTYPE) on the device: (numerators over 25200, doubles)."""
+    L = _bind()
+    eng = engine or default_engine()
+    slots = np.ascontiguousarray(slots, abi.INSTANCE_DTYPE).reshape(-1, 8)
+    n = len(slots)
+    num = np.zeros(n, np.int32)
+    cost = np.zeros(n, np.float64)
+    _check(L.msg_frag_cost_batch(eng._h, n, slots.ctypes.data, num.ctypes.data, cost.ctypes.data), eng)
+    return num, cost
+
+
+def frag_cost(cluster: Cluster, gpu: int) -> float:
+    """migsched::frag_cost of one GPU of a cluster snapshot."""
+    return float(frag_cost_batch(cluster.slots[8 * gpu:8 * gpu + 8])[1][0])
 
 
 def pack_gpu_word(slots8: np.ndarray) -> int:

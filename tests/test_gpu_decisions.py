@@ -259,3 +259,38 @@ def test_try_dequeue_random(d):
         assert st == 0
         assert placed == ref_placed
         assert normalize_slots(c.slots) == normalize_slots(ref_slots)
+
+
+def test_frag_cost_known_answers_and_random_gpus(d):
+    """frag_cost on the device (msg_frag_cost_batch) — the reference's
+    known answers (test_frag_metric.cpp:43-93) and random GPUs with busy,
+    idle and draining instances against frag_cost_masks."""
+    from paper_2512_16099_b200.model import COMPUTE_SLICES, MEMORY_SLICES
+
+    c = d.Cluster(1)
+    assert d.frag_cost(c, 0) == 0.0                       # empty
+    c.add_busy(0, 2, 0, 1)
+    assert d.frag_cost(c, 0) == 0.35                      # 3g@0
+    c = d.Cluster(1)
+    c.add_busy(0, 3, 2, 1)
+    c.add_idle(0, 3, 4)
+    c.add_idle(0, 5, 0)
+    assert d.frag_cost(c, 0) == 0.2                       # 2g@2 (+ idle instances: no effect)
+    rng = np.random.default_rng(11)
+    snaps = np.stack([random_cluster(rng, 1, fill=6) for _ in range(3000)])
+    num, cost = d.frag_cost_batch(snaps)
+    for i, s8 in enumerate(snaps):
+        bc = bm = kc = km = 0
+        for st in range(8):
+            x = s8[st]
+            if x["profile"] < 0 or x["state"] == abi.SLOT_IDLE or x["state"] == abi.SLOT_EMPTY:
+                continue
+            mc = ((1 << COMPUTE_SLICES[x["profile"]]) - 1) << st
+            mm = ((1 << MEMORY_SLICES[x["profile"]]) - 1) << st
+            kc |= mc
+            km |= mm
+            if x["state"] == abi.SLOT_BUSY:
+                bc |= mc
+                bm |= mm
+        n_, den = rb.ref_frag_cost(bc, bm, kc, km)
+        assert cost[i] == n_ / den and num[i] * den == n_ * 25200, i
