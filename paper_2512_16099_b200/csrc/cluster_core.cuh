@@ -263,6 +263,7 @@ struct ClusterSim {
     // returns the same reduced record.  Deferred timeline samples ride along.
     MSG_DI void exchange(XRec& r) {
         if (NS == 1) return;
+        wp::sync();  // warp 0's lanes see thread 0's deferred samples
         r.ks[0] = npend > 0 ? sc->pend_k[0] : 0ull;
         r.ks[1] = npend > 1 ? sc->pend_k[1] : 0ull;
         const unsigned par = xround & 1u, use = xround >> 1;
@@ -555,7 +556,8 @@ struct ClusterSim {
 #pragma unroll 4
         for (uint32_t i = T; i < n_act; i += NT)
             if (ast[i] == ST_RUN) arem[i] = wp::dsub(arem[i], sc->q[w_k(W_(aslot[i] >> 3)) - 1]);
-        wp::bsync();
+        // no trailing barrier: every reader of arem starts with one, and
+        // reschedule revisits entry i on the same thread
     }
 
     MSG_DI void reschedule() {  // sim.cpp:167-175
@@ -568,7 +570,8 @@ struct ClusterSim {
                 atkey[i] = wp::dadd(now, wp::dmul(r, sc->f[w_k(W_(aslot[i] >> 3)) - 1]));
             }
         }
-        wp::bsync();
+        // no trailing barrier: next_event scans entry i on the same thread and
+        // starts with one before any cross-thread read
     }
 
     MSG_DI void record_sample(double t, unsigned long long ktot) {
@@ -584,13 +587,11 @@ struct ClusterSim {
 
     MSG_DI void sample() {  // sim.cpp:177-181
         if (NS > 1) {  // deferred: the next exchange sums the shards' parts
-            wp::bsync();
-            if (T == 0) {
+            if (T == 0) {  // thread 0 also keeps ksum (refresh_gpu): no barrier needed here
                 sc->pend_t[npend] = now;
                 sc->pend_k[npend] = sc->ksum;
             }
             ++npend;
-            wp::bsync();
             return;
         }
         if (tl_dirty) {
@@ -743,8 +744,14 @@ struct ClusterSim {
         block_lexmin(hi, lo, z0, z1, pay);
         NL = NB = 0;
         if (lb) {
-            NL = block_sum(nl);
-            NB = block_sum(nb);
+            if ((g_hi - g_lo) * 7 < 65536) {  // both counts in one reduction
+                const unsigned x = block_sum(nl | (nb << 16));
+                NL = x & 0xFFFFu;
+                NB = x >> 16;
+            } else {
+                NL = block_sum(nl);
+                NB = block_sum(nb);
+            }
         }
         key = ((uint64_t)hi << 32) | lo;
     }

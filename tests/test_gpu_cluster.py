@@ -57,3 +57,53 @@ def test_c4_prefix_16384_gpus(engine):
     sp.mean_interarrival_s = 25.0 / 2048
     sp.job_count = 600
     _check(engine, rb.ref_generate_batch(sp, [0]), [SimConfig(gpu_count=16384)], relaxed=True)
+
+
+def _no_events(results):
+    for r in results:
+        r.events = None
+    return results
+
+
+def test_c4_prefix_sharded_cluster_matches_reference(engine, monkeypatch):
+    """Without the event log the 16384-GPU trace runs on a 16-CTA cluster
+    (GPU-range shards exchanging packed keys over DSMEM): the reference's
+    results on a prefix, and bit-identical to one CTA on a longer one."""
+    sp = preset("normal25")
+    sp.mean_interarrival_s = 25.0 / 2048
+    sp.job_count = 600
+    b = rb.ref_generate_batch(sp, [0])
+    cfg = [SimConfig(gpu_count=16384)]
+    ref = _no_events(rb.ref_run_batch_results(b, cfg))
+    got = engine.run_batch(b, cfg, abi.OUT_JOBS | abi.OUT_TIMELINE)
+    bad = [d for r, g in zip(ref, got) if (d := diff_results_relaxed_timeline(r, g))]
+    assert not bad, bad
+    sp.job_count = 4000
+    b = rb.ref_generate_batch(sp, [0])
+    sharded = engine.run_batch(b, cfg, abi.OUT_JOBS | abi.OUT_TIMELINE)[0]
+    monkeypatch.setenv("MSG_SHARDS", "1")
+    one = engine.run_batch(b, cfg, abi.OUT_JOBS | abi.OUT_TIMELINE)[0]
+    assert sharded.summary.tobytes() == one.summary.tobytes()
+    assert sharded.per_job.tobytes() == one.per_job.tobytes()
+    assert sharded.frag_timeline.tobytes() == one.frag_timeline.tobytes()
+
+
+@pytest.mark.parametrize("shards,groups", [(4, 2), (2, 4), (8, 2)])
+def test_device_groups_on_one_gpu(engine, monkeypatch, shards, groups):
+    """The multi-GPU protocol (device groups exchanging stamped records
+    through global-memory inboxes) with all groups as clusters of this GPU:
+    the reference's results (timeline to 1e-9)."""
+    monkeypatch.setenv("MSG_SHARDS", str(shards))
+    monkeypatch.setenv("MSG_VDEV", str(groups))
+    sp = preset("normal25")
+    sp.mean_interarrival_s = 25.0 / 256
+    sp.job_count = 800
+    churn = WorkloadSpec(mean_interarrival_s=0.4 / 256, median_s=4.0, sigma=1.2, job_count=800)
+    for spec, cfg in ((sp, SimConfig(gpu_count=2048)),
+                      (churn, SimConfig(gpu_count=2048, sched=SchedulerConfig(threshold=0.3), migration_overlap_s=0.5,
+                                        reconfig_latency_s=0.1))):
+        b = rb.ref_generate_batch(spec, [3])
+        ref = _no_events(rb.ref_run_batch_results(b, [cfg]))
+        got = engine.run_batch(b, [cfg], abi.OUT_JOBS | abi.OUT_TIMELINE)
+        bad = [d for r, g in zip(ref, got) if (d := diff_results_relaxed_timeline(r, g))]
+        assert not bad, bad
