@@ -401,23 +401,6 @@ struct TraceSim {
         }
     }
 
-    // reschedule_completions (sim.cpp:167-175): prediction now + max(rem,0)*f.
-    MSG_DI void reschedule() {
-        wp::sync();
-#pragma unroll
-        for (int i = 0; i < SPL; ++i) {
-            const int slot = L + 32 * i;
-            const bool run = sm->st[slot] == ST_RUN;
-            const unsigned k = run ? w_k(sm->gw[slot >> 3]) : 1u;
-            const double f = wp::shfl(my_f, (int)k - 1);
-            if (run) {
-                double r = sm->rem[slot];
-                if (r < 0.0) r = 0.0;  // std::max(rem, 0.0)
-                sm->tkey[slot] = wp::dadd(now, wp::dmul(r, f));
-            }
-        }
-    }
-
     // sample_timeline (sim.cpp:177-181): sequential sum in GPU order / G.
     // The running prefix sums are kept, so after a change on GPU g only the
     // tail g .. G-1 of the chain is re-added (same additions, same order).
@@ -442,20 +425,36 @@ struct TraceSim {
     }
 
     // -------------------------------------------------------------- events
-    // Next timer pop; returns -1 none, 0 completion, 1 migration end,
-    // 2 service start, 3 arrival.
-    MSG_DI int next_event(int& ev_slot) {
+    // reschedule_completions (sim.cpp:167-175) fused with the next timer pop
+    // (Engine::execute, sim.cpp:123-141): every Running slot's prediction
+    // now + max(rem,0)*f is recomputed and stored, and the same pass forms
+    // the (time, kind, job, push seq) keys of all armed timers.  Returns -1
+    // none, 0 completion, 1 migration end, 2 service start, 3 arrival.
+    MSG_DI int resched_next(int& ev_slot) {
         wp::sync();
         unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
         int bsl = -1;
+        double bt = 0.0;
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
             const uint8_t s = sm->st[slot];
+            const bool run = s == ST_RUN;
+            const unsigned k = run ? w_k(sm->gw[slot >> 3]) : 1u;
+            const double f = wp::shfl(my_f, (int)k - 1);
             if (s >= ST_RUN) {
-                const uint64_t tk = time_key(sm->tkey[slot]);
+                double t;
+                if (run) {
+                    double r = sm->rem[slot];
+                    if (r < 0.0) r = 0.0;  // std::max(rem, 0.0)
+                    t = wp::dadd(now, wp::dmul(r, f));
+                    sm->tkey[slot] = t;
+                } else {
+                    t = sm->tkey[slot];
+                }
+                const uint64_t tk = time_key(t);
                 const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;
-                const unsigned kind = s == ST_RUN ? 0u : (s == ST_DRAIN ? 1u : 2u);
+                const unsigned kind = run ? 0u : (s == ST_DRAIN ? 1u : 2u);
                 const unsigned tie = (kind << 28) | (unsigned)sm->job[slot];
                 const unsigned ms = s == ST_DRAIN ? sm->mseq[slot] : 0u;
                 const bool better =
@@ -467,6 +466,7 @@ struct TraceSim {
                     btie = tie;
                     bms = ms;
                     bsl = slot;
+                    bt = t;
                 }
             }
         }
@@ -493,7 +493,7 @@ struct TraceSim {
         }
         const int wl = wp::ffs(wp::ballot(match)) - 1;
         ev_slot = wp::shfl(bsl, wl);
-        now = sm->tkey[ev_slot];
+        now = wp::shfl(bt, wl);
         return (int)(mtie >> 28);
     }
 
@@ -882,14 +882,13 @@ struct TraceSim {
     MSG_DI void run() {  // Engine::execute (sim.cpp:123-141)
         for (;;) {
             int slot = -1;
-            const int kind = next_event(slot);
+            const int kind = resched_next(slot);  // reschedules the previous handler's completions
             if (kind < 0) break;
             ++n_handler;
             advance_all();
             if (kind == 3) handle_arrival();
             else if (kind == 2) handle_service_start(slot);
             else handle_departure(slot, kind == 0);
-            reschedule();
             sample();
         }
     }

@@ -192,14 +192,17 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
             return MSG_ERR_INVALID_ARGUMENT;
         }
     }
-    parallel_for(s->n_in, 64, [&](uint32_t t) {
+    // defer_arrays (the pipelined path): only config errors here; each
+    // trace is checked by run_pipelined just before its chunk is staged,
+    // and a failing one keeps its (unused) slot in the layout.
+    parallel_for(s->n_in, defer_arrays ? 4096 : 64, [&](uint32_t t) {
         const uint32_t ci = b->config_index ? b->config_index[t] : 0;
         if (cs[ci].status != MSG_OK) {
             checks[t].status = cs[ci].status;
             checks[t].message = cs[ci].message;
             return;
         }
-        checks[t] = check_trace(b, t);
+        if (!defer_arrays) checks[t] = check_trace(b, t);
     });
 
     pt.mark("  validate");
@@ -260,7 +263,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     CK(s->h_service.ensure(N * sizeof(double)));
     CK(s->h_profile.ensure(N));
     CK(s->h_ids.ensure(N * sizeof(int64_t)));
-    bool any_perm = false;
+    bool any_perm = defer_arrays;  // deferred checks: identity order is not known yet
     for (auto& tr : s->traces) any_perm |= tr.has_perm != 0;
     s->any_perm = any_perm;
     if (any_perm) CK(s->h_perm.ensure(N * sizeof(uint32_t)));
@@ -314,7 +317,7 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         CK(cudaMemcpyAsync(s->d_profile.p, hp, njobs, cudaMemcpyHostToDevice, st));
         if (any_perm) CK(cudaMemcpyAsync(s->d_perm.p, hperm, njobs * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     }
-    if (!s->traces.empty())
+    if (!s->traces.empty() && !defer_arrays)
         CK(cudaMemcpyAsync(s->d_traces.p, s->traces.data(), s->traces.size() * sizeof(DevTrace),
                            cudaMemcpyHostToDevice, st));
     if (!s->configs.empty())
@@ -587,13 +590,41 @@ msg_status collect_impl(msg_engine* eng, msg_staged* s, msg_batch_result** out) 
 
 // ---- pipelined msg_run_batch for large ensembles ---------------------------
 // Summary / job-row output over many small-cluster traces: the batch is cut
-// into kPipeChunks trace ranges, each on its own stream — host staging of
+// into trace ranges (pipe_bounds), each on its own stream — host staging of
 // chunk k+1 overlaps the H2D + kernel of chunk k, and the D2H + decode of
 // the first chunks overlap the kernels of the last.  The chunk kernels run
 // concurrently (one warp per trace, latency-bound), so the wall time is
 // close to validation + one chunk's staging + the kernel + one chunk's
 // readback.
-constexpr int kPipeChunks = 4;  // == size of msg_engine::pstream
+constexpr int kMaxPipeChunks = 8;  // == size of msg_engine::pstream
+
+// Chunk boundaries over the device traces: relative chunk weights from
+// MSG_PIPE_W ("1,2,2,3"; tuning), else kDefaultPipe equal chunks.
+constexpr int kDefaultPipe = 4;
+int pipe_bounds(uint32_t T, uint32_t* d0s) {
+    double w[kMaxPipeChunks];
+    int n = 0;
+    if (const char* e = std::getenv("MSG_PIPE_W")) {
+        const char* c = e;
+        while (*c && n < kMaxPipeChunks) {
+            char* end = nullptr;
+            const double v = std::strtod(c, &end);
+            if (end == c) break;
+            if (v > 0) w[n++] = v;
+            c = *end == ',' ? end + 1 : end;
+        }
+    }
+    if (n == 0)
+        for (n = 0; n < kDefaultPipe; ++n) w[n] = 1.0;
+    double tot = 0, acc = 0;
+    for (int k = 0; k < n; ++k) tot += w[k];
+    d0s[0] = 0;
+    for (int k = 0; k < n; ++k) {
+        acc += w[k];
+        d0s[k + 1] = k + 1 == n ? T : (uint32_t)std::min<double>(T, std::floor(T * acc / tot));
+    }
+    return n;
+}
 
 void fill_summary(msg_trace_summary& o, const DevTrace& tr, const DevSummary& x) {
     o.status = x.status;
@@ -619,7 +650,9 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     const uint32_t T = (uint32_t)s->traces.size();
     const bool want_jobs = (s->out_flags & MSG_OUT_JOBS) != 0;
     PhaseTimer pt;
-    for (int k = 0; k < kPipeChunks; ++k) {
+    uint32_t d0s[kMaxPipeChunks + 1];
+    const int n_chunks = pipe_bounds(T, d0s);
+    for (int k = 0; k < n_chunks; ++k) {
         if (!eng->pstream[k]) CK(cudaStreamCreateWithFlags(&eng->pstream[k], cudaStreamNonBlocking));
         if (!eng->pevent[k]) CK(cudaEventCreateWithFlags(&eng->pevent[k], cudaEventDisableTiming));
     }
@@ -632,23 +665,38 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     int64_t* hid = s->h_ids.as<int64_t>();
     uint32_t* hperm = s->any_perm ? s->h_perm.as<uint32_t>() : nullptr;
     SimArgs a = make_args(eng, s);
-    uint32_t d0s[kPipeChunks + 1];
-    for (int k = 0; k <= kPipeChunks; ++k) d0s[k] = (uint32_t)((uint64_t)T * k / kPipeChunks);
     auto joff = [&](uint32_t d) { return d < T ? s->traces[d].job_off : s->n_jobs; };
-    for (int k = 0; k < kPipeChunks; ++k) {
+    for (int k = 0; k < n_chunks; ++k) {
         const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
         if (d0 == d1) continue;
         cudaStream_t st = eng->pstream[k];
+        // Check (sim.cpp:97-116) and stage each trace of the chunk while its
+        // inputs are hot; a failing trace runs as an empty one and is
+        // reported from its check.
+        std::atomic<uint32_t> n_perm{0};
         parallel_for(d1 - d0, 32, [&](uint32_t i) {
-            const uint32_t d = d0 + i;
-            stage_trace_arrays(b, s->src_of[d], s->traces[d], ha, hs, hp, hid, hperm);
+            const uint32_t d = d0 + i, t = s->src_of[d];
+            DevTrace& tr = s->traces[d];
+            TraceCheck c = check_trace(b, t);
+            if (c.status != MSG_OK) {
+                s->status[t] = c.status;
+                s->message[t] = std::move(c.message);
+                tr.n_jobs = 0;
+                tr.has_perm = 0;
+                return;
+            }
+            tr.has_perm = c.identity ? 0 : 1;
+            if (tr.has_perm) n_perm.fetch_add(1, std::memory_order_relaxed);
+            stage_trace_arrays(b, t, tr, ha, hs, hp, hid, hperm);
         });
+        CK(cudaMemcpyAsync(s->d_traces.as<DevTrace>() + d0, s->traces.data() + d0, (d1 - d0) * sizeof(DevTrace),
+                           cudaMemcpyHostToDevice, st));
         const uint64_t j0 = joff(d0), j1 = joff(d1), nj = j1 - j0;
         if (nj) {
             CK(cudaMemcpyAsync(s->d_arrival.as<double>() + j0, ha + j0, nj * sizeof(double), cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(s->d_service.as<double>() + j0, hs + j0, nj * sizeof(double), cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(s->d_profile.as<uint8_t>() + j0, hp + j0, nj, cudaMemcpyHostToDevice, st));
-            if (hperm)
+            if (n_perm.load())
                 CK(cudaMemcpyAsync(s->d_perm.as<uint32_t>() + j0, hperm + j0, nj * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, st));
         }
@@ -691,13 +739,14 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     const JobOut* hj = s->h_jobs.as<JobOut>();
     std::atomic<uint64_t> handler{0};
     std::atomic<bool> pending{false};
-    for (int k = 0; k < kPipeChunks; ++k) {
+    for (int k = 0; k < n_chunks; ++k) {
         const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
         if (d0 == d1) continue;
         CK(cudaEventSynchronize(eng->pevent[k]));
         pt.mark("  chunk kernel+D2H done");
         parallel_for(d1 - d0, 64, [&](uint32_t i) {
             const uint32_t d = d0 + i, t = s->src_of[d];
+            if (s->status[t] != MSG_OK) return;  // failed its check: reported as such, no rows
             const DevTrace& tr = s->traces[d];
             const DevSummary& x = ds[d];
             msg_trace_summary& o = res->summaries[t];
@@ -784,7 +833,7 @@ void msg_engine_destroy(msg_engine* e) {
     if (e->stream) cudaStreamSynchronize(e->stream);
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 8; ++k) {
         if (e->pstream[k]) {
             cudaStreamSynchronize(e->pstream[k]);
             cudaStreamDestroy(e->pstream[k]);

@@ -181,8 +181,8 @@ struct msg_engine {
     int sm_count = 0;
     char name[256] = {0};
     msg_staged* cached = nullptr;
-    cudaStream_t pstream[4] = {};  // pipelined msg_run_batch (host_runtime.cpp, run_pipelined)
-    cudaEvent_t pevent[4] = {};
+    cudaStream_t pstream[8] = {};  // pipelined msg_run_batch (host_runtime.cpp, run_pipelined)
+    cudaEvent_t pevent[8] = {};
     msgk::DevBuf dscr[12];  // decision-level scratch (host_decide.cpp)
     msgk::HostBuf hscr[4];
 };

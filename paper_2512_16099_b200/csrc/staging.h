@@ -96,6 +96,29 @@ inline TraceCheck check_trace(const msg_trace_batch* b, uint32_t t) {
     TraceCheck r;
     const uint64_t lo = b->offsets[t], hi = b->offsets[t + 1];
     const uint64_t n = hi - lo;
+    {
+        // Fast pass, no early exit (vectorisable): any bad profile, unsorted
+        // or NaN arrival, non-positive or NaN service, non-increasing ids.
+        // A clean trace returns here; anything else takes the exact pass
+        // below, which finds the first failure and its message.
+        const int32_t* pf = b->profile + lo;
+        const double* ar = b->arrival_s + lo;
+        const double* sv = b->service_s + lo;
+        const int64_t* id = b->job_id + lo;
+        unsigned bad = 0, dec = 0;
+        if (n) bad |= (unsigned)pf[0] >= (unsigned)MSG_PROFILE_COUNT || !(ar[0] >= -1.0) || !(sv[0] > 0.0);
+        for (uint64_t i = 1; i < n; ++i) {
+            bad |= ((unsigned)pf[i] >= (unsigned)MSG_PROFILE_COUNT) | !(ar[i] >= ar[i - 1]) | !(sv[i] > 0.0);
+            dec |= id[i] <= id[i - 1];
+        }
+        if (!bad && !dec) {
+            if (n >= kMaxJobsPerTrace) {
+                r.status = MSG_ERR_UNSUPPORTED;
+                r.message = "Unsupported: at most 2^22 - 1 jobs per trace";
+            }
+            return r;
+        }
+    }
     // First failing job in trace order; at one job the checks run in the
     // reference's order: profile, sortedness, service, duplicate id.
     uint64_t bad_idx = n;

@@ -193,6 +193,9 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
     traces[5] = [Job(0, 10.0, 5, 1.0), Job(1, 5.0, 5, 1.0)]  # TraceUnsorted
     traces[300] = [Job(0, 0.0, 0, 10.0)]  # 1g.5gb on a static 2g-only layout, no repartitioning: JobsPending
     traces[599] = []
+    traces[7] = [Job(5, 0.0, 5, 2.0), Job(3, 1.0, 4, 1.0), Job(4, 1.0, 5, 3.0), Job(-2, 1.0, 0, 0.5)]  # rank != order
+    traces[400] = [Job(1, 0.0, 5, 1.0), Job(2, 1.0, 5, 1.0), Job(1, 2.0, 5, 1.0)]  # duplicate id
+    traces[450] = [Job(1, 0.0, 5, 1.0), Job(2, 1.0, 5, 0.0)]  # non-positive service
     cfgs = [SimConfig(gpu_count=8),
             SimConfig(gpu_count=1, sched=SchedulerConfig(features=FeatureFlags(True, False, True),
                                                          static_layout=[[(2, 0), (2, 4)]]))]
@@ -205,6 +208,7 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
     assert piped.jobs.tobytes() == plain.jobs.tobytes()
     assert np.array_equal(piped.job_offsets, plain.job_offsets)
     assert piped[300].code == "JobsPending" and piped[5].code == "TraceUnsorted"
+    assert piped[400].code == "BadSpec" and piped[450].code == "BadSpec" and piped[7].ok
     bad = []
     for t, (r, g) in enumerate(zip(ref, piped)):
         r.events = r.frag_timeline = None
