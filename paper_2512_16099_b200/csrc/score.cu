@@ -508,6 +508,8 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
     TmaSmem sm{tables, reinterpret_cast<uint64_t(*)[kChunk]>(ring),
                reinterpret_cast<uint64_t*>(ring + sizeof(uint64_t) * kChunk * kStages),
                reinterpret_cast<StageMeta*>(ring + sizeof(uint64_t) * kChunk * kStages + 8 * kStages)};
+    // the merge kernel may launch now: it waits for this grid (griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;");
     score_smem_init(sm.t, a.tables, a.lazymask);
     const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
     const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
@@ -615,6 +617,7 @@ __device__ __forceinline__ void busy_item(const ScoreArgs& a, const ScoreSmem& s
 template <bool DYN>
 __global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem sm;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of score_reduce_kernel
     const uint32_t* list = a.scratch + a.n + 1;  // score_reduce_kernel
     const uint32_t need = *(volatile const uint32_t*)(a.scratch + a.n);
     if (need == 0) return;
@@ -633,6 +636,8 @@ __global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) 
 // without a Lazy candidate are listed for pass 2 (scratch[n] = count, then
 // the list; the order is irrelevant, every pass-2 block reads the same list).
 __global__ void score_reduce_kernel(ScoreArgs a, uint32_t items_per) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of pass 1
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= a.n) return;
     uint64_t best = ~0ull, cnt = 0;
@@ -701,11 +706,27 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         case 6: score_tma_kernel<true, false><<<grid, block, kTmaDynBytes, stream>>>(a); break;
         default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
     }
-    if (tma) score_reduce_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(a, (uint32_t)(items / a.n));
-    if (tma && a.lb) {  // pass 2: snapshots without a Lazy candidate
-        const dim3 g2((unsigned)std::min<uint64_t>(items, (uint64_t)sms * 4));
-        if (a.dyn) score_busy_kernel<true><<<g2, block, 0, stream>>>(a);
-        else score_busy_kernel<false><<<g2, block, 0, stream>>>(a);
+    if (!tma) return cudaGetLastError();
+    // The merge and pass 2 launch as programmatic dependents: their launch
+    // overlaps the previous kernel's tail; griddepcontrol.wait in each holds
+    // its reads until the previous grid has completed.
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t lc{};
+    lc.stream = stream;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    lc.gridDim = dim3((a.n + 255) / 256);
+    lc.blockDim = dim3(256);
+    cudaError_t e = cudaLaunchKernelEx(&lc, score_reduce_kernel, a, (uint32_t)(items / a.n));
+    if (e != cudaSuccess) return e;
+    if (a.lb) {  // pass 2: snapshots without a Lazy candidate
+        lc.gridDim = dim3((unsigned)std::min<uint64_t>(items, (uint64_t)sms * 4));
+        lc.blockDim = block;
+        e = a.dyn ? cudaLaunchKernelEx(&lc, score_busy_kernel<true>, a)
+                  : cudaLaunchKernelEx(&lc, score_busy_kernel<false>, a);
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }

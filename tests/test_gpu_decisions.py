@@ -222,6 +222,31 @@ def test_schedule_random_clusters(d, G):
             assert got.tobytes() == want.tobytes(), (op, thr, lb, dyn)
 
 
+@pytest.mark.parametrize("G", [9000, 16386])
+def test_schedule_multi_item_snapshots(d, G):
+    """Snapshots longer than one scorer item (4 chunks of 2048 GPUs): 9000
+    GPUs = 2 items, 16386 = 3 items with a 2-GPU tail; the snapshot's last
+    item to finish merges them.  Configs alternate so consecutive launches
+    exercise both pass-2 list counters, and the register path (an odd
+    count, G + 1) runs between them."""
+    rng = np.random.default_rng(G)
+    n = 6
+    snaps = np.stack([random_cluster(rng, G) for _ in range(n)])
+    profs = rng.integers(0, 6, n)
+    odd = np.stack([random_cluster(rng, G + 1) for _ in range(2)])
+    for rep in range(2):
+        for thr, lb, dyn in ((0.4, True, True), (0.0, True, False), (1.0, False, True), (0.0, True, True),
+                             (0.6, True, True)):
+            cfg = SchedulerConfig(threshold=thr, features=FeatureFlags(lb, dyn, True))
+            got = d.schedule_batch(abi.OP_SCHEDULE, snaps, profs, cfg, G)
+            want = _ref_sched_all(abi.OP_SCHEDULE, snaps, profs, threshold=thr, lb=lb, dyn=dyn)
+            assert got.tobytes() == want.tobytes(), (rep, thr, lb, dyn)
+            if rep == 1 and thr == 0.0:
+                got = d.schedule_batch(abi.OP_SCHEDULE, odd, profs[:2], cfg, G + 1)
+                want = _ref_sched_all(abi.OP_SCHEDULE, odd, profs[:2], threshold=thr, lb=lb, dyn=dyn)
+                assert got.tobytes() == want.tobytes(), ("odd", thr, lb, dyn)
+
+
 @pytest.mark.parametrize("G", [2, 3, 8, 17])
 def test_planners_random_clusters(d, G):
     rng = np.random.default_rng(100 + G)
