@@ -124,6 +124,19 @@ def profile_traffic(name):
         return None
 
 
+def profile_issue(name):
+    """Issue-side ncu metrics of a kernel from the committed summary (the
+    event loop's bound: issue slots, occupancy, active threads per warp)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f).get(name, {})
+        return {"issue_slots_busy_pct": d["issue_slots_busy_pct"], "achieved_occupancy_pct": d["achieved_occupancy_pct"],
+                "threads_per_warp_instr": d["warp_execution_efficiency_threads"],
+                "top_stalls_per_issue": d["top_stalls_per_issue"], "source": d["round"]}
+    except Exception:
+        return None
+
+
 def workload(rank):
     """This rank's shard of the C2 ensemble (weak scaling: TRACES_RUN seeds per
     rank, paper_2512_16099_b200.ensemble.rank_seeds)."""
@@ -498,7 +511,9 @@ def main():
         "roofline": {"kernel": "sim_kernel", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "peak_kind": peak_kind,
                      "traffic": profile_traffic("sim_kernel"),
-                     "note": "event loop is a serial dependent chain per trace (latency-bound); see scorer_sweep"},
+                     "note": "event loop is a serial dependent chain per trace: latency/issue-bound, the HBM "
+                             "fraction is not its bound (SURVEY 8d); see issue and scorer_sweep",
+                     "issue": profile_issue("sim_kernel")},
         "clocks": clk,
     }
     if rank == 0 and not args.no_sweep:
