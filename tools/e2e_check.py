@@ -1,13 +1,26 @@
-import os, sys, time, gc
-sys.path.insert(0, "/root/repo")
+"""e2e msg_run_batch timing in isolation (development aid): result held vs
+dropped, with and without torch's CUDA runtime initialised first."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if "torch" in sys.argv[1:]:
+    import torch
+    torch.cuda.set_device(0)
+    x = torch.ones(1 << 20, device="cuda")
+    torch.cuda.synchronize()
 from paper_2512_16099_b200 import abi
 from paper_2512_16099_b200.engine import Engine, generate_batch
 from paper_2512_16099_b200.model import SimConfig, preset
 eng = Engine(0)
 b = generate_batch(preset("normal25"), 0, 4096)
 cfg = [SimConfig(gpu_count=8)]
+if "staged" in sys.argv[1:]:  # what bench.py does first: a staged copy, timed launches with L2 flushes
+    st = eng.stage(b, cfg, 0)
+    for _ in range(13):
+        eng.flush_l2()
+        st.time_launch()
 for mode in ("hold", "drop", "hold", "drop"):
-    for _ in range(3): out = eng.run_batch(b, cfg, abi.OUT_JOBS)
+    for _ in range(3):
+        out = eng.run_batch(b, cfg, abi.OUT_JOBS)
     ts = []
     for _ in range(15):
         t0 = time.perf_counter()
@@ -18,4 +31,5 @@ for mode in ("hold", "drop", "hold", "drop"):
         ts.append(time.perf_counter() - t0)
     out = None
     s = sorted(ts)
-    print(mode, "mean %.3f median %.3f min %.3f max %.3f" % (1e3*sum(ts)/len(ts), 1e3*s[7], 1e3*s[0], 1e3*s[-1]))
+    print(sys.argv[1:], mode, "mean %.3f median %.3f min %.3f max %.3f" % (1e3 * sum(ts) / len(ts), 1e3 * s[7],
+                                                                          1e3 * s[0], 1e3 * s[-1]))
