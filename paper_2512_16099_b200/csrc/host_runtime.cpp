@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <immintrin.h>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -150,6 +151,35 @@ inline void put_row(msg_job_row* dst, int64_t id, double arrival, const JobOut& 
     row.gpu = j.gpu;
     row.migrations = j.mig;
     row.reserved0 = 0;
+}
+
+// A trace's rows, written with non-temporal 16-byte stores in pairs (144 B
+// = 9 aligned vectors): the row buffer is far larger than the caches and is
+// not read back here, so the stores skip the read-for-ownership.
+// MSG_ROWS_NT=0 writes them with plain stores.
+inline void put_rows(msg_job_row* rows, uint32_t n, const int64_t* ids, const double* ha, const JobOut* hj,
+                     const uint8_t* hp) {
+    static const bool nt = [] {
+        const char* e = std::getenv("MSG_ROWS_NT");
+        return !(e && e[0] == '0');
+    }();
+    uint32_t r = 0;
+    if (nt) {
+        if (n && (reinterpret_cast<uintptr_t>(rows) & 15)) {
+            put_row(rows, ids[0], ha[0], hj[0], hp[0]);
+            r = 1;
+        }
+        for (; r + 2 <= n; r += 2) {
+            alignas(16) msg_job_row tmp[2];
+            put_row(tmp, ids[r], ha[r], hj[r], hp[r]);
+            put_row(tmp + 1, ids[r + 1], ha[r + 1], hj[r + 1], hp[r + 1]);
+            const __m128i* src = reinterpret_cast<const __m128i*>(tmp);
+            __m128i* dst = reinterpret_cast<__m128i*>(rows + r);
+            for (int k = 0; k < 9; ++k) _mm_stream_si128(dst + k, _mm_load_si128(src + k));
+        }
+    }
+    for (; r < n; ++r) put_row(rows + r, ids[r], ha[r], hj[r], hp[r]);
+    if (nt) _mm_sfence();
 }
 
 msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
@@ -760,9 +790,8 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
                 return;
             }
             if (!want_jobs) return;
-            msg_job_row* rows = res->jobs.p.get() + res->job_off[t];
-            for (uint32_t r = 0; r < tr.n_jobs; ++r)
-                put_row(rows + r, ids[r], ha[tr.job_off + r], hj[tr.job_off + r], hp[tr.job_off + r]);
+            put_rows(res->jobs.p.get() + res->job_off[t], tr.n_jobs, ids, ha + tr.job_off, hj + tr.job_off,
+                     hp + tr.job_off);
         });
         pt.mark("  chunk decoded");
     }
