@@ -71,6 +71,17 @@
 
 namespace msgk {
 
+#ifdef MSG_PHASE_PROF
+// Development build only (tools/c4_phases.sh): SM cycles per phase of the
+// event loop on CTA 0 of group 0 — 0 timer scan, 1 speculative placement
+// search, 2 exchanges, 3 advance, 4 arrival, 5 departure, 6 service start,
+// 7 reschedule + sample; [8] exchanges, [9] events.
+__device__ unsigned long long g_phase[16];
+#define MSG_PH(k) ph_mark(k)
+#else
+#define MSG_PH(k) ((void)0)
+#endif
+
 struct BlockScratch {
     unsigned hi[2][32], lo[2][32], tie[2][32], ms[2][32];
     int pay[2][32];
@@ -263,6 +274,10 @@ struct ClusterSim {
     // returns the same reduced record.  Deferred timeline samples ride along.
     MSG_DI void exchange(XRec& r) {
         if (NS == 1) return;
+#ifdef MSG_PHASE_PROF
+        const int ph_saved = ph_cur;
+        MSG_PH(2);
+#endif
         wp::sync();  // warp 0's lanes see thread 0's deferred samples
         r.ks[0] = npend > 0 ? sc->pend_k[0] : 0ull;
         r.ks[1] = npend > 1 ? sc->pend_k[1] : 0ull;
@@ -312,6 +327,9 @@ struct ClusterSim {
         // deferred timeline samples, in order
         for (uint32_t i = 0; i < npend; ++i) record_sample(sc->pend_t[i], r.ks[i]);
         npend = 0;
+#ifdef MSG_PHASE_PROF
+        MSG_PH(ph_saved);
+#endif
     }
 
     // --------------------------------------------------------------- events
@@ -341,6 +359,19 @@ struct ClusterSim {
     // gpu_smem: dynamic shared memory for the owned GPUs — 9 B per GPU (mask
     // words, cost ids), plus 96 B per GPU for its 8 slots when slots_smem —
     // or nullptr (everything global).
+#ifdef MSG_PHASE_PROF
+    long long ph_t = 0;
+    int ph_cur = 0;
+    MSG_DI void ph_mark(int k) {
+        if (T == 0 && sh == 0 && gs == 0) {
+            const long long c = clock64();
+            if (ph_t) atomicAdd(&g_phase[ph_cur], (unsigned long long)(c - ph_t));
+            ph_t = c;
+            if (k == 2) atomicAdd(&g_phase[8], 1ull);
+        }
+        ph_cur = k;
+    }
+#endif
     MSG_DI void setup(const SimArgs& a, const DevTables* tables, BlockScratch* scratch, unsigned char* gpu_smem,
                       bool slots_smem, uint32_t t) {
         T = wp::tid();
@@ -557,21 +588,7 @@ struct ClusterSim {
         for (uint32_t i = T; i < n_act; i += NT)
             if (ast[i] == ST_RUN) arem[i] = wp::dsub(arem[i], sc->q[w_k(W_(aslot[i] >> 3)) - 1]);
         // no trailing barrier: every reader of arem starts with one, and
-        // reschedule revisits entry i on the same thread
-    }
-
-    MSG_DI void reschedule() {  // sim.cpp:167-175
-        wp::bsync();
-#pragma unroll 4
-        for (uint32_t i = T; i < n_act; i += NT) {
-            if (ast[i] == ST_RUN) {
-                double r = arem[i];
-                if (r < 0.0) r = 0.0;
-                atkey[i] = wp::dadd(now, wp::dmul(r, sc->f[w_k(W_(aslot[i] >> 3)) - 1]));
-            }
-        }
-        // no trailing barrier: next_event scans entry i on the same thread and
-        // starts with one before any cross-thread read
+        // the next timer scan revisits entry i on the same thread
     }
 
     MSG_DI void record_sample(double t, unsigned long long ktot) {
@@ -619,6 +636,8 @@ struct ClusterSim {
     }
 
     // --------------------------------------------------------- next event
+    // reschedule_completions (sim.cpp:167-175: every Running job's
+    // prediction now + max(rem,0)*f) fused with the scan for the next timer.
     // Returns the kind (-1 none, 0 completion, 1 migration end, 2 service
     // start, 3 arrival); for slot timers `slot` is the global slot and
     // `ev_i` its index in this shard's active list (-1 on other shards).
@@ -629,7 +648,16 @@ struct ClusterSim {
 #pragma unroll 4
         for (uint32_t i = T; i < n_act; i += NT) {
             const uint8_t s = ast[i];
-            const uint64_t tk = time_key(atkey[i]);
+            double t;
+            if (s == ST_RUN) {
+                double r = arem[i];
+                if (r < 0.0) r = 0.0;
+                t = wp::dadd(now, wp::dmul(r, sc->f[w_k(W_(aslot[i] >> 3)) - 1]));
+                atkey[i] = t;
+            } else {
+                t = atkey[i];
+            }
+            const uint64_t tk = time_key(t);
             const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;
             const unsigned kind = s == ST_RUN ? 0u : (s == ST_DRAIN ? 1u : 2u);
             const unsigned tie = (kind << 28) | (unsigned)ajob[i];
@@ -660,9 +688,11 @@ struct ClusterSim {
             // masks it reads do not change before handle_arrival.
             spec = a_idx < N && q_head == q_tail;
             if (spec) {
+                MSG_PH(1);
                 uint64_t k;
                 local_dispatch(a_prof, k, r.c[0], r.c[1]);
                 r.pad2 = k;
+                MSG_PH(0);
             }
             r.hi = bhi;
             r.lo = blo;
@@ -1202,16 +1232,23 @@ struct ClusterSim {
     MSG_DI void run() {
         for (;;) {
             int slot = -1, ia = -1;
+            MSG_PH(0);
             const int kind = next_event(slot, ia);
             if (kind < 0) break;
             ++n_handler;
+            MSG_PH(3);
             advance_all();
+            MSG_PH(kind == 3 ? 4 : kind == 2 ? 6 : 5);
             if (kind == 3) handle_arrival();
             else if (kind == 2) handle_service_start(slot, ia);
             else handle_departure(slot, ia, kind == 0);
-            reschedule();
-            sample();
+            MSG_PH(7);
+            sample();  // the completions are rescheduled by the next scan
+#ifdef MSG_PHASE_PROF
+            if (T == 0 && sh == 0 && gs == 0) atomicAdd(&g_phase[9], 1ull);
+#endif
         }
+        MSG_PH(0);
     }
 
     MSG_DI void finish(DevSummary* out) {  // metrics (sim.cpp:414-502), warp 0 of shard 0

@@ -173,3 +173,15 @@ cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace msgk
+
+#ifdef MSG_PHASE_PROF
+extern "C" int msg_debug_phase(unsigned long long* out, int n, int reset) {
+    if (n > 16) n = 16;
+    if (cudaMemcpyFromSymbol(out, msgk::g_phase, n * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(msgk::g_phase, z, sizeof(z));
+    }
+    return n;
+}
+#endif
