@@ -52,6 +52,9 @@ constexpr int kScoreThreads = MSG_SCORE_THREADS;
 #ifndef MSG_SCORE_MINB
 #define MSG_SCORE_MINB 4
 #endif
+#ifndef MSG_SCORE_ILP2  // pass 1 scores two listed words per iteration (0: one)
+#define MSG_SCORE_ILP2 1
+#endif
 #ifndef MSG_SCORE_ITEM
 #define MSG_SCORE_ITEM 4
 #endif
@@ -124,10 +127,12 @@ struct ItemAcc {
 // is the word's candidate: one FFS.  REUSE selects the rescoring pass that
 // clears !reused on idle-exact starts.
 template <int P, bool LB, bool DYN, bool REUSE>
-__device__ __forceinline__ void score_word(const ScoreSmem& sm, uint64_t w, unsigned local, ItemAcc& acc) {
+__device__ __forceinline__ void score_word(const ScoreSmem& sm, uint64_t w, unsigned local, ItemAcc& acc,
+                                           bool valid = true) {
     using Q = Prof<P>;
     const unsigned lo = (unsigned)w;
     unsigned A = sm.avail[P * 256 + ((lo >> 16) & 0xFFu)];  // starts | count << 8
+    if (!valid) A = 0;  // a placeholder word: no candidate, no count
     if (!DYN) {  // candidate_starts: exact idle instances only
         A &= (unsigned)(w >> (24 + Q::pbase)) & ((1u << Q::n) - 1u);
         A |= (unsigned)__popc(A) << 8;
@@ -482,10 +487,22 @@ __device__ __forceinline__ void consume_lazy(const ScoreArgs& a, const TmaSmem& 
     }
     __syncwarp();
     acc.anyx = 0;
+#if MSG_SCORE_ILP2
+    // two words per iteration: their dependent shared-memory lookup chains
+    // (list -> word -> avail/bct -> rank rows) overlap
+    for (unsigned i = lane; i < n; i += 64) {
+        const bool has1 = i + 32 < n;
+        const unsigned idx0 = wl[i], idx1 = wl[has1 ? i + 32 : i];
+        const uint64_t w0 = buf[idx0], w1 = buf[idx1];
+        score_word<P, true, DYN, false>(sm.t, w0, m.base + idx0, acc);
+        score_word<P, true, DYN, false>(sm.t, w1, m.base + idx1, acc, has1);
+    }
+#else
     for (unsigned i = lane; i < n; i += 32) {
         const unsigned idx = wl[i];
         score_word<P, true, DYN, false>(sm.t, buf[idx], m.base + idx, acc);
     }
+#endif
     if (DYN && __any_sync(0xffffffffu, acc.anyx != 0)) {
         for (unsigned i = lane; i < n; i += 32) {
             const unsigned idx = wl[i];
