@@ -156,9 +156,14 @@ struct SimArgs {
     const uint32_t* perm;    // arrival order -> rank (only traces with has_perm)
     int32_t* queue;          // FCFS queue storage, n_jobs per trace
     JobOut* jobs;
+    JobOut* jobs_host;       // optional (pipelined msg_run_batch): a finished trace's records, also
+                             // stored by its warp into mapped pinned host memory (no separate D2H)
     EventRec* events;
     double* timeline;        // (t, mean) pairs
     DevSummary* summary;
+    DevSummary* summary_host;  // optional (pipelined msg_run_batch): the summary, also in mapped host memory,
+    uint32_t* done_host;       // then done_host[t] = done_epoch once the trace's host records are visible
+    uint32_t done_epoch;
     uint32_t n_traces;
     uint32_t out_flags;
     // block engine (G > 32): cluster arena, indexed by GPU (cl_goff + g) or

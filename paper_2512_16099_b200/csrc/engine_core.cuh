@@ -117,6 +117,7 @@ struct TraceSim {
     const uint32_t* perm;
     int32_t* queue;
     JobOut* jobs;
+    JobOut* jobs_h;  // SimArgs::jobs_host of this trace, or null
     EventRec* evs;
     double* tl;
     uint32_t N, ev_cap, tl_cap, oflags;
@@ -193,6 +194,7 @@ struct TraceSim {
         perm = tr.has_perm ? a.perm + tr.job_off : nullptr;
         queue = a.queue + tr.job_off;
         jobs = a.jobs + tr.job_off;
+        jobs_h = a.jobs_host ? a.jobs_host + tr.job_off : nullptr;
         evs = a.events ? a.events + tr.ev_off : nullptr;
         tl = a.timeline ? a.timeline + 2 * tr.tl_off : nullptr;
         ev_cap = tr.ev_cap;
@@ -273,6 +275,7 @@ struct TraceSim {
         arr = nullptr;
         perm = nullptr;
         jobs = a.scratch ? a.scratch + (size_t)i * a.rank_cap : nullptr;
+        jobs_h = nullptr;
         evs = a.events + (size_t)i * a.ev_cap;
         ev_cap = a.ev_cap;
         tl = nullptr;
@@ -894,7 +897,7 @@ struct TraceSim {
     }
 
     // metrics (sim.cpp:414-502): sums in job-id order, then divide.
-    MSG_DI void finish(DevSummary* out) {
+    MSG_DI void finish(DevSummary* out, DevSummary* out_host = nullptr) {
         wp::sync();
         DevSummary s;
         s.status = q_head < q_tail ? STATUS_JOBS_PENDING : STATUS_OK;
@@ -907,8 +910,10 @@ struct TraceSim {
                 double w = 0.0, e = 0.0, t = 0.0, a = 0.0, d = 0.0;
                 if (j < N) {
                     a = arr[j];
-                    const double sc = jobs[j].sched;
-                    d = jobs[j].done;
+                    const JobOut jo = jobs[j];
+                    if (jobs_h) jobs_h[j] = jo;  // coalesced: a warp stores 32 consecutive records
+                    const double sc = jo.sched;
+                    d = jo.done;
                     w = wp::dsub(sc, a);
                     e = wp::dsub(d, sc);
                     t = wp::dadd(w, e);
@@ -957,7 +962,10 @@ struct TraceSim {
         s.max_intra = max_intra;
         s.max_inter = max_inter;
         s.tl_sum = tl_sum;
-        if (L == 0) *out = s;
+        if (L == 0) {
+            *out = s;
+            if (out_host) *out_host = s;
+        }
     }
 };
 
@@ -968,7 +976,12 @@ MSG_DI void simulate_trace(const SimArgs& a, const DevTables* tables, WarpSmem<S
     TraceSim<SPL, DETAIL> sim;
     sim.setup(a, tables, ws, t);
     sim.run();
-    sim.finish(a.summary + t);
+    sim.finish(a.summary + t, a.summary_host ? a.summary_host + t : nullptr);
+    if (a.done_host) {  // publish: every lane's host stores, then the trace's flag
+        wp::gfence_sys();
+        wp::sync();
+        if (wp::lane() == 0) *(volatile uint32_t*)(a.done_host + t) = a.done_epoch;
+    }
 }
 
 // One decision-level operation on one cluster snapshot (decide.cu): the

@@ -65,6 +65,8 @@ struct msg_staged {
     // pinned host mirrors (rank order)
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
+    HostBuf h_done;           // run_pipelined: per-trace completion flags (mapped, written by the kernel)
+    uint32_t done_epoch = 0;  // the flag value of the current run
     // device
     DevBuf d_arrival, d_service, d_profile, d_perm, d_traces, d_configs, d_init, d_tables_unused;
     DevBuf d_queue, d_jobs, d_events, d_timeline, d_summary;
@@ -682,6 +684,18 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     PhaseTimer pt;
     uint32_t d0s[kMaxPipeChunks + 1];
     const int n_chunks = pipe_bounds(T, d0s);
+    // Job records reach the host through the kernel's own stores into mapped
+    // pinned memory as each trace finishes (MSG_JOBS_D2H=1: one copy per chunk
+    // after its kernel instead).
+    static const bool jobs_d2h = std::getenv("MSG_JOBS_D2H") != nullptr;
+    // Each trace also publishes its summary and a completion flag in mapped
+    // host memory, so host threads decode traces as they finish, under the
+    // kernels still running (MSG_PIPE_POLL=0: chunk by chunk after each
+    // chunk's event).
+    static const bool poll = !jobs_d2h && [] {
+        const char* e = std::getenv("MSG_PIPE_POLL");
+        return !(e && e[0] == '0');
+    }();
     for (int k = 0; k < n_chunks; ++k) {
         if (!eng->pstream[k]) CK(cudaStreamCreateWithFlags(&eng->pstream[k], cudaStreamNonBlocking));
         if (!eng->pevent[k]) CK(cudaEventCreateWithFlags(&eng->pevent[k], cudaEventDisableTiming));
@@ -689,6 +703,13 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     const size_t N = std::max<uint64_t>(s->n_jobs, 1);
     CK(s->h_summary.ensure(std::max<uint32_t>(T, 1) * sizeof(DevSummary)));
     if (want_jobs) CK(s->h_jobs.ensure(N * sizeof(JobOut)));
+    if (poll) {
+        const void* had = s->h_done.p;
+        CK(s->h_done.ensure(std::max<uint32_t>(T, 1) * sizeof(uint32_t)));
+        if (s->h_done.p != had) std::memset(s->h_done.p, 0, s->h_done.cap);
+        if (++s->done_epoch == 0) s->done_epoch = 1;  // 0 is the zeroed buffer
+    }
+    volatile uint32_t* hdone = poll ? s->h_done.as<uint32_t>() : nullptr;
     double* ha = s->h_arrival.as<double>();
     double* hs = s->h_service.as<double>();
     uint8_t* hp = s->h_profile.as<uint8_t>();
@@ -734,12 +755,19 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         c.traces = s->d_traces.as<DevTrace>() + d0;
         c.summary = s->d_summary.as<DevSummary>() + d0;
         c.n_traces = d1 - d0;
+        if (want_jobs && !jobs_d2h) c.jobs_host = s->h_jobs.as<JobOut>();  // finished traces store their rows
+        if (poll) {
+            c.summary_host = s->h_summary.as<DevSummary>() + d0;
+            c.done_host = s->h_done.as<uint32_t>() + d0;
+            c.done_epoch = s->done_epoch;
+        }
         cudaError_t e = launch_sim(s->spl, c, st);
         if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim (pipelined)");
         ++eng->launches;
-        CK(cudaMemcpyAsync(s->h_summary.as<DevSummary>() + d0, s->d_summary.as<DevSummary>() + d0,
-                           (d1 - d0) * sizeof(DevSummary), cudaMemcpyDeviceToHost, st));
-        if (want_jobs && nj)
+        if (!poll)
+            CK(cudaMemcpyAsync(s->h_summary.as<DevSummary>() + d0, s->d_summary.as<DevSummary>() + d0,
+                               (d1 - d0) * sizeof(DevSummary), cudaMemcpyDeviceToHost, st));
+        if (want_jobs && nj && jobs_d2h)
             CK(cudaMemcpyAsync(s->h_jobs.as<JobOut>() + j0, s->d_jobs.as<JobOut>() + j0, nj * sizeof(JobOut),
                                cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(eng->pevent[k], st));
@@ -768,15 +796,35 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     const DevSummary* ds = s->h_summary.as<DevSummary>();
     const JobOut* hj = s->h_jobs.as<JobOut>();
     std::atomic<uint64_t> handler{0};
-    std::atomic<bool> pending{false};
-    for (int k = 0; k < n_chunks; ++k) {
-        const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
+    std::atomic<bool> pending{false}, lost{false};
+    // Waits for trace d's completion flag; false if its chunk ended (or
+    // failed) without it — then the chunk's event reports the error below.
+    auto wait_done = [&](uint32_t d) {
+        int k = 0;
+        while (k + 1 < n_chunks && d >= d0s[k + 1]) ++k;
+        for (uint32_t spins = 1;; ++spins) {
+            if (hdone[d] == s->done_epoch) break;
+            if ((spins & 4095u) == 0) {
+                const cudaError_t q = cudaEventQuery(eng->pevent[k]);
+                if (q != cudaErrorNotReady && hdone[d] != s->done_epoch) {
+                    lost = true;
+                    return false;
+                }
+            }
+            _mm_pause();
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return true;
+    };
+    for (int k = 0; k < (poll ? 1 : n_chunks); ++k) {
+        const uint32_t d0 = poll ? 0 : d0s[k], d1 = poll ? T : d0s[k + 1];
         if (d0 == d1) continue;
-        CK(cudaEventSynchronize(eng->pevent[k]));
+        if (!poll) CK(cudaEventSynchronize(eng->pevent[k]));
         pt.mark("  chunk kernel+D2H done");
         parallel_for(d1 - d0, 64, [&](uint32_t i) {
             const uint32_t d = d0 + i, t = s->src_of[d];
             if (s->status[t] != MSG_OK) return;  // failed its check: reported as such, no rows
+            if (poll && !wait_done(d)) return;
             const DevTrace& tr = s->traces[d];
             const DevSummary& x = ds[d];
             msg_trace_summary& o = res->summaries[t];
@@ -794,6 +842,14 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
                      hp + tr.job_off);
         });
         pt.mark("  chunk decoded");
+    }
+    if (poll) {
+        for (int k = 0; k < n_chunks; ++k)
+            if (d0s[k] != d0s[k + 1]) CK(cudaEventSynchronize(eng->pevent[k]));
+        if (lost) {
+            eng->last_error = "CudaError: a pipelined chunk completed without publishing a trace";
+            return MSG_ERR_CUDA;
+        }
     }
     if (pending && want_jobs) {  // the reference throws for these traces: drop their rows
         uint64_t w = 0;
