@@ -18,6 +18,17 @@ if "staged" in sys.argv[1:]:  # what bench.py does first: a staged copy, timed l
     for _ in range(13):
         eng.flush_l2()
         st.time_launch()
+if "nvml" in sys.argv[1:]:  # bench.py's clock sampler around a short region
+    import bench
+    c = bench.ClockSampler(0)
+    c.start()
+    time.sleep(0.05)
+    c.stop()
+if "bench" in sys.argv[1:]:  # bench.py's own workload object
+    import bench
+    bench.TRACES_RUN = 4096
+    b, cfg0 = bench.workload(0)
+    cfg = [cfg0]
 for mode in ("hold", "drop", "hold", "drop"):
     for _ in range(3):
         out = eng.run_batch(b, cfg, abi.OUT_JOBS)
