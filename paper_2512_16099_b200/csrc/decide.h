@@ -15,7 +15,7 @@ struct ScoreArgs {
     uint32_t n;
     uint32_t lb, dyn, lazymask;
     // scratch (n + 1 + n words; the first n unused): the count and list of
-    // snapshots pass 1 left without a Lazy candidate (score_list_kernel)
+    // snapshots pass 1 left without a Lazy candidate (score_reduce_kernel)
     uint32_t* scratch;
     uint64_t* items;  // TMA path: 2 words per item (score_items_bytes)
 };
