@@ -3,8 +3,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -18,7 +21,7 @@
 namespace msgk {
 
 // Persistent fork-join pool for the host-side staging / decoding loops: the
-// workers are created once (hardware_concurrency - 1) and woken per call, so
+// workers are created once (threads_for_this_process() - 1) and woken per call, so
 // a batch pays no thread creation.  One parallel region at a time (calls
 // from several host threads serialise on the pool).
 class HostPool {
@@ -62,8 +65,25 @@ class HostPool {
 
   private:
     HostPool() {
-        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned hw = threads_for_this_process();
         for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    // MSG_HOST_THREADS, else the CPUs this process may run on (affinity
+    // mask), shared evenly among the processes of one node under torchrun
+    // (LOCAL_WORLD_SIZE): one process per GPU must not oversubscribe the host.
+    static unsigned threads_for_this_process() {
+        if (const char* e = std::getenv("MSG_HOST_THREADS")) {
+            const long v = std::strtol(e, nullptr, 10);
+            if (v > 0) return (unsigned)std::min(v, 1024L);
+        }
+        unsigned n = std::max(1u, std::thread::hardware_concurrency());
+        cpu_set_t set;
+        if (sched_getaffinity(0, sizeof(set), &set) == 0) n = std::max(1, CPU_COUNT(&set));
+        if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
+            const long w = std::strtol(e, nullptr, 10);
+            if (w > 1) n = std::max(1u, n / (unsigned)w);
+        }
+        return n;
     }
     void loop() {
         uint64_t seen = 0;
