@@ -158,13 +158,9 @@ inline void put_row(msg_job_row* dst, int64_t id, double arrival, const JobOut& 
 // A trace's rows, written with non-temporal 16-byte stores in pairs (144 B
 // = 9 aligned vectors): the row buffer is far larger than the caches and is
 // not read back here, so the stores skip the read-for-ownership.
-// MSG_ROWS_NT=0 writes them with plain stores.
+// nt false (MSG_ROWS_NT=0): plain stores.
 inline void put_rows(msg_job_row* rows, uint32_t n, const int64_t* ids, const double* ha, const JobOut* hj,
-                     const uint8_t* hp) {
-    static const bool nt = [] {
-        const char* e = std::getenv("MSG_ROWS_NT");
-        return !(e && e[0] == '0');
-    }();
+                     const uint8_t* hp, bool nt) {
     uint32_t r = 0;
     if (nt) {
         if (n && (reinterpret_cast<uintptr_t>(rows) & 15)) {
@@ -687,15 +683,17 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     // Job records reach the host through the kernel's own stores into mapped
     // pinned memory as each trace finishes (MSG_JOBS_D2H=1: one copy per chunk
     // after its kernel instead).
-    static const bool jobs_d2h = std::getenv("MSG_JOBS_D2H") != nullptr;
+    auto env_off = [](const char* name) {
+        const char* e = std::getenv(name);
+        return e && e[0] == '0';
+    };
+    const bool jobs_d2h = std::getenv("MSG_JOBS_D2H") != nullptr;
     // Each trace also publishes its summary and a completion flag in mapped
     // host memory, so host threads decode traces as they finish, under the
     // kernels still running (MSG_PIPE_POLL=0: chunk by chunk after each
     // chunk's event).
-    static const bool poll = !jobs_d2h && [] {
-        const char* e = std::getenv("MSG_PIPE_POLL");
-        return !(e && e[0] == '0');
-    }();
+    const bool poll = !jobs_d2h && !env_off("MSG_PIPE_POLL");
+    const bool rows_nt = !env_off("MSG_ROWS_NT");
     for (int k = 0; k < n_chunks; ++k) {
         if (!eng->pstream[k]) CK(cudaStreamCreateWithFlags(&eng->pstream[k], cudaStreamNonBlocking));
         if (!eng->pevent[k]) CK(cudaEventCreateWithFlags(&eng->pevent[k], cudaEventDisableTiming));
@@ -839,7 +837,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             }
             if (!want_jobs) return;
             put_rows(res->jobs.p.get() + res->job_off[t], tr.n_jobs, ids, ha + tr.job_off, hj + tr.job_off,
-                     hp + tr.job_off);
+                     hp + tr.job_off, rows_nt);
         });
         pt.mark("  chunk decoded");
     }

@@ -217,6 +217,27 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
     assert not bad, bad[:3]
 
 
+@pytest.mark.parametrize("env", [{"MSG_PIPE_POLL": "0"}, {"MSG_JOBS_D2H": "1"}, {"MSG_ROWS_NT": "0"},
+                                 {"MSG_PIPE_W": "1,2,3,1,1,1,1,1"}, {"MSG_NO_PIPELINE": "1"}])
+def test_pipeline_variants_agree(engine, monkeypatch, env):
+    """The pipelined msg_run_batch's variants — chunk-by-chunk decode after
+    each chunk's event, job records by copy, plain row stores, other chunk
+    weights, no pipeline — return the same bytes as the default (records
+    and a completion flag published per trace in mapped host memory)."""
+    from paper_2512_16099_b200.engine import generate_batch
+
+    b = generate_batch(preset("normal25"), 5, 700)
+    cfg = [SimConfig(gpu_count=8)]
+    want = engine.run_batch(b, cfg, abi.OUT_JOBS)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = engine.run_batch(b, cfg, abi.OUT_JOBS)
+    assert got.summaries.tobytes() == want.summaries.tobytes()
+    assert got.jobs.tobytes() == want.jobs.tobytes()
+    again = engine.run_batch(b, cfg, abi.OUT_JOBS)  # the next run's completion flags (new epoch)
+    assert again.jobs.tobytes() == want.jobs.tobytes()
+
+
 def test_report_files_from_gpu_results_match_reference(engine):
     """§8f row 1: the reference CLI's files (events.jsonl, report.json,
     report.csv, fragcost_timeline.csv) formatted natively from the GPU
