@@ -499,10 +499,14 @@ def main():
         eng.run_batch(batch, [cfg], abi.OUT_JOBS)
     barrier()
     e2e_s = []
+    import gc
+
+    gc.disable()  # as timeit does: no collector pauses inside the timed calls
     for _ in range(args.steps):
         t0 = time.perf_counter()
         out = eng.run_batch(batch, [cfg], abi.OUT_JOBS)
         e2e_s.append(time.perf_counter() - t0)
+    gc.enable()
     barrier()
     e2e_step = allreduce(sum(e2e_s) / len(e2e_s), MAX)
     e2e_value = total_events / e2e_step
