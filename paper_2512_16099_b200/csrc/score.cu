@@ -476,10 +476,17 @@ __device__ __forceinline__ void consume_lazy(const ScoreArgs& a, const TmaSmem& 
     const int K = __popc(a.lazymask & 0xFFu);
     const bool whole = m.nvalid == (uint32_t)kChunk;
     unsigned n = 0;
+    // all of the thread's words first: the list stores below may not be
+    // reordered above later loads of the stage, so interleaving them would
+    // expose one shared-memory latency per word
+    unsigned los[kWordsPerThread];
+#pragma unroll
+    for (int k = 0; k < kWordsPerThread; ++k)
+        los[k] = reinterpret_cast<const uint32_t*>(buf)[2 * (wbase + (unsigned)k * 32u + lane)];
 #pragma unroll
     for (int k = 0; k < kWordsPerThread; ++k) {
         const unsigned idx = wbase + (unsigned)k * 32u + lane;
-        const unsigned lo = reinterpret_cast<const uint32_t*>(buf)[2 * idx];
+        const unsigned lo = los[k];
         const bool lz = (whole || idx < m.nvalid) && __popc(lo & 0x7Fu) < K;
         const unsigned bal = __ballot_sync(0xffffffffu, lz);
         if (lz) wl[n + __popc(bal & lt)] = (uint16_t)idx;
