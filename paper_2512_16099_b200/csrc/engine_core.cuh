@@ -394,13 +394,21 @@ struct TraceSim {
         if (!(dt > 0.0)) return;  // dt <= 0: last_update = now only
         const double q = wp::ddiv(dt, my_f);
         wp::sync();
+        // every load before the first store (the stores could alias them)
+        bool run[SPL];
+        unsigned k[SPL];
+        double r[SPL];
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
-            const bool run = sm->st[slot] == ST_RUN;
-            const unsigned k = run ? w_k(sm->gw[slot >> 3]) : 1u;
-            const double qk = wp::shfl(q, (int)k - 1);
-            if (run) sm->rem[slot] = wp::dsub(sm->rem[slot], qk);
+            run[i] = sm->st[slot] == ST_RUN;
+            k[i] = run[i] ? w_k(sm->gw[slot >> 3]) : 1u;
+            r[i] = sm->rem[slot];
+        }
+#pragma unroll
+        for (int i = 0; i < SPL; ++i) {
+            const double qk = wp::shfl(q, (int)k[i] - 1);
+            if (run[i]) sm->rem[L + 32 * i] = wp::dsub(r[i], qk);
         }
     }
 
@@ -438,28 +446,41 @@ struct TraceSim {
         unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
         int bsl = -1;
         double bt = 0.0;
+        // every load before the first store (the tkey stores could alias them)
+        uint8_t sv[SPL];
+        unsigned kv[SPL], jv[SPL], mv[SPL];
+        double rv[SPL], tv[SPL];
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
-            const uint8_t s = sm->st[slot];
+            sv[i] = sm->st[slot];
+            kv[i] = sv[i] == ST_RUN ? w_k(sm->gw[slot >> 3]) : 1u;
+            rv[i] = sm->rem[slot];
+            tv[i] = sm->tkey[slot];
+            jv[i] = (unsigned)sm->job[slot];
+            mv[i] = sm->mseq[slot];
+        }
+#pragma unroll
+        for (int i = 0; i < SPL; ++i) {
+            const int slot = L + 32 * i;
+            const uint8_t s = sv[i];
             const bool run = s == ST_RUN;
-            const unsigned k = run ? w_k(sm->gw[slot >> 3]) : 1u;
-            const double f = wp::shfl(my_f, (int)k - 1);
+            const double f = wp::shfl(my_f, (int)kv[i] - 1);
             if (s >= ST_RUN) {
                 double t;
                 if (run) {
-                    double r = sm->rem[slot];
+                    double r = rv[i];
                     if (r < 0.0) r = 0.0;  // std::max(rem, 0.0)
                     t = wp::dadd(now, wp::dmul(r, f));
                     sm->tkey[slot] = t;
                 } else {
-                    t = sm->tkey[slot];
+                    t = tv[i];
                 }
                 const uint64_t tk = time_key(t);
                 const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;
                 const unsigned kind = run ? 0u : (s == ST_DRAIN ? 1u : 2u);
-                const unsigned tie = (kind << 28) | (unsigned)sm->job[slot];
-                const unsigned ms = s == ST_DRAIN ? sm->mseq[slot] : 0u;
+                const unsigned tie = (kind << 28) | jv[i];
+                const unsigned ms = s == ST_DRAIN ? mv[i] : 0u;
                 const bool better =
                     hi < bhi ||
                     (hi == bhi && (lo < blo || (lo == blo && (tie < btie || (tie == btie && ms < bms)))));
