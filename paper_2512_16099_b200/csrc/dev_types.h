@@ -142,6 +142,7 @@ struct DevTables {
     uint8_t feasid[256];         // blocked_m -> id of its per-profile feasible-count vector
     uint8_t idealid[80];         // popc(busy_c) * 9 + popc(busy_m) -> id of its ideal-count vector
     uint8_t cost4pair[32 * 32];  // [ideal id][feasible id] -> 4-mask cost id
+    uint32_t share_run[6 * 8];   // [profile][start] -> a Running instance's share of the GPU word
 };
 
 // Kernel arguments of the per-trace event loop (engine_core.cuh).

@@ -373,6 +373,32 @@ struct TraceSim {
         return w;
     }
 
+    // One instance's share of its GPU's word.  Instances on a GPU are pairwise
+    // memory-disjoint (gpu.cpp:146-156) and compute bits lie inside memory
+    // bits, so the word is the bitwise SUM of these shares and every
+    // lifecycle transition updates it exactly by adding / subtracting them:
+    // the same word refresh_gpu would rebuild from the 8 slots, without the
+    // slot loads and the two warp reductions.
+    MSG_DI unsigned share(unsigned st, int p, int s) const {
+        if (st < ST_RUN) return 0u;
+        const unsigned t = tb->share_run[p * 8 + s];  // Running: busy c/m, blocked m, one running job
+        return st == ST_RUN ? t : (st == ST_WAIT ? t - (1u << 24) : (t & 0xFF0000u));
+    }
+
+    // Store GPU g's new word (warp-uniform) and its timeline cost, as
+    // refresh_gpu does.
+    MSG_DI unsigned set_gpu(int g, unsigned w) {
+        const double nc = cost4w(w), oc = sm->gcost[g];
+        wp::sync();
+        if (L == 0) {
+            sm->gw[g] = w;
+            sm->gcost[g] = nc;
+        }
+        if (wp::dbits(nc) != wp::dbits(oc) && (unsigned)g < tl_from) tl_from = (unsigned)g;
+        wp::sync();
+        return w;
+    }
+
     // ------------------------------------------------- contention model
     // slowdown(k) = 1 + alpha*(k-1) (sim.cpp:26-31): DMUL then DADD.
     MSG_DI double factor(unsigned k) const {
@@ -462,37 +488,30 @@ struct TraceSim {
         }
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
+            // branch-free: every slot forms its key, unarmed ones an all-NONE
+            // key that never wins
             const int slot = L + 32 * i;
             const uint8_t s = sv[i];
-            const bool run = s == ST_RUN;
+            const bool run = s == ST_RUN, armed = s >= ST_RUN, drain = s == ST_DRAIN;
             const double f = wp::shfl(my_f, (int)kv[i] - 1);
-            if (s >= ST_RUN) {
-                double t;
-                if (run) {
-                    double r = rv[i];
-                    if (r < 0.0) r = 0.0;  // std::max(rem, 0.0)
-                    t = wp::dadd(now, wp::dmul(r, f));
-                    sm->tkey[slot] = t;
-                } else {
-                    t = tv[i];
-                }
-                const uint64_t tk = time_key(t);
-                const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;
-                const unsigned kind = run ? 0u : (s == ST_DRAIN ? 1u : 2u);
-                const unsigned tie = (kind << 28) | jv[i];
-                const unsigned ms = s == ST_DRAIN ? mv[i] : 0u;
-                const bool better =
-                    hi < bhi ||
-                    (hi == bhi && (lo < blo || (lo == blo && (tie < btie || (tie == btie && ms < bms)))));
-                if (better) {
-                    bhi = hi;
-                    blo = lo;
-                    btie = tie;
-                    bms = ms;
-                    bsl = slot;
-                    bt = t;
-                }
-            }
+            const double r = rv[i] < 0.0 ? 0.0 : rv[i];  // std::max(rem, 0.0)
+            const double tp = wp::dadd(now, wp::dmul(r, f));
+            if (run) sm->tkey[slot] = tp;
+            const double t = run ? tp : tv[i];
+            const uint64_t tk = time_key(t);
+            const unsigned hi = armed ? (unsigned)(tk >> 32) : NONE, lo = armed ? (unsigned)tk : NONE;
+            const unsigned kind = run ? 0u : (drain ? 1u : 2u);
+            const unsigned tie = armed ? ((kind << 28) | jv[i]) : NONE;
+            const unsigned ms = armed ? (drain ? mv[i] : 0u) : NONE;
+            const uint64_t ka = ((uint64_t)hi << 32) | lo, kb = ((uint64_t)tie << 32) | ms;
+            const uint64_t ba = ((uint64_t)bhi << 32) | blo, bb = ((uint64_t)btie << 32) | bms;
+            const bool better = ka < ba || (ka == ba && kb < bb);
+            bhi = better ? hi : bhi;
+            blo = better ? lo : blo;
+            btie = better ? tie : btie;
+            bms = better ? ms : bms;
+            bsl = better ? slot : bsl;
+            bt = better ? t : bt;
         }
         const unsigned mhi = wp::rmin(bhi);
         const bool have_arrival = a_idx < N;
@@ -646,10 +665,13 @@ struct TraceSim {
     }
 
     // apply_placement + start_service (sim.cpp:199-218).
-    MSG_DI double apply_placement(int g, int s, int32_t r, double sv, unsigned nops) {
+    MSG_DI double apply_placement(int g, int p, int s, int32_t r, double sv, unsigned nops) {
         const double delay = wp::dmul((double)nops, latency);
         const double ss = wp::dadd(now, delay);
         const int slot = g * 8 + s;
+        // the destination held no instance or an idle one, and create only
+        // destroys idle ones: the GPU gains exactly the new instance's share
+        const unsigned w = sm->gw[g] + share(delay > 0.0 ? ST_WAIT : ST_RUN, p, s);
         if (L == 0) {
             sm->job[slot] = r;
             sm->mig[slot] = 0;
@@ -658,7 +680,7 @@ struct TraceSim {
             sm->tkey[slot] = ss;
             jobs[r].sched = ss;
         }
-        refresh_gpu(g);
+        set_gpu(g, w);
         return ss;
     }
 
@@ -667,7 +689,7 @@ struct TraceSim {
     MSG_DI void place(const Decision& d, int32_t r, int p, double sv, uint8_t kind) {
         const CreateRes cr = create(d.g, p, d.s);
         const unsigned nops = (unsigned)wp::popc(cr.dmask) + (cr.reused ? 0u : 1u);
-        const double ss = apply_placement(d.g, d.s, r, sv, nops);
+        const double ss = apply_placement(d.g, p, d.s, r, sv, nops);
         emit(kind, r, (unsigned)d.g, 0, (unsigned)p, (unsigned)d.s, 0, EF_PLACED | (cr.reused ? EF_REUSED : 0),
              snap_mode ? (uint64_t)d.evals : wp::dbits(ss));
         emit_reconfig(d.g, p, d.s, cr);
@@ -702,8 +724,14 @@ struct TraceSim {
         const uint8_t jst = sm->st[from_slot];
         const double jrem = sm->rem[from_slot], jtk = sm->tkey[from_slot];
         const unsigned jmig = sm->mig[from_slot];
-        const unsigned fcb = k2w(sm->gw[fg]);
-        const unsigned tcb = k2w(sm->gw[tg]);
+        const unsigned wf = sm->gw[fg], wt = sm->gw[tg];
+        const unsigned fcb = k2w(wf);
+        const unsigned tcb = k2w(wt);
+        // source: the job's share leaves, a draining replica's (blocked
+        // memory only) stays while overlap > 0; destination: the job's share
+        const unsigned sh_to = share(jst, q, ts);
+        unsigned nwf = wf - share(jst, q, fs) + (overlap > 0.0 ? share(ST_DRAIN, q, fs) : 0u);
+        if (tg == fg) nwf += sh_to;
         wp::sync();
         if (L == 0) sm->st[from_slot] = ST_DRAIN;  // start_draining
         const CreateRes cr = create(tg, q, ts);
@@ -722,8 +750,8 @@ struct TraceSim {
             }
         }
         if (overlap > 0.0) ++mseq_ctr;
-        const unsigned nwf = refresh_gpu(fg);
-        const unsigned nwt = tg != fg ? refresh_gpu(tg) : nwf;
+        set_gpu(fg, nwf);
+        const unsigned nwt = tg != fg ? set_gpu(tg, wt + sh_to) : nwf;
         const uint64_t costs = (uint64_t)fcb | ((uint64_t)k2w(nwf) << 16) | ((uint64_t)tcb << 32) |
                                ((uint64_t)k2w(nwt) << 48);
         emit(EV_MIGRATION_START, r, (unsigned)fg, (unsigned)tg, (unsigned)q, (unsigned)fs, (unsigned)ts,
@@ -876,6 +904,7 @@ struct TraceSim {
         const int g = slot >> 3;
         const int32_t r = sm->job[slot];
         const int m = sm->mig[slot];
+        const unsigned w = sm->gw[g] - share(sm->st[slot], sm->prof[slot], slot & 7);
         wp::sync();
         if (L == 0) {
             sm->st[slot] = ST_IDLE;  // release_job / finish_draining: the instance stays, idle
@@ -885,7 +914,7 @@ struct TraceSim {
                 jobs[r].mig = m;
             }
         }
-        refresh_gpu(g);
+        set_gpu(g, w);
         emit(completion ? EV_COMPLETION : EV_MIGRATION_END, r, (unsigned)g, 0, 0, 0, 0, 0, 0);
         if (completion) sample();  // post-departure level
         const int passes = (completion && (cflags & CF_MIG)) ? 2 : 1;
@@ -897,10 +926,11 @@ struct TraceSim {
 
     MSG_DI void handle_service_start(int slot) {  // sim.cpp:317-323
         wp::sync();
+        const unsigned w = sm->gw[slot >> 3] + (1u << 24);  // WaitingStart -> Running: one more running job
         if (L == 0) {
             sm->st[slot] = ST_RUN;  // start_service: rem already holds service_s
         }
-        refresh_gpu(slot >> 3);
+        set_gpu(slot >> 3, w);
     }
 
     MSG_DI void run() {  // Engine::execute (sim.cpp:123-141)

@@ -140,6 +140,11 @@ inline int build_tables(DevTables* t) {
     if (d4.size() > 256) return -2;
     for (size_t i = 0; i < k4.size(); ++i)
         t->cost4pair[i] = (uint8_t)(std::lower_bound(d4.begin(), d4.end(), k4[i]) - d4.begin());
+    for (int p = 0; p < 6; ++p)
+        for (int s = 0; s < 8; ++s) {
+            const unsigned m = host_fpm(p, s) & 0xFFu;
+            t->share_run[p * 8 + s] = (host_fpc(p, s) & 0x7Fu) | (m << 8) | (m << 16) | (1u << 24);
+        }
     for (size_t i = 0; i < 256; ++i) {
         t->cost4val[i] = i < d4.size() ? (double)d4[i] / 25200.0 : 0.0;
         t->cost4k[i] = i < d4.size() ? (uint16_t)d4[i] : 0;
