@@ -552,21 +552,22 @@ struct TraceSim {
             unsigned kmin = NONE, nl = 0, nb = 0;
 #pragma unroll
             for (int i = 0; i < SPL; ++i) {
+                // branch-free: every slot scores, non-candidates (illegal
+                // start, unavailable, beyond G) drop out of the min and counts
                 const int slot = L + 32 * i;
                 const int g = slot >> 3, s = slot & 7;
-                if (g < G && ((smask >> s) & 1u)) {
-                    const unsigned w = sm->gw[g];
-                    const bool exact = sm->st[slot] == ST_IDLE && sm->prof[slot] == p;
-                    if ((dyn || exact) && !(fpm(p, s) & w_km(w))) {  // candidate_starts + avail
-                        const unsigned rk = rank2(w_bc(w) | fpc(p, s), w_bm(w) | fpm(p, s));
-                        const unsigned lazy = (lazymask >> wp::popc(w_bc(w))) & 1u;
-                        const unsigned key = ((lazy ^ 1u) << 31) | (rk << 26) | ((exact ? 0u : 1u) << 25) |
-                                             ((unsigned)g << 3) | (unsigned)s;
-                        kmin = key < kmin ? key : kmin;
-                        nl += lazy;
-                        nb += lazy ^ 1u;
-                    }
-                }
+                const unsigned w = sm->gw[g];
+                const bool exact = sm->st[slot] == ST_IDLE && sm->prof[slot] == p;
+                const unsigned fm = fpm(p, s);
+                const bool cand = g < G && ((smask >> s) & 1u) && (dyn || exact) &&
+                                  !(fm & w_km(w));  // candidate_starts + avail
+                const unsigned rk = rank2((w_bc(w) | fpc(p, s)) & 0x7Fu, (w_bm(w) | fm) & 0xFFu);
+                const unsigned lazy = (lazymask >> wp::popc(w_bc(w))) & 1u;
+                const unsigned key = ((lazy ^ 1u) << 31) | (rk << 26) | ((exact ? 0u : 1u) << 25) |
+                                     ((unsigned)g << 3) | (unsigned)s;
+                kmin = cand && key < kmin ? key : kmin;
+                nl += cand ? lazy : 0u;
+                nb += cand ? (lazy ^ 1u) : 0u;
             }
             const unsigned k = wp::rmin(kmin);
             const unsigned cnt = wp::radd(nl | (nb << 16));  // <= 8 candidates per lane
