@@ -74,13 +74,19 @@ template <int SPL>
 struct WarpSmem {
     static constexpr int NS = 32 * SPL;  // slots
     static constexpr int NG = 4 * SPL;   // GPUs
-    double rem[NS];    // RunJob::remaining_work (WAIT: service demand)
-    double tkey[NS];   // timer time of the slot
+    struct alignas(16) RT {
+        double rem;    // RunJob::remaining_work (WAIT: service demand)
+        double tkey;   // timer time of the slot
+    };
+    RT rt[NS];         // side by side: the timer scan reads both with one 16-byte load
     double gcost[NG];  // frag_cost(gpu) for the timeline (4-mask form)
     double tlp[NG + 2];  // timeline prefix sums: tlp[g] = ((c0 + c1) + ...) + c(g-1), reference order
-    int32_t job[NS];   // bound job rank (RUN/WAIT) or migrating job (DRAIN)
+    struct alignas(8) JM {
+        int32_t job;    // bound job rank (RUN/WAIT) or migrating job (DRAIN)
+        uint32_t mseq;  // MigrationEnd push sequence
+    };
+    JM jm[NS];
     uint32_t cseq[NS]; // instance creation order (vector order, gpu.cpp:88-111)
-    uint32_t mseq[NS]; // MigrationEnd push sequence
     uint32_t gw[NG];   // per-GPU mask word
     uint16_t mig[NS];  // migrations of the bound job
     uint8_t prof[NS];  // instance profile
@@ -300,7 +306,7 @@ struct TraceSim {
                 sm->st[slot] = (uint8_t)(v & 0xFu);
                 sm->prof[slot] = (uint8_t)((v >> 4) & 0xFu);
                 sm->cseq[slot] = v >> 8;
-                sm->job[slot] = a.job_in[base + slot];
+                sm->jm[slot].job = a.job_in[base + slot];
                 sm->mig[slot] = 0;
                 if ((v & 0xFu) != ST_EMPTY) {
                     maxseq = (v >> 8) > maxseq ? (v >> 8) : maxseq;
@@ -327,7 +333,7 @@ struct TraceSim {
                 const bool busy = s == ST_RUN || s == ST_WAIT;
                 a.slot_out[base + slot] = (uint32_t)(busy ? ST_RUN : s) | ((uint32_t)sm->prof[slot] << 4) |
                                           (sm->cseq[slot] << 8);
-                a.job_out[base + slot] = busy ? sm->job[slot] : -1;
+                a.job_out[base + slot] = busy ? sm->jm[slot].job : -1;
             }
         }
     }
@@ -429,12 +435,12 @@ struct TraceSim {
             const int slot = L + 32 * i;
             run[i] = sm->st[slot] == ST_RUN;
             k[i] = run[i] ? w_k(sm->gw[slot >> 3]) : 1u;
-            r[i] = sm->rem[slot];
+            r[i] = sm->rt[slot].rem;
         }
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const double qk = wp::shfl(q, (int)k[i] - 1);
-            if (run[i]) sm->rem[L + 32 * i] = wp::dsub(r[i], qk);
+            if (run[i]) sm->rt[L + 32 * i].rem = wp::dsub(r[i], qk);
         }
     }
 
@@ -481,10 +487,12 @@ struct TraceSim {
             const int slot = L + 32 * i;
             sv[i] = sm->st[slot];
             kv[i] = sv[i] == ST_RUN ? w_k(sm->gw[slot >> 3]) : 1u;
-            rv[i] = sm->rem[slot];
-            tv[i] = sm->tkey[slot];
-            jv[i] = (unsigned)sm->job[slot];
-            mv[i] = sm->mseq[slot];
+            const typename WS::RT x = sm->rt[slot];
+            rv[i] = x.rem;
+            tv[i] = x.tkey;
+            const typename WS::JM y = sm->jm[slot];
+            jv[i] = (unsigned)y.job;
+            mv[i] = y.mseq;
         }
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
@@ -496,7 +504,7 @@ struct TraceSim {
             const double f = wp::shfl(my_f, (int)kv[i] - 1);
             const double r = rv[i] < 0.0 ? 0.0 : rv[i];  // std::max(rem, 0.0)
             const double tp = wp::dadd(now, wp::dmul(r, f));
-            if (run) sm->tkey[slot] = tp;
+            if (run) sm->rt[slot].tkey = tp;
             const double t = run ? tp : tv[i];
             const uint64_t tk = time_key(t);
             const unsigned hi = armed ? (unsigned)(tk >> 32) : NONE, lo = armed ? (unsigned)tk : NONE;
@@ -674,11 +682,11 @@ struct TraceSim {
         // destroys idle ones: the GPU gains exactly the new instance's share
         const unsigned w = sm->gw[g] + share(delay > 0.0 ? ST_WAIT : ST_RUN, p, s);
         if (L == 0) {
-            sm->job[slot] = r;
+            sm->jm[slot].job = r;
             sm->mig[slot] = 0;
-            sm->rem[slot] = sv;
+            sm->rt[slot].rem = sv;
             sm->st[slot] = delay > 0.0 ? ST_WAIT : ST_RUN;  // WAIT: ServiceStart timer at ss
-            sm->tkey[slot] = ss;
+            sm->rt[slot].tkey = ss;
             jobs[r].sched = ss;
         }
         set_gpu(g, w);
@@ -721,9 +729,9 @@ struct TraceSim {
         wp::sync();
         const int fg = from_slot >> 3, fs = from_slot & 7;
         const int q = sm->prof[from_slot];
-        const int32_t r = sm->job[from_slot];
+        const int32_t r = sm->jm[from_slot].job;
         const uint8_t jst = sm->st[from_slot];
-        const double jrem = sm->rem[from_slot], jtk = sm->tkey[from_slot];
+        const double jrem = sm->rt[from_slot].rem, jtk = sm->rt[from_slot].tkey;
         const unsigned jmig = sm->mig[from_slot];
         const unsigned wf = sm->gw[fg], wt = sm->gw[tg];
         const unsigned fcb = k2w(wf);
@@ -739,15 +747,15 @@ struct TraceSim {
         if (L == 0) {
             const int dst = tg * 8 + ts;
             sm->st[dst] = jst;
-            sm->job[dst] = r;
+            sm->jm[dst].job = r;
             sm->mig[dst] = (uint16_t)(jmig + 1u);
-            sm->rem[dst] = jrem;
-            sm->tkey[dst] = jtk;
+            sm->rt[dst].rem = jrem;
+            sm->rt[dst].tkey = jtk;
             if (overlap <= 0.0) {
                 sm->st[from_slot] = ST_IDLE;  // finish_draining at once
             } else {
-                sm->tkey[from_slot] = wp::dadd(now, overlap);
-                sm->mseq[from_slot] = mseq_ctr;
+                sm->rt[from_slot].tkey = wp::dadd(now, overlap);
+                sm->jm[from_slot].mseq = mseq_ctr;
             }
         }
         if (overlap > 0.0) ++mseq_ctr;
@@ -777,7 +785,7 @@ struct TraceSim {
             unsigned kmin = NONE, cnt = 0;
             if (s == ST_RUN || s == ST_WAIT) {
                 const int q = sm->prof[sl];
-                const unsigned r = (unsigned)sm->job[sl];
+                const unsigned r = (unsigned)sm->jm[sl].job;
                 const unsigned ofc = fpc(q, own), ofm = fpm(q, own);
                 const unsigned n = count_of(q), stride = stride_of(q);
 #pragma unroll
@@ -830,7 +838,7 @@ struct TraceSim {
                         const unsigned cs = cs_of(q);
                         if (!((lazymask >> src_cs) & 1u) && lazy_cs + cs < src_cs - cs && ((pl >> q) & 1u)) {
                             const unsigned rk = rank2(w_bc(w) & ~fpc(q, s), w_bm(w) & ~fpm(q, s));
-                            const unsigned key = (rk << 27) | ((unsigned)g << 22) | (unsigned)sm->job[slot];
+                            const unsigned key = (rk << 27) | ((unsigned)g << 22) | (unsigned)sm->jm[slot].job;
                             if (key < kmin) {
                                 kmin = key;
                                 bsl = slot;
@@ -903,7 +911,7 @@ struct TraceSim {
     MSG_DI void handle_departure(int slot, bool completion) {
         wp::sync();
         const int g = slot >> 3;
-        const int32_t r = sm->job[slot];
+        const int32_t r = sm->jm[slot].job;
         const int m = sm->mig[slot];
         const unsigned w = sm->gw[g] - share(sm->st[slot], sm->prof[slot], slot & 7);
         wp::sync();
