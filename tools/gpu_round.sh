@@ -1,7 +1,8 @@
+TAG=${1:-round}
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/v15_tests.log
-timeout 600 python bench.py > gpurun_out/v15_bench.json 2> gpurun_out/v15_bench.err
-timeout 600 python bench.py --impl reference > gpurun_out/v15_bench_ref.json 2> gpurun_out/v15_bench_ref.err
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/v15_smoke.log 2>&1; echo smoke=$? >> gpurun_out/v15_smoke.log
-tail -3 gpurun_out/v15_tests.log; cat gpurun_out/v15_bench.json | head -c 600
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/${TAG}_tests.log
+timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo smoke=$? >> gpurun_out/${TAG}_smoke.log
+tail -3 gpurun_out/${TAG}_tests.log; cat gpurun_out/${TAG}_bench.json | head -c 600
