@@ -736,7 +736,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             }
             tr.has_perm = c.identity ? 0 : 1;
             if (tr.has_perm) n_perm.fetch_add(1, std::memory_order_relaxed);
-            stage_trace_arrays(b, t, tr, ha, hs, hp, hid, hperm);
+            stage_trace_arrays(b, t, tr, ha, hs, hp, hid, hperm, false);  // ids stay in the batch
         });
         CK(cudaMemcpyAsync(s->d_traces.as<DevTrace>() + d0, s->traces.data() + d0, (d1 - d0) * sizeof(DevTrace),
                            cudaMemcpyHostToDevice, st));
@@ -828,7 +828,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             msg_trace_summary& o = res->summaries[t];
             fill_summary(o, tr, x);
             handler += x.handler_events;
-            const int64_t* ids = hid + tr.job_off;
+            const int64_t* ids = tr.has_perm ? hid + tr.job_off : b->job_id + b->offsets[t];
             if (x.status == MSG_ERR_JOBS_PENDING) {
                 const int64_t jid = x.pending_rank >= 0 ? ids[x.pending_rank] : -1;
                 res->messages[t] = "JobsPending: job " + std::to_string(jid) + " did not complete";

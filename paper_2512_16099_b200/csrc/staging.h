@@ -185,15 +185,17 @@ inline TraceCheck check_trace(const msg_trace_batch* b, uint32_t t) {
 // Copy one validated trace into the rank-order (job-id order) arrays; for
 // traces whose ids are not increasing, also the arrival-order permutation
 // (arrivals pop in (time, job id) order, TimerLater sim.cpp:49-56).
+// copy_ids = false: an identity-order trace's ids are not copied (the caller
+// reads them from the batch itself, which outlives its use).
 inline void stage_trace_arrays(const msg_trace_batch* b, uint32_t t, const DevTrace& tr, double* ha, double* hs,
-                               uint8_t* hp, int64_t* hid, uint32_t* hperm) {
+                               uint8_t* hp, int64_t* hid, uint32_t* hperm, bool copy_ids = true) {
     const uint64_t lo = b->offsets[t];
     const uint64_t o = tr.job_off;
     const uint32_t n = tr.n_jobs;
     if (!tr.has_perm) {
         std::memcpy(ha + o, b->arrival_s + lo, n * sizeof(double));
         std::memcpy(hs + o, b->service_s + lo, n * sizeof(double));
-        std::memcpy(hid + o, b->job_id + lo, n * sizeof(int64_t));
+        if (copy_ids) std::memcpy(hid + o, b->job_id + lo, n * sizeof(int64_t));
         for (uint32_t i = 0; i < n; ++i) hp[o + i] = (uint8_t)b->profile[lo + i];
         return;
     }
