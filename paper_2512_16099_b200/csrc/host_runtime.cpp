@@ -628,7 +628,7 @@ constexpr int kMaxPipeChunks = 8;  // == size of msg_engine::pstream
 
 // Chunk boundaries over the device traces: relative chunk weights from
 // MSG_PIPE_W ("1,2,2,3"; tuning), else kDefaultPipe equal chunks.
-constexpr int kDefaultPipe = 4;
+constexpr int kDefaultPipe = 8;  // r01-v18 sweep (tools/pipe_tune.py): 8 equal chunks ~4% faster than 4 on the C2 e2e
 int pipe_bounds(uint32_t T, uint32_t* d0s) {
     double w[kMaxPipeChunks];
     int n = 0;
