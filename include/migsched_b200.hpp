@@ -36,6 +36,15 @@ public:
     Error(std::string code, const std::string& what) : std::runtime_error(code + ": " + what), code_(std::move(code)) {}
     const std::string& code() const noexcept { return code_; }
 
+    // From a library message, which is already the reference's what() text
+    // ("Code: message"): what() of the result equals the reference's.
+    static Error from_library(int status, const char* text) {
+        std::string code = msg_status_name(status), m = text ? text : "";
+        const std::string prefix = code + ": ";
+        if (m.rfind(prefix, 0) == 0) m.erase(0, prefix.size());
+        return Error(std::move(code), m);
+    }
+
 private:
     std::string code_;
 };
@@ -228,12 +237,12 @@ public:
         msg_batch_result* r = nullptr;
         const uint32_t flags = MSG_OUT_JOBS | (with_events ? MSG_OUT_EVENTS | MSG_OUT_TIMELINE : 0u);
         const msg_status st = msg_run_batch(eng_.get(), &b, &ch.c, 1, flags, &r);
-        if (st != MSG_OK) throw Error(msg_status_name(st), msg_engine_last_error(eng_.get()));
+        if (st != MSG_OK) throw Error::from_library(st, msg_engine_last_error(eng_.get()));
         std::unique_ptr<msg_batch_result, void (*)(msg_batch_result*)> hold(r, msg_result_free);
         std::vector<SimResult> out(traces.size());
         for (uint32_t t = 0; t < b.n_traces; ++t) {
             const msg_trace_summary* s = msg_result_summary(r, t);
-            if (s->status != MSG_OK) throw Error(msg_status_name(s->status), msg_result_message(r, t));
+            if (s->status != MSG_OK) throw Error::from_library(s->status, msg_result_message(r, t));
             SimReport& rep = out[t].report;
             rep.mean_wait_s = s->mean_wait_s;
             rep.mean_execution_s = s->mean_execution_s;
@@ -282,10 +291,7 @@ inline std::vector<Job> load_trace(const std::string& path) {
     msg_trace_file* f = nullptr;
     char msg[512];
     const msg_status st = msg_trace_load(path.c_str(), &f, msg, sizeof msg);
-    if (st != MSG_OK) {
-        const std::string m(msg), code = msg_status_name(st);
-        throw Error(code, m.size() > code.size() + 2 ? m.substr(code.size() + 2) : m);
-    }
+    if (st != MSG_OK) throw Error::from_library(st, msg);
     const uint64_t n = msg_trace_file_jobs(f);
     std::vector<Job> jobs(n);
     const int64_t* id = msg_trace_file_ids(f);

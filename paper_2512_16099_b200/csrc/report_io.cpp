@@ -13,6 +13,12 @@
 // building a JSON document.
 #include <nlohmann/json.hpp>
 
+// The byte format of every double written here is nlohmann 3.11.3's
+// to_chars, the version the reference was built and its goldens made with.
+static_assert(NLOHMANN_JSON_VERSION_MAJOR == 3 && NLOHMANN_JSON_VERSION_MINOR == 11 &&
+                  NLOHMANN_JSON_VERSION_PATCH == 3,
+              "report_io.cpp needs nlohmann/json 3.11.3 (third_party/nlohmann)");
+
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>

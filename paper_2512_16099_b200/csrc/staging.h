@@ -20,6 +20,8 @@ namespace msgk {
 inline constexpr uint32_t kMaxGpusEnsemble = 32;          // WarpSmem<8>
 inline constexpr uint64_t kMaxJobsPerTrace = 1ull << 22;  // key layout (engine_core.cuh)
 
+inline constexpr const char* kProfileNames[] = {"7g.40gb", "4g.20gb", "3g.20gb",  // profiles.cpp:8-15
+                                                "2g.10gb", "1g.10gb", "1g.5gb"};
 inline constexpr const char* kStatusNames[] = {"Ok",          "InvalidPlacement", "SlicesBusy",   "UnknownJob", "UnknownGpu",
                               "NotLazy",     "UnknownProfile",   "BadThreshold", "BadConfig",  "BadSpec",
                               "TraceUnsorted", "BadConcurrency", "JobsPending",  "ParseError"};
@@ -61,7 +63,8 @@ inline CfgState validate_config(const msg_config& c) {
                 // add_idle_instance -> slice_footprint (profiles.cpp:49-57)
                 if (st < 0 || st > 7 || !((host_startmask(p) >> st) & 1u))
                     return fail(MSG_ERR_INVALID_PLACEMENT, "placement (" + std::to_string(st) + "," +
-                                                               std::to_string(host_ms(p)) + ") is not valid");
+                                                               std::to_string(host_ms(p)) + ") is not valid for profile " +
+                                                               kProfileNames[p]);
                 if (host_fpm(p, st) & used)  // gpu.cpp:103-113
                     return fail(MSG_ERR_SLICES_BUSY,
                                 "layout instance overlaps an existing instance on GPU " + std::to_string(g));

@@ -85,7 +85,7 @@ def _check(st: int, eng=None):
         msg = ""
         if eng is not None and eng._h:
             msg = lib().msg_engine_last_error(eng._h).decode()
-        raise MigschedError(abi.STATUS_NAMES.get(st, str(st)), msg)
+        raise MigschedError.from_library(abi.STATUS_NAMES.get(st, str(st)), msg)
 
 
 class Staged:
@@ -204,17 +204,22 @@ class _Mem:
 
 
 def _view(ptr, n, dtype, owner):
-    """Zero-copy numpy view of n records at ptr, keeping `owner` alive."""
+    """Zero-copy, read-only numpy view of n records at ptr, keeping `owner`
+    (the whole batch's result buffers) alive; .copy() for an independent,
+    writable array."""
     if not ptr or n == 0:
         return np.zeros(0, dtype)
-    return np.asarray(_Mem(ptr, n * dtype.itemsize, owner)).view(dtype)
+    v = np.asarray(_Mem(ptr, n * dtype.itemsize, owner)).view(dtype)
+    v.flags.writeable = False
+    return v
 
 
 class BatchResult:
     """Results of one batch (msg_batch_result), decoded lazily.
 
     `summaries` (SUMMARY_DTYPE[n]) and `jobs` (JOB_DTYPE, all traces,
-    `job_offsets`) are zero-copy views into the library's buffers; indexing
+    `job_offsets`) are zero-copy, read-only views into the library's
+    buffers (any view keeps the whole batch's buffers alive); indexing
     or iterating yields per-trace TraceResult objects shaped like the
     reference's SimResult."""
 
@@ -270,14 +275,20 @@ def _decode(r, flags: int) -> BatchResult:
     return BatchResult(r, flags)
 
 
-_default_engine: Optional[Engine] = None
+_default_engines: dict = {}
 
 
-def default_engine() -> Engine:
-    global _default_engine
-    if _default_engine is None:
-        _default_engine = Engine(0)
-    return _default_engine
+def default_engine(device: Optional[int] = None) -> Engine:
+    """One cached Engine per CUDA device; `device` defaults to this
+    process's device (torch's current device, else LOCAL_RANK, else 0)."""
+    if device is None:
+        from .ensemble import local_device
+
+        device = local_device()
+    eng = _default_engines.get(device)
+    if eng is None:
+        eng = _default_engines[device] = Engine(device)
+    return eng
 
 
 def run(trace, cfg: SimConfig, out_flags: int = abi.OUT_JOBS | abi.OUT_EVENTS | abi.OUT_TIMELINE) -> TraceResult:
@@ -338,7 +349,7 @@ def load_trace(path: str) -> TraceBatch:
     st = L.msg_trace_load(os.fsencode(path), C.byref(h), msg, len(msg))
     if st != 0:
         text = msg.value.decode(errors="replace")
-        raise MigschedError(abi.STATUS_NAMES.get(st, str(st)), text.split(": ", 1)[-1])
+        raise MigschedError.from_library(abi.STATUS_NAMES.get(st, str(st)), text)
     try:
         n = int(L.msg_trace_file_jobs(h))
 

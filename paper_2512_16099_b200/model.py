@@ -48,6 +48,14 @@ class MigschedError(RuntimeError):
     def __init__(self, code: str, message: str = ""):
         super().__init__(f"{code}: {message}" if message else code)
         self.code = code
+        self.message = message
+
+    @classmethod
+    def from_library(cls, code: str, text: str) -> "MigschedError":
+        """From a library message, which is the reference's what() text
+        ("Code: message"; include/migsched_b200.h): str(e) == what()."""
+        prefix = code + ": "
+        return cls(code, text[len(prefix):] if text.startswith(prefix) else text)
 
 
 @dataclass

@@ -3,8 +3,10 @@
 A TraceResult holds numpy views of the decoded records (include/
 migsched_b200.h): `summary` (SUMMARY_DTYPE record), `per_job` (JOB_DTYPE,
 job-id order like metrics()), `events` (EVENT_DTYPE, the EventLog) and
-`frag_timeline` (TIMELINE_DTYPE).  Arrays are copies, independent of the
-library-owned result buffers.
+`frag_timeline` (TIMELINE_DTYPE).  For results of the CUDA engine the arrays
+are zero-copy, read-only views into the library-owned buffers of the whole
+batch (engine.BatchResult): a kept TraceResult keeps those buffers alive;
+call .copy() on an array for an independent, writable one.
 """
 from __future__ import annotations
 
@@ -55,7 +57,7 @@ class TraceResult:
 
     def raise_for_status(self) -> "TraceResult":
         if self.status != 0:
-            raise MigschedError(self.code, self.message)
+            raise MigschedError.from_library(self.code, self.message)
         return self
 
     # SimReport-style accessors (sim.hpp:75-86)

@@ -220,7 +220,8 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
     o.timeline_sum = sum.tl_sum;
     r->status = sum.status;
     if (sum.status != MSG_OK) {
-        r->message = "JobsPending";
+        r->message = "JobsPending: job " + std::to_string(sum.pending_rank >= 0 ? hid[sum.pending_rank] : -1) +
+                     " did not complete";
         return r;
     }
     for (uint32_t k = 0; k < tr.n_jobs; ++k) {

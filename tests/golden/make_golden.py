@@ -80,6 +80,54 @@ def cases():
     yield "ties_g3", ties, 2, SimConfig(gpu_count=3, reconfig_latency_s=0.25, migration_overlap_s=1.0)
 
 
+def aggregates(only=None):
+    """Ensemble aggregates (full-size checks on the GPU box): C2 and C5 at
+    4096 seeds and the whole C3 grid (4 combos x 5 loads
+    x 1024 seeds, run_ablation's combos, tools/migsched.cpp:64-99).  `only`
+    recomputes a subset of the tags and keeps the other stored entries."""
+    path = os.path.join(HERE, "aggregates.json")
+    agg = json.load(open(path)) if os.path.exists(path) else {}
+
+    def aggregate(tag, spec, seeds, cfg):
+        if only is not None and tag not in only:
+            return
+        b = rb.ref_generate_batch(spec, seeds) if spec is not None else None
+        s, _ = rb.ref_run_batch_summaries(b, [cfg], threads=0)
+        agg[tag] = {
+            "seeds": [int(seeds[0]), int(seeds[-1])],
+            "spec": spec.__dict__,
+            "cfg": cfg_dict(cfg),
+            "handler_events": int(s["handler_events"].sum()),
+            "migrations": int(s["migration_count"].sum()),
+            "reconfig_ops": int(s["reconfig_op_count"].sum()),
+            "dequeues": int(s["dequeue_count"].sum()),
+            "sum_mean_turnaround": float(np.add.reduce(s["mean_turnaround_s"])),
+            "mean_turnaround_bits": s["mean_turnaround_s"].tobytes().hex()[:0],
+            "checksum_turnaround": s["mean_turnaround_s"].view(np.uint64).sum(dtype=np.uint64).item(),
+            "checksum_makespan": s["workload_makespan_s"].view(np.uint64).sum(dtype=np.uint64).item(),
+            "checksum_timeline": s["timeline_sum"].view(np.uint64).sum(dtype=np.uint64).item(),
+        }
+
+    aggregate("c2_4096", preset("normal25"), list(range(4096)), SimConfig(gpu_count=8))
+    c5 = WorkloadSpec(mean_interarrival_s=0.4, median_s=4.0, sigma=1.2, profile_mix=(0.5, 0.3, 0.2, 0.0))
+    aggregate("c5_4096", c5, list(range(4096)), SimConfig(gpu_count=8, sched=SchedulerConfig(threshold=0.3),
+                                                          migration_overlap_s=0.5, reconfig_latency_s=0.1))
+    for ia in C3_LOADS:
+        for i, f in enumerate(C3_COMBOS):
+            sp = preset("normal25")
+            sp.mean_interarrival_s = float(ia)
+            aggregate(f"c3_ia{ia}_combo{i}", sp, list(range(1024)), SimConfig(gpu_count=4, sched=SchedulerConfig(
+                features=f, static_layout=None if f.dynamic_partitioning else static_layout_preset("static-a"))))
+    with open(path, "w") as f:
+        json.dump(agg, f, indent=1)
+    return agg
+
+
+C3_LOADS = (10, 15, 25, 35, 50)
+C3_COMBOS = (FeatureFlags(False, False, False), FeatureFlags(True, False, False),
+             FeatureFlags(True, True, False), FeatureFlags(True, True, True))
+
+
 def main():
     arrays = {}
     meta = {}
@@ -117,41 +165,14 @@ def main():
     with open(os.path.join(HERE, "runs.json"), "w") as f:
         json.dump(meta, f, indent=1)
 
-    # Ensemble aggregates (full-size checks on the GPU box).
-    agg = {}
-
-    def aggregate(tag, spec, seeds, cfg):
-        b = rb.ref_generate_batch(spec, seeds) if spec is not None else None
-        s, _ = rb.ref_run_batch_summaries(b, [cfg], threads=0)
-        agg[tag] = {
-            "seeds": [int(seeds[0]), int(seeds[-1])],
-            "spec": spec.__dict__,
-            "cfg": cfg_dict(cfg),
-            "handler_events": int(s["handler_events"].sum()),
-            "migrations": int(s["migration_count"].sum()),
-            "reconfig_ops": int(s["reconfig_op_count"].sum()),
-            "dequeues": int(s["dequeue_count"].sum()),
-            "sum_mean_turnaround": float(np.add.reduce(s["mean_turnaround_s"])),
-            "mean_turnaround_bits": s["mean_turnaround_s"].tobytes().hex()[:0],
-            "checksum_turnaround": s["mean_turnaround_s"].view(np.uint64).sum(dtype=np.uint64).item(),
-            "checksum_makespan": s["workload_makespan_s"].view(np.uint64).sum(dtype=np.uint64).item(),
-            "checksum_timeline": s["timeline_sum"].view(np.uint64).sum(dtype=np.uint64).item(),
-        }
-
-    aggregate("c2_4096", preset("normal25"), list(range(4096)), SimConfig(gpu_count=8))
-    c5 = WorkloadSpec(mean_interarrival_s=0.4, median_s=4.0, sigma=1.2, profile_mix=(0.5, 0.3, 0.2, 0.0))
-    aggregate("c5_4096", c5, list(range(4096)), SimConfig(gpu_count=8, sched=SchedulerConfig(threshold=0.3),
-                                                          migration_overlap_s=0.5, reconfig_latency_s=0.1))
-    for i, f in enumerate([FeatureFlags(False, False, False), FeatureFlags(True, False, False),
-                           FeatureFlags(True, True, False), FeatureFlags(True, True, True)]):
-        sp = preset("normal25")
-        sp.mean_interarrival_s = 25.0
-        aggregate(f"c3_ia25_combo{i}", sp, list(range(1024)), SimConfig(gpu_count=4, sched=SchedulerConfig(
-            features=f, static_layout=None if f.dynamic_partitioning else static_layout_preset("static-a"))))
-    with open(os.path.join(HERE, "aggregates.json"), "w") as f:
-        json.dump(agg, f, indent=1)
+    agg = aggregates()
     print("wrote", len(meta), "runs and", len(agg), "aggregates")
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["aggregates"]:
+        print("aggregates:", len(aggregates()))
+    elif sys.argv[1:2] == ["aggregates"]:
+        print("aggregates:", len(aggregates(only=set(sys.argv[2:]))))
+    else:
+        main()

@@ -46,3 +46,19 @@ def test_error_codes(name, trace, cfg, code):
         assert rb.ref_run_batch_results(b, [cfg])[0].code == code
     if rb.port_available():
         assert rb.port_run_batch_results(b, [cfg])[0].code == code
+
+
+@pytest.mark.skipif(not rb.ref_available(), reason="reference library not built")
+@pytest.mark.parametrize("name,trace,cfg,code", CASES, ids=[c[0] for c in CASES])
+def test_error_text_is_reference_what(name, trace, cfg, code):
+    """str(MigschedError) raised for a failed trace equals the reference's
+    Error::what() ("Code: message", error.hpp:10-19) — the code appears once."""
+    from paper_2512_16099_b200.model import MigschedError
+
+    b = TraceBatch.from_traces([trace])
+    got = emu_run_batch_results(b, [cfg])[0]
+    ref = rb.ref_run_batch_results(b, [cfg])[0]
+    with pytest.raises(MigschedError) as e:
+        got.raise_for_status()
+    assert e.value.code == code
+    assert str(e.value) == ref.message
