@@ -33,6 +33,7 @@
 // reference consumes (sim.cpp:347-349, ComplexityStats).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <deque>
@@ -107,9 +108,32 @@ inline void to_slots(const migsched::GpuState& g, msg_instance* s8) {
     }
 }
 
-inline std::vector<msg_instance> to_slots(std::span<const migsched::GpuState> gpus) {
+// A cluster snapshot whose busy jobs carry surrogate ids gpu * 8 + (rank of
+// the job id among the GPU's busy jobs).  The reference's decisions compare
+// job ids only between jobs of one GPU (plan_intra: (cost, job, start)) or
+// after the GPU index (plan_inter: (cost, gpu, job)); schedule and
+// try_dequeue never compare them.  So the surrogates give the same
+// decisions while the reference's callers may reuse ids across GPUs (its
+// oracle suites do, oracle.cpp:117-125).  `orig` maps surrogate -> id.
+inline std::vector<msg_instance> to_slots(std::span<const migsched::GpuState> gpus, std::vector<int64_t>* orig) {
     std::vector<msg_instance> s(gpus.size() * 8 + 8);
-    for (size_t g = 0; g < gpus.size(); ++g) to_slots(gpus[g], s.data() + 8 * g);
+    if (orig) orig->assign(gpus.size() * 8, -1);
+    for (size_t g = 0; g < gpus.size(); ++g) {
+        msg_instance* s8 = s.data() + 8 * g;
+        to_slots(gpus[g], s8);
+        int64_t ids[8];
+        int n = 0;
+        for (int k = 0; k < 8; ++k)
+            if (s8[k].state == MSG_SLOT_BUSY) ids[n++] = s8[k].job;
+        std::sort(ids, ids + n);
+        for (int k = 0; k < 8; ++k) {
+            if (s8[k].state != MSG_SLOT_BUSY) continue;
+            const int64_t r = std::lower_bound(ids, ids + n, s8[k].job) - ids;
+            const int64_t sur = static_cast<int64_t>(g) * 8 + r;
+            if (orig) (*orig)[static_cast<size_t>(sur)] = s8[k].job;
+            s8[k].job = sur;
+        }
+    }
     return s;
 }
 
@@ -137,7 +161,7 @@ inline migsched::ScheduleDecision decide(int32_t op, const migsched::JobRequest&
         throw migsched::Error("UnknownProfile", "job " + std::to_string(job.id) + " requests an unknown profile");
     std::lock_guard<std::mutex> lk(box().mu);
     msg_engine* eng = engine();
-    const std::vector<msg_instance> slots = to_slots(gpus);
+    const std::vector<msg_instance> slots = to_slots(gpus, nullptr);
     const int32_t prof = p;
     const msg_sched_config c = sched_config(cfg);
     msg_decision d{};
@@ -183,7 +207,8 @@ inline migsched::MigrationPlan plan(int32_t op, std::vector<migsched::GpuState>&
     if (!enabled) return {};
     std::lock_guard<std::mutex> lk(box().mu);
     msg_engine* eng = engine();
-    const std::vector<msg_instance> before = to_slots(std::span<const migsched::GpuState>(gpus));
+    std::vector<int64_t> orig;
+    const std::vector<msg_instance> before = to_slots(std::span<const migsched::GpuState>(gpus), &orig);
     const int32_t G = static_cast<int32_t>(gpus.size());
     const int32_t g = gpu_id;
     uint32_t cap = 64;
@@ -211,7 +236,7 @@ inline migsched::MigrationPlan plan(int32_t op, std::vector<migsched::GpuState>&
     for (int32_t k = 0; k < s.n_moves; ++k) {
         const msg_move& m = moves[static_cast<size_t>(k)];
         migsched::MigrationMove mv;
-        mv.job = m.job;
+        mv.job = orig[static_cast<size_t>(m.job)];
         mv.profile = static_cast<migsched::ProfileId>(m.profile);
         const int size = migsched::profile(mv.profile).size;
         mv.from_gpu = m.from_gpu;
@@ -292,12 +317,13 @@ inline std::vector<migsched::DequeueResult> try_dequeue(std::deque<migsched::Job
     {
         std::lock_guard<std::mutex> lk(policy_detail::box().mu);
         msg_engine* eng = policy_detail::engine();
-        std::vector<msg_instance> slots = policy_detail::to_slots(std::span<const migsched::GpuState>(gpus));
+        std::vector<msg_instance> slots =
+            policy_detail::to_slots(std::span<const migsched::GpuState>(gpus), nullptr);
         const uint64_t qoff[2] = {0, queue.size()};
-        std::vector<int64_t> qjob;
+        std::vector<int64_t> qjob;  // surrogate ids past the busy ones (placement never compares ids)
         std::vector<int32_t> qprof;
         for (const auto& j : queue) {
-            qjob.push_back(j.id);
+            qjob.push_back(static_cast<int64_t>(gpus.size() * 8 + qjob.size()));
             qprof.push_back(static_cast<int32_t>(j.profile));
         }
         const msg_sched_config c = policy_detail::sched_config(cfg);

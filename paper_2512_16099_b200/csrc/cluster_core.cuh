@@ -106,6 +106,7 @@ template <bool DETAIL>
 struct ClusterSim {
     BlockScratch* sc;
     const DevTables* tb;
+    const uint16_t* stab;  // per-word placement table (host_tables.h, build_score_table) or null
     // per slot (global slot index 8g + s)
     uint8_t* st;
     uint8_t* prof;
@@ -382,6 +383,7 @@ struct ClusterSim {
         bph = 0;
         sc = scratch;
         tb = tables;
+        stab = a.score_tab;
         S = wp::cluster_size();
         sh = wp::cluster_rank();
         D = a.n_dev < 1 ? 1u : a.n_dev;
@@ -747,7 +749,31 @@ struct ClusterSim {
         const bool lb = (cflags & CF_LB) != 0;
         uint64_t kmin = ~0ull;
         unsigned nl = 0, nb = 0;
+        // With load balancing and dynamic partitioning, a GPU without a
+        // draining instance (blocked memory == busy memory) is scored by one
+        // lookup in the scorer's per-word table (score.cu: lowest
+        // post-placement rank, the starts reaching it, the candidate count);
+        // the rest take the per-start loop below.
+        const uint16_t* Tp = (lb && dyn && stab) ? stab + p * 2048 : nullptr;
         for (int g = g_lo + (int)T; g < g_hi; g += (int)NT) {
+            if (Tp) {
+                const unsigned wd = gw[g - g_lo];
+                const unsigned bm = w_bm(wd);
+                if (w_km(wd) == bm) {
+                    const unsigned pc = (unsigned)wp::popc(w_bc(wd));
+                    const unsigned e = Tp[pc * 256u + bm];
+                    const unsigned cnt = e & 7u;
+                    const unsigned lazy = (lazymask >> pc) & 1u;
+                    const unsigned mm = (e >> 3) & 0x7Fu, r = mm & (gx[g - g_lo] >> pb);
+                    const unsigned j = (unsigned)wp::ffs(r ? r : mm) - 1u;
+                    const uint64_t k = ((uint64_t)(lazy ^ 1u) << 47) | ((uint64_t)(e >> 10) << 42) |
+                                       ((uint64_t)(r ? 0u : 1u) << 41) | ((uint64_t)g << 3) | (uint64_t)(j * stride);
+                    kmin = cnt && k < kmin ? k : kmin;
+                    nl += lazy ? cnt : 0u;
+                    nb += lazy ? 0u : cnt;
+                    continue;
+                }
+            }
             const unsigned wd = gw[g - g_lo];
             const unsigned ex = gx[g - g_lo] >> pb;
             const unsigned lazy = (lazymask >> wp::popc(w_bc(wd))) & 1u;

@@ -8,15 +8,14 @@ namespace msgk {
 
 struct ScoreArgs {
     const DevTables* tables;
+    const uint16_t* stab;     // build_score_table (host_tables.h): [profile][popc busy_c][busy_m]
     const uint64_t* words;    // n * G packed GPU words (msg_pack_gpu_word)
     const uint8_t* profile;   // n job profiles
     uint64_t* out;            // 2 per snapshot: argmin key, (lazy << 32 | busy) candidate counts
     uint64_t G;
     uint32_t n;
     uint32_t lb, dyn, lazymask;
-    // scratch (n + 1 + n words; the first n unused): the count and list of
-    // snapshots pass 1 left without a Lazy candidate (score_reduce_kernel)
-    uint32_t* scratch;
+    uint32_t* scratch;        // unused (kept for the ABI's scratch sizing)
     uint64_t* items;  // TMA path: 2 words per item (score_items_bytes)
 };
 

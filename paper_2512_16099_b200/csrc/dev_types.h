@@ -151,6 +151,7 @@ struct SimArgs {
     const DevConfig* configs;
     const uint32_t* init_slots;
     const DevTables* tables;
+    const uint16_t* score_tab;  // the arrival scorer's per-word table (host_tables.h, build_score_table), or null
     const double* arrival;   // rank order
     const double* service;
     const uint8_t* profile;

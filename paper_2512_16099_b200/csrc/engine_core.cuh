@@ -417,33 +417,6 @@ struct TraceSim {
         t_prev = 0.0;
     }
 
-    // advance_all (sim.cpp:153-165): rem -= dt / slowdown(k) for every running
-    // job.  dt is uniform (see t_prev), so the <= 7 distinct quotients are
-    // computed once, lane k-1 holding dt / slowdown(k), and fetched by shuffle.
-    MSG_DI void advance_all() {
-        const double dt = wp::dsub(now, t_prev);
-        t_prev = now;
-        if (!(dt > 0.0)) return;  // dt <= 0: last_update = now only
-        const double q = wp::ddiv(dt, my_f);
-        wp::sync();
-        // every load before the first store (the stores could alias them)
-        bool run[SPL];
-        unsigned k[SPL];
-        double r[SPL];
-#pragma unroll
-        for (int i = 0; i < SPL; ++i) {
-            const int slot = L + 32 * i;
-            run[i] = sm->st[slot] == ST_RUN;
-            k[i] = run[i] ? w_k(sm->gw[slot >> 3]) : 1u;
-            r[i] = sm->rt[slot].rem;
-        }
-#pragma unroll
-        for (int i = 0; i < SPL; ++i) {
-            const double qk = wp::shfl(q, (int)k[i] - 1);
-            if (run[i]) sm->rt[L + 32 * i].rem = wp::dsub(r[i], qk);
-        }
-    }
-
     // sample_timeline (sim.cpp:177-181): sequential sum in GPU order / G.
     // The running prefix sums are kept, so after a change on GPU g only the
     // tail g .. G-1 of the chain is re-added (same additions, same order).
@@ -469,19 +442,25 @@ struct TraceSim {
 
     // -------------------------------------------------------------- events
     // reschedule_completions (sim.cpp:167-175) fused with the next timer pop
-    // (Engine::execute, sim.cpp:123-141): every Running slot's prediction
-    // now + max(rem,0)*f is recomputed and stored, and the same pass forms
-    // the (time, kind, job, push seq) keys of all armed timers.  Returns -1
-    // none, 0 completion, 1 migration end, 2 service start, 3 arrival.
+    // (Engine::execute, sim.cpp:123-141) and with the popped handler's
+    // advance_all (sim.cpp:153-165, the first step of every handler): one
+    // pass over the slots recomputes every Running slot's prediction
+    // now + max(rem,0)*f and forms the (time, kind, job, push seq) keys of
+    // all armed timers; once the warp-wide argmin fixes the new `now`, the
+    // same registers give rem -= dt / slowdown(k), and each Running slot's
+    // (rem, prediction) pair is stored with one 16-byte store.  The <= 7
+    // distinct quotients dt / slowdown(k) are computed once (lane k-1) and
+    // fetched by shuffle; dt is warp-uniform (see t_prev).  Returns -1 none,
+    // 0 completion, 1 migration end, 2 service start, 3 arrival.
     MSG_DI int resched_next(int& ev_slot) {
         wp::sync();
         unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
         int bsl = -1;
         double bt = 0.0;
-        // every load before the first store (the tkey stores could alias them)
+        // every load before the first store (the stores could alias them)
         uint8_t sv[SPL];
         unsigned kv[SPL], jv[SPL], mv[SPL];
-        double rv[SPL], tv[SPL];
+        double rv[SPL], tv[SPL], pv[SPL];
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
@@ -504,7 +483,7 @@ struct TraceSim {
             const double f = wp::shfl(my_f, (int)kv[i] - 1);
             const double r = rv[i] < 0.0 ? 0.0 : rv[i];  // std::max(rem, 0.0)
             const double tp = wp::dadd(now, wp::dmul(r, f));
-            if (run) sm->rt[slot].tkey = tp;
+            pv[i] = tp;
             const double t = run ? tp : tv[i];
             const uint64_t tk = time_key(t);
             const unsigned hi = armed ? (unsigned)(tk >> 32) : NONE, lo = armed ? (unsigned)tk : NONE;
@@ -523,29 +502,44 @@ struct TraceSim {
         }
         const unsigned mhi = wp::rmin(bhi);
         const bool have_arrival = a_idx < N;
+        int kind = 3;
         if (mhi == NONE) {
-            if (!have_arrival) return -1;
+            if (!have_arrival) return -1;  // the run is over: predictions are no longer needed
             now = a_t;
-            return 3;
-        }
-        const unsigned mlo = wp::rmin(bhi == mhi ? blo : NONE);
-        const unsigned mtie = wp::rmin((bhi == mhi && blo == mlo) ? btie : NONE);
-        bool match = bhi == mhi && blo == mlo && btie == mtie;
-        if ((mtie >> 28) == 1u) {  // same job, same time MigrationEnds: push order
-            const unsigned mms = wp::rmin(match ? bms : NONE);
-            match = match && bms == mms;
-        }
-        if (have_arrival) {
-            const uint64_t sk = ((uint64_t)mhi << 32) | mlo;
-            if (time_key(a_t) < sk) {  // arrivals rank last on equal time
+        } else {
+            const unsigned mlo = wp::rmin(bhi == mhi ? blo : NONE);
+            const unsigned mtie = wp::rmin((bhi == mhi && blo == mlo) ? btie : NONE);
+            bool match = bhi == mhi && blo == mlo && btie == mtie;
+            if ((mtie >> 28) == 1u) {  // same job, same time MigrationEnds: push order
+                const unsigned mms = wp::rmin(match ? bms : NONE);
+                match = match && bms == mms;
+            }
+            if (have_arrival && time_key(a_t) < (((uint64_t)mhi << 32) | mlo)) {  // arrivals rank last on equal time
                 now = a_t;
-                return 3;
+            } else {
+                const int wl = wp::ffs(wp::ballot(match)) - 1;
+                ev_slot = wp::shfl(bsl, wl);
+                now = wp::shfl(bt, wl);
+                kind = (int)(mtie >> 28);
             }
         }
-        const int wl = wp::ffs(wp::ballot(match)) - 1;
-        ev_slot = wp::shfl(bsl, wl);
-        now = wp::shfl(bt, wl);
-        return (int)(mtie >> 28);
+        // advance_all of the popped handler: dt <= 0 leaves rem unchanged
+        const double dt = wp::dsub(now, t_prev);
+        t_prev = now;
+        const bool adv = dt > 0.0;
+        double q = 0.0;
+        if (adv) q = wp::ddiv(dt, my_f);
+#pragma unroll
+        for (int i = 0; i < SPL; ++i) {
+            const double qk = wp::shfl(q, (int)kv[i] - 1);
+            if (sv[i] == ST_RUN) {
+                typename WS::RT x;
+                x.rem = adv ? wp::dsub(rv[i], qk) : rv[i];
+                x.tkey = pv[i];
+                sm->rt[L + 32 * i] = x;
+            }
+        }
+        return kind;
     }
 
     // ------------------------------------------------------------ schedule
@@ -945,10 +939,11 @@ struct TraceSim {
     MSG_DI void run() {  // Engine::execute (sim.cpp:123-141)
         for (;;) {
             int slot = -1;
-            const int kind = resched_next(slot);  // reschedules the previous handler's completions
+            // reschedules the previous handler's completions, pops the next
+            // timer and advances every running job to it
+            const int kind = resched_next(slot);
             if (kind < 0) break;
             ++n_handler;
-            advance_all();
             if (kind == 3) handle_arrival();
             else if (kind == 2) handle_service_start(slot);
             else handle_departure(slot, kind == 0);

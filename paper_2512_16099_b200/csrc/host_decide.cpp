@@ -119,6 +119,7 @@ msg_status msg_score_device(msg_engine* eng, uint32_t n, int64_t G, const uint64
     cudaSetDevice(eng->device);
     ScoreArgs a{};
     a.tables = eng->tables.as<DevTables>();
+    a.stab = eng->score_tab.as<uint16_t>();
     a.words = d_words;
     a.profile = d_profile;
     a.out = d_out;

@@ -395,6 +395,7 @@ SimArgs make_args(msg_engine* eng, msg_staged* s) {
     a.configs = s->d_configs.as<DevConfig>();
     a.init_slots = s->d_init.as<uint32_t>();
     a.tables = eng->tables.as<DevTables>();
+    a.score_tab = eng->score_tab.as<uint16_t>();
     a.arrival = s->d_arrival.as<double>();
     a.service = s->d_service.as<double>();
     a.profile = s->d_profile.as<uint8_t>();
@@ -905,6 +906,10 @@ msg_status msg_engine_create(int device, msg_engine** out) {
     if (build_tables(&t) != 31) return MSG_ERR_INVALID_ARGUMENT;
     CK(e->tables.ensure(sizeof(DevTables)));
     CK(cudaMemcpy(e->tables.p, &t, sizeof(DevTables), cudaMemcpyHostToDevice));
+    std::vector<uint16_t> stab(kScoreTab);
+    build_score_table(t, stab.data());
+    CK(e->score_tab.ensure(sizeof(uint16_t) * kScoreTab));
+    CK(cudaMemcpy(e->score_tab.p, stab.data(), sizeof(uint16_t) * kScoreTab, cudaMemcpyHostToDevice));
     *out = e.release();
     return MSG_OK;
 }

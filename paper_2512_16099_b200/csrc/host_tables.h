@@ -69,6 +69,44 @@ inline void enumerate_reachable(int first, unsigned bc, unsigned bm, std::vector
 // Ranks are assigned over the reachable pairs only (31 distinct costs, the
 // survey's exhaustive count); unreachable table entries get rank 31, which
 // no engine state can look up.
+// The arrival scorer's per-word table (score.cu): for job profile p and a
+// GPU word with popc(busy_c) = pc and busy memory = blocked memory = bm (no
+// draining instance), candidate_starts + the per-start cost of schedule()
+// (scheduler.cpp:19-28,57-66) folded into one u16 entry:
+//   bits 10-14  the lowest post-placement cost rank over the available
+//               starts (cost2rank[min(pc + cs, 7)][bm | fm(start)])
+//   bits 3-9    which starts (ordinals j, start = j * stride) reach it
+//   bits 0-2    how many starts are available (the candidate count, <= 7)
+// Bit 15 (the Lazy/Busy pass) is filled in per launch from the threshold
+// (score.cu, fast_tab_init).  A word without an available start gets
+// kScoreNoCand: rank field 31 and, with the pass bit, a key above every
+// real one; minimum-start mask 1 keeps the start decode in range; count 0.
+constexpr int kScoreTab = 6 * 8 * 256;
+constexpr uint16_t kScoreNoCand = 0x7C08;
+inline void build_score_table(const DevTables& t, uint16_t* out) {
+    for (int p = 0; p < 6; ++p)
+        for (int pc = 0; pc < 8; ++pc)
+            for (unsigned bm = 0; bm < 256; ++bm) {
+                const int row = std::min(pc + host_cs(p), 7);
+                unsigned best = 32, mm = 0, cnt = 0, j = 0;
+                for (int s = 0; s < 8; ++s) {
+                    if (!((host_startmask(p) >> s) & 1u)) continue;
+                    const unsigned fm = host_fpm(p, s);
+                    if (!(fm & bm)) {
+                        const unsigned r = t.cost2rank[row * 256 + (bm | fm)];
+                        if (r < best) {
+                            best = r;
+                            mm = 0;
+                        }
+                        if (r == best) mm |= 1u << j;
+                        ++cnt;
+                    }
+                    ++j;
+                }
+                out[(p * 8 + pc) * 256 + bm] = cnt ? (uint16_t)(best << 10 | mm << 3 | cnt) : kScoreNoCand;
+            }
+}
+
 inline int build_tables(DevTables* t) {
     std::memset(t, 0, sizeof(*t));
     std::vector<uint8_t> mark(8 * 256, 0);

@@ -140,6 +140,13 @@ struct DevBuf {
         cap = 0;
         const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
         cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) return e;
+        // Defined contents from the start: result buffers are copied back
+        // by capacity (event / scratch records a run did not write), and
+        // compute-sanitizer initcheck holds every copied byte to that.
+        // Only on growth; ordered before any stream's later work.
+        e = cudaMemset(p, 0, want);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
         if (e == cudaSuccess) cap = want;
         return e;
     }
@@ -195,6 +202,7 @@ struct msg_engine {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     msgk::DevBuf tables;
+    msgk::DevBuf score_tab;  // the arrival scorer's per-word table (host_tables.h, build_score_table)
     msgk::DevBuf flush;
     uint64_t launches = 0;
     std::string last_error;

@@ -16,19 +16,22 @@
 // key [pass|rank|!reused|gpu:32|start] and merges it per snapshot with one
 // atomicMin; Lazy/all candidate counts ride two REDUX.ADD and one atomicAdd.
 //
-// Per word the hot path is table-driven (tables in shared memory, built
-// once per block):
-//   bct[p][busy_c]  byte offset of the post-placement LUT row
-//                   (popc(busy_c) + cs, capped at 7) | !lazy << 31;
-//   avail[p][km]    legal starts memory-disjoint from the blocked mask;
-//   rank26[...]     cost rank of (row, busy_m | fm(start)), pre-shifted.
-// So a word costs ~12 instructions plus LDS + LOP3 + predicated VIMNMX per
-// legal start.  The reuse bit (idle instance of exactly this placement,
-// scheduler.cpp:62-66) is resolved off the hot path: words are first scored
-// as "not reused"; a warp whose chunk holds any idle-exact bit of the profile
-// rescores that chunk with the bit (rare: an idle instance of the very
-// profile requested).  Since the reuse-aware key of a candidate is never
-// larger than its plain key, the minimum over both passes is exact.
+// Per word the hot path is one lookup.  With load balancing and dynamic
+// partitioning (the schedule() default), a word whose blocked memory equals
+// its busy memory (no draining instance — every word of a run without
+// migration overlap) is scored from stab[profile][popc busy_c][busy_m]
+// (build_score_table): the lowest post-placement cost rank over the
+// available starts, which starts reach it, and how many starts are
+// available.  The word's key is then assembled with a few ALU ops: the pass
+// bit from the classification (classify, gpu.cpp:168-177: Lazy = 0, Busy =
+// 1), the rank, !reused (an idle instance of exactly the profile at one of
+// the minimum-rank starts, scheduler.cpp:62-66 — the idle-exact bits ride in
+// the word), the word index and the start.  Since Lazy keys sort below Busy
+// keys, ONE pass over the words yields schedule()'s two-pass answer
+// (scheduler.cpp:57-80: Busy GPUs only when no Lazy GPU has a candidate);
+// candidate counts are kept per class.  Words with a draining instance, and
+// the !dyn / first-fit variants, take the per-start path (tables in shared
+// memory, or in global memory for the rare draining word).
 //
 // Bound: HBM bandwidth — 8 B per scored GPU.
 #include <cuda_runtime.h>
@@ -36,6 +39,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "decide.h"
 #include "dev_types.h"
@@ -51,9 +55,6 @@ constexpr int kScoreThreads = MSG_SCORE_THREADS;
 #endif
 #ifndef MSG_SCORE_MINB
 #define MSG_SCORE_MINB 4
-#endif
-#ifndef MSG_SCORE_ILP2  // pass 1 scores two listed words per iteration (0: one)
-#define MSG_SCORE_ILP2 1
 #endif
 #ifndef MSG_SCORE_ITEM
 #define MSG_SCORE_ITEM 4
@@ -113,6 +114,41 @@ __device__ __forceinline__ void score_smem_init(ScoreSmem& s, const DevTables* t
     }
 }
 
+// The per-word table of the default (load balancing + dynamic
+// partitioning) path (host_tables.h, build_score_table), copied into shared
+// memory once per block with the pass bit (bit 15: Busy) of each entry's
+// popc(busy_c) set from this launch's threshold; NoTab for the other
+// variants.  Keys at or above kNoCandKey mean "no candidate".
+constexpr int kScoreTabEntries = 6 * 8 * 256;
+constexpr unsigned kNoCandEntry = 0xFC08u;
+constexpr unsigned kNoCandKey = 0xFC000000u;
+struct FastTab {
+    uint16_t t[kScoreTabEntries];
+};
+struct NoTab {};
+
+__device__ __forceinline__ void fast_tab_init(FastTab& s, const uint16_t* g, unsigned lazymask) {
+    const uint4* src = reinterpret_cast<const uint4*>(g);
+    uint4* dst = reinterpret_cast<uint4*>(s.t);
+    for (unsigned i = threadIdx.x; i < kScoreTabEntries / 8; i += blockDim.x) {
+        // 8 entries of one (profile, pc) row: pc = (entry >> 8) & 7
+        const unsigned pc = ((i * 8u) >> 8) & 7u;
+        const unsigned pass = (((lazymask >> pc) & 1u) ^ 1u) * 0x80008000u;
+        uint4 v = __ldg(src + i);
+        // entries without a candidate (count 0) always carry the pass bit
+        auto fix = [&](unsigned x) {
+            unsigned y = x | pass;
+            y |= ((x & 0x7u) == 0 ? 0x8000u : 0u) | (((x >> 16) & 0x7u) == 0 ? 0x80000000u : 0u);
+            return y;
+        };
+        v.x = fix(v.x);
+        v.y = fix(v.y);
+        v.z = fix(v.z);
+        v.w = fix(v.w);
+        dst[i] = v;
+    }
+}
+
 // Running per-thread state of one item.
 struct ItemAcc {
     unsigned best;   // item-local key minimum
@@ -167,6 +203,83 @@ __device__ __forceinline__ void score_word(const ScoreSmem& sm, uint64_t w, unsi
     }
 }
 
+// Per-start scoring of one word of profile P with load balancing and
+// dynamic partitioning, tables read from global memory (L1): the rare words
+// with a draining instance (blocked memory != busy memory).  Returns the
+// word's minimum key (x) and its candidate count filed under Lazy << 16 or
+// Busy (y).
+template <int P>
+__device__ __noinline__ uint2 score_word_generic(const DevTables* tb, uint64_t w, unsigned local, unsigned lazymask) {
+    using Q = Prof<P>;
+    const unsigned lo = (unsigned)w;
+    const unsigned pc = (unsigned)__popc(lo & 0x7Fu), bm = (lo >> 8) & 0xFFu, km = (lo >> 16) & 0xFFu;
+    const unsigned row = min(pc + Q::cs, 7u);
+    const unsigned busy = ((lazymask >> pc) & 1u) ^ 1u;
+    const unsigned ex = (unsigned)(w >> (24 + Q::pbase));
+    unsigned best = 0xFFFFFFFFu, n = 0;
+#pragma unroll
+    for (unsigned j = 0; j < Q::n; ++j) {
+        if (Q::fm(j) & km) continue;
+        ++n;
+        const unsigned r = __ldg(&tb->cost2rank[row * 256 + (bm | Q::fm(j))]);
+        const unsigned key = (busy << 31) | (r << 26) | ((((ex >> j) & 1u) ^ 1u) << 25) | (local << 3) |
+                             (j * Q::stride);
+        best = min(best, key);
+    }
+    return make_uint2(best, n << (busy ? 0 : 16));
+}
+
+// One word of profile P with load balancing and dynamic partitioning: one
+// lookup in the per-profile table T = shared table + P * 2048.
+// Branch-free; returns false (and contributes nothing) for a word with a
+// draining instance, which the caller rescores with score_word_generic.
+// lk3 = the word's item-local index << 3.
+template <int P>
+__device__ __forceinline__ bool score_word_fast(const uint16_t* T, uint64_t w, unsigned lk3, ItemAcc& acc) {
+    using Q = Prof<P>;
+    const unsigned lo = (unsigned)w;
+    const unsigned pc = (unsigned)__popc(lo & 0x7Fu);
+    const unsigned bm = (lo >> 8) & 0xFFu;
+    const bool plain = ((lo ^ (lo >> 8)) & 0xFF00u) == 0;  // blocked memory == busy memory: no draining
+    unsigned e = T[pc * 256u + bm];
+    e = plain ? e : kNoCandEntry;
+    const unsigned mm = (e >> 3) & 0x7Fu;                      // minimum-rank starts
+    const unsigned r = mm & (unsigned)(w >> (24 + Q::pbase));  // ... with an idle-exact instance
+    const unsigned sel = r ? r : mm;
+    const unsigned j = (unsigned)__ffs(sel) - 1u;
+    const unsigned key = ((e >> 10) << 26) | (r ? 0u : 1u << 25) | lk3 | (j * Q::stride);
+    acc.best = min(acc.best, key);
+    acc.cnt += (e & 7u) << ((~e >> 11) & 16u);  // Lazy (pass 0) candidates in the high half
+    return plain;
+}
+
+// The thread's words of one chunk (x[k].x at local index l_k, x[k].y at
+// l_k + 1), all through the table, then the draining ones (if any in the
+// warp) through the per-start path.
+template <int P, int NW2>
+__device__ __forceinline__ void score_words_fast(const uint16_t* T, const DevTables* tb, const ulonglong2 (&x)[NW2],
+                                                 unsigned l0, unsigned lazymask, ItemAcc& acc) {
+    unsigned slow = 0;
+#pragma unroll
+    for (int k = 0; k < NW2; ++k) {
+        const unsigned l3 = (l0 + (unsigned)k * 2 * kScoreThreads) << 3;
+        slow |= (score_word_fast<P>(T, x[k].x, l3, acc) ? 0u : 1u) << (2 * k);
+        slow |= (score_word_fast<P>(T, x[k].y, l3 + 8u, acc) ? 0u : 1u) << (2 * k + 1);
+    }
+    if (__builtin_expect(__any_sync(0xffffffffu, slow != 0), 0)) {
+#pragma unroll
+        for (int k = 0; k < 2 * NW2; ++k) {  // static indices: the words stay in registers
+            if ((slow >> k) & 1u) {
+                const uint64_t w = (k & 1) ? x[k >> 1].y : x[k >> 1].x;
+                const uint2 g = score_word_generic<P>(tb, w, l0 + (unsigned)(k >> 1) * 2 * kScoreThreads + (k & 1),
+                                                      lazymask);
+                acc.best = min(acc.best, g.x);
+                acc.cnt += g.y;
+            }
+        }
+    }
+}
+
 struct ChunkData {
     ulonglong2 v[kWordsPerThread / 2];
 };
@@ -209,6 +322,12 @@ __device__ __forceinline__ void score_chunk(const ScoreSmem& sm, const ChunkData
     }
 }
 
+template <int P>
+__device__ __forceinline__ void score_chunk_fast(const uint16_t* T, const ScoreArgs& a, const ChunkData& d,
+                                                 unsigned base, ItemAcc& acc) {
+    score_words_fast<P>(T, a.tables, d.v, base + threadIdx.x * 2u, a.lazymask, acc);
+}
+
 // Work cursor over the flattened (item, chunk) sequence of one block.
 struct Cursor {
     uint32_t item, snap, chunk, end;  // current item, its snapshot, chunk index, item end chunk
@@ -220,7 +339,8 @@ struct Cursor {
 // snapshot's slots with one 64-bit atomicMin / atomicAdd.
 template <bool LB>
 __device__ __forceinline__ void flush_item(const ScoreArgs& a, const ItemAcc& acc, uint32_t snap, uint32_t first) {
-    const unsigned best = __reduce_min_sync(0xffffffffu, acc.best);
+    unsigned best = __reduce_min_sync(0xffffffffu, acc.best);
+    best = best >= kNoCandKey ? 0xFFFFFFFFu : best;  // the table's no-candidate entries
     const unsigned cnt = LB ? __reduce_add_sync(0xffffffffu, acc.cnt) : 0u;
     if ((threadIdx.x & 31) == 0) {
         if (best != 0xFFFFFFFFu) {
@@ -238,9 +358,9 @@ __device__ __forceinline__ void flush_item(const ScoreArgs& a, const ItemAcc& ac
 // Scores `c` (the cursor's chunk) while the following chunk loads into
 // `n`; advances the cursor; true when the item is finished.
 template <int P, bool LB, bool DYN>
-__device__ __forceinline__ bool score_step(const ScoreArgs& a, const ScoreSmem& sm, const ChunkData& c, ChunkData& n,
-                                           Cursor& cu, ItemAcc& acc, uint32_t first, uint32_t chunks_per,
-                                           uint32_t n_items, uint32_t items_per) {
+__device__ __forceinline__ bool score_step(const ScoreArgs& a, const ScoreSmem& sm, const uint16_t* T,
+                                           const ChunkData& c, ChunkData& n, Cursor& cu, ItemAcc& acc, uint32_t first,
+                                           uint32_t chunks_per, uint32_t n_items, uint32_t items_per) {
     Cursor nx = cu;
     bool more = true;
     if (++nx.chunk >= nx.end) {
@@ -255,9 +375,12 @@ __device__ __forceinline__ bool score_step(const ScoreArgs& a, const ScoreSmem& 
     }
     if (more) n = load_chunk(a, nx.snap, (uint64_t)nx.chunk * kChunk);
     const unsigned base = (cu.chunk - first) * kChunk;
-    acc.anyx = 0;
-    score_chunk<P, LB, DYN, false>(sm, c, base, acc);
-    if (LB && DYN && __any_sync(0xffffffffu, acc.anyx != 0)) score_chunk<P, LB, DYN, true>(sm, c, base, acc);
+    if constexpr (LB && DYN) {
+        score_chunk_fast<P>(T + P * 2048, a, c, base, acc);
+    } else {
+        acc.anyx = 0;
+        score_chunk<P, LB, DYN, false>(sm, c, base, acc);
+    }
     const bool done = nx.item != cu.item || !more;
     cu = nx;
     return done;
@@ -273,7 +396,8 @@ struct WarpPart {
 
 template <bool LB>
 __device__ __forceinline__ void stash_item(const ItemAcc& acc, WarpPart* wpart) {
-    const unsigned best = __reduce_min_sync(0xffffffffu, acc.best);
+    unsigned best = __reduce_min_sync(0xffffffffu, acc.best);
+    best = best >= kNoCandKey ? 0xFFFFFFFFu : best;  // the table's no-candidate entries
     const unsigned cnt = LB ? __reduce_add_sync(0xffffffffu, acc.cnt) : 0u;
     if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = WarpPart{best, cnt};
 }
@@ -281,13 +405,13 @@ __device__ __forceinline__ void stash_item(const ItemAcc& acc, WarpPart* wpart) 
 // One item: its chunks are scored with the profile's specialised code while
 // the following chunk (possibly the next item's first) is in flight.
 template <int P, bool LB, bool DYN>
-__device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& sm, ChunkData& cur, Cursor& cu,
-                                           uint32_t chunks_per, uint32_t n_items, uint32_t items_per) {
+__device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& sm, const uint16_t* T, ChunkData& cur,
+                                           Cursor& cu, uint32_t chunks_per, uint32_t n_items, uint32_t items_per) {
     ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
     const uint32_t snap = cu.snap, first = cu.chunk;
     for (;;) {  // the following chunk loads while this one is scored
         ChunkData next;
-        const bool done = score_step<P, LB, DYN>(a, sm, cur, next, cu, acc, first, chunks_per, n_items, items_per);
+        const bool done = score_step<P, LB, DYN>(a, sm, T, cur, next, cu, acc, first, chunks_per, n_items, items_per);
         cur = next;
         if (done) break;
     }
@@ -301,7 +425,14 @@ __device__ __forceinline__ void score_item(const ScoreArgs& a, const ScoreSmem& 
 template <bool LB, bool DYN>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(ScoreArgs a) {
     __shared__ __align__(16) ScoreSmem sm;
-    score_smem_init(sm, a.tables, a.lazymask);
+    __shared__ __align__(16) std::conditional_t<LB && DYN, FastTab, NoTab> ft;
+    const uint16_t* T = nullptr;
+    if constexpr (LB && DYN) {
+        fast_tab_init(ft, a.stab, a.lazymask);
+        T = ft.t;
+    } else {
+        score_smem_init(sm, a.tables, a.lazymask);
+    }
     __syncthreads();
     const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
     const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
@@ -316,12 +447,12 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(ScoreArgs a) {
     ChunkData cur = load_chunk(a, cu.snap, (uint64_t)cu.chunk * kChunk);
     while (cu.item < n_items) {
         switch (cu.prof) {
-            case 0: score_item<0, LB, DYN>(a, sm, cur, cu, chunks_per, n_items, items_per); break;
-            case 1: score_item<1, LB, DYN>(a, sm, cur, cu, chunks_per, n_items, items_per); break;
-            case 2: score_item<2, LB, DYN>(a, sm, cur, cu, chunks_per, n_items, items_per); break;
-            case 3: score_item<3, LB, DYN>(a, sm, cur, cu, chunks_per, n_items, items_per); break;
-            case 4: score_item<4, LB, DYN>(a, sm, cur, cu, chunks_per, n_items, items_per); break;
-            default: score_item<5, LB, DYN>(a, sm, cur, cu, chunks_per, n_items, items_per); break;
+            case 0: score_item<0, LB, DYN>(a, sm, T, cur, cu, chunks_per, n_items, items_per); break;
+            case 1: score_item<1, LB, DYN>(a, sm, T, cur, cu, chunks_per, n_items, items_per); break;
+            case 2: score_item<2, LB, DYN>(a, sm, T, cur, cu, chunks_per, n_items, items_per); break;
+            case 3: score_item<3, LB, DYN>(a, sm, T, cur, cu, chunks_per, n_items, items_per); break;
+            case 4: score_item<4, LB, DYN>(a, sm, T, cur, cu, chunks_per, n_items, items_per); break;
+            default: score_item<5, LB, DYN>(a, sm, T, cur, cu, chunks_per, n_items, items_per); break;
         }
     }
 }
@@ -353,7 +484,8 @@ struct StageMeta {
 
 // The stage ring lives in dynamic shared memory (beyond the 48 KiB static limit).
 struct TmaSmem {
-    ScoreSmem& t;             // static: the scoring tables
+    const ScoreSmem* t;       // static: the per-start scoring tables (generic variants)
+    const uint16_t* ft;       // static: the per-word table (load balancing + dynamic partitioning)
     uint64_t (*buf)[kChunk];  // [kStages][kChunk]
     uint64_t* full;           // [kStages]
     StageMeta* meta;          // [kStages]
@@ -422,6 +554,9 @@ __device__ __forceinline__ void prod_issue(const ScoreArgs& a, TmaSmem& sm, Prod
     m.prof = p.prof;
     m.first = p.first;
     m.last = p.chunk + 1 >= p.end;
+    if (nvalid < (uint32_t)kChunk) {  // a snapshot's last chunk: the tail reads as fully occupied GPUs
+        for (uint32_t i = nvalid; i < (uint32_t)kChunk; ++i) sm.buf[stage][i] = 0xFFFF7Full;
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage's previous reads precede the copy
     mbar_arrive_tx(&sm.full[stage], nvalid * 8u);
     bulk_load(sm.buf[stage], a.words + (uint64_t)p.snap * a.G + c0, nvalid * 8u, &sm.full[stage]);
@@ -441,8 +576,8 @@ __device__ __forceinline__ void score_stage(const TmaSmem& sm, int stage, const 
     for (int k = 0; k < kWordsPerThread / 2; ++k) {
         const unsigned l = t2 + (unsigned)k * 2 * kScoreThreads;
         const ulonglong2 x = v[threadIdx.x + (unsigned)k * kScoreThreads];
-        score_word<P, LB, DYN, REUSE>(sm.t, whole || l < m.nvalid ? x.x : kFull, m.base + l, acc);
-        score_word<P, LB, DYN, REUSE>(sm.t, whole || l + 1 < m.nvalid ? x.y : kFull, m.base + l + 1, acc);
+        score_word<P, LB, DYN, REUSE>(*sm.t, whole || l < m.nvalid ? x.x : kFull, m.base + l, acc);
+        score_word<P, LB, DYN, REUSE>(*sm.t, whole || l + 1 < m.nvalid ? x.y : kFull, m.base + l + 1, acc);
     }
 }
 
@@ -451,72 +586,24 @@ __device__ __forceinline__ void consume_stage(const TmaSmem& sm, int stage, cons
                                               WarpPart* wpart) {
     acc.anyx = 0;
     score_stage<P, LB, DYN, false>(sm, stage, m, acc);
-    if (LB && DYN && __any_sync(0xffffffffu, acc.anyx != 0)) score_stage<P, LB, DYN, true>(sm, stage, m, acc);
     if (m.last) {
         stash_item<LB>(acc, wpart);
         acc = ItemAcc{0xFFFFFFFFu, 0u, 0u};
     }
 }
 
-// Pass 1 of load-balanced scoring (scheduler.cpp:47-81 scores Lazy GPUs first
-// and Busy GPUs only when no Lazy GPU has a candidate): only Lazy words are
-// scored.  Each warp classifies its 32 x kWordsPerThread words of the stage
-// with one table lookup each, compacts the Lazy ones into a per-warp index
-// list (ballot + prefix popc), and scores the list with all 32 lanes, so the
-// per-start work is spent on Lazy words only.  Snapshots left without a Lazy
-// candidate are completed by score_busy_kernel (pass 2).
-template <int P, bool DYN>
-__device__ __forceinline__ void consume_lazy(const ScoreArgs& a, const TmaSmem& sm, int stage, const StageMeta& m,
-                                             ItemAcc& acc, uint16_t* wl, WarpPart* wpart) {
-    const uint64_t* buf = sm.buf[stage];
-    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const unsigned wbase = warp * 32u * kWordsPerThread;
-    const unsigned lt = (1u << lane) - 1u;
-    // classify's lazy set is {popc(busy_c) < K} (pc / 7.0 < threshold is monotone in pc)
-    const int K = __popc(a.lazymask & 0xFFu);
-    const bool whole = m.nvalid == (uint32_t)kChunk;
-    unsigned n = 0;
-    // all of the thread's words first: the list stores below may not be
-    // reordered above later loads of the stage, so interleaving them would
-    // expose one shared-memory latency per word
-    unsigned los[kWordsPerThread];
+// The default path (load balancing + dynamic partitioning): every word of
+// the stage scored with one table lookup, Lazy and Busy together in one
+// pass (module comment).
+template <int P>
+__device__ __forceinline__ void consume_fast(const ScoreArgs& a, const TmaSmem& sm, int stage, const StageMeta& m,
+                                             ItemAcc& acc, WarpPart* wpart) {
+    // a snapshot's last chunk was padded with full-GPU words by the producer
+    const ulonglong2* v = reinterpret_cast<const ulonglong2*>(sm.buf[stage]);
+    ulonglong2 x[kWordsPerThread / 2];
 #pragma unroll
-    for (int k = 0; k < kWordsPerThread; ++k)
-        los[k] = reinterpret_cast<const uint32_t*>(buf)[2 * (wbase + (unsigned)k * 32u + lane)];
-#pragma unroll
-    for (int k = 0; k < kWordsPerThread; ++k) {
-        const unsigned idx = wbase + (unsigned)k * 32u + lane;
-        const unsigned lo = los[k];
-        const bool lz = (whole || idx < m.nvalid) && __popc(lo & 0x7Fu) < K;
-        const unsigned bal = __ballot_sync(0xffffffffu, lz);
-        if (lz) wl[n + __popc(bal & lt)] = (uint16_t)idx;
-        n += __popc(bal);
-    }
-    __syncwarp();
-    acc.anyx = 0;
-#if MSG_SCORE_ILP2
-    // two words per iteration: their dependent shared-memory lookup chains
-    // (list -> word -> avail/bct -> rank rows) overlap
-    for (unsigned i = lane; i < n; i += 64) {
-        const bool has1 = i + 32 < n;
-        const unsigned idx0 = wl[i], idx1 = wl[has1 ? i + 32 : i];
-        const uint64_t w0 = buf[idx0], w1 = buf[idx1];
-        score_word<P, true, DYN, false>(sm.t, w0, m.base + idx0, acc);
-        score_word<P, true, DYN, false>(sm.t, w1, m.base + idx1, acc, has1);
-    }
-#else
-    for (unsigned i = lane; i < n; i += 32) {
-        const unsigned idx = wl[i];
-        score_word<P, true, DYN, false>(sm.t, buf[idx], m.base + idx, acc);
-    }
-#endif
-    if (DYN && __any_sync(0xffffffffu, acc.anyx != 0)) {
-        for (unsigned i = lane; i < n; i += 32) {
-            const unsigned idx = wl[i];
-            score_word<P, true, DYN, true>(sm.t, buf[idx], m.base + idx, acc);
-        }
-    }
-    __syncwarp();
+    for (int k = 0; k < kWordsPerThread / 2; ++k) x[k] = v[threadIdx.x + (unsigned)k * kScoreThreads];
+    score_words_fast<P>(sm.ft + P * 2048, a.tables, x, m.base + threadIdx.x * 2u, a.lazymask, acc);
     if (m.last) {
         stash_item<true>(acc, wpart);
         acc = ItemAcc{0xFFFFFFFFu, 0u, 0u};
@@ -525,21 +612,26 @@ __device__ __forceinline__ void consume_lazy(const ScoreArgs& a, const TmaSmem& 
 
 template <bool LB, bool DYN>
 __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kernel(ScoreArgs a) {
-    __shared__ __align__(16) ScoreSmem tables;
-    __shared__ uint16_t wlist[kScoreThreads / 32][32 * kWordsPerThread];  // pass 1: Lazy words per warp
-    __shared__ WarpPart wpart[2][kScoreThreads / 32];                     // item ends, by stage parity
+    constexpr bool kFast = LB && DYN;
+    __shared__ __align__(16) std::conditional_t<kFast, FastTab, ScoreSmem> tabs;
+    __shared__ WarpPart wpart[2][kScoreThreads / 32];  // item ends, by stage parity
     extern __shared__ __align__(128) unsigned char ring[];
-    TmaSmem sm{tables, reinterpret_cast<uint64_t(*)[kChunk]>(ring),
+    TmaSmem sm{nullptr, nullptr, reinterpret_cast<uint64_t(*)[kChunk]>(ring),
                reinterpret_cast<uint64_t*>(ring + sizeof(uint64_t) * kChunk * kStages),
                reinterpret_cast<StageMeta*>(ring + sizeof(uint64_t) * kChunk * kStages + 8 * kStages)};
     // the merge kernel may launch now: it waits for this grid (griddepcontrol.wait)
     asm volatile("griddepcontrol.launch_dependents;");
-    score_smem_init(sm.t, a.tables, a.lazymask);
+    if constexpr (kFast) {
+        fast_tab_init(tabs, a.stab, a.lazymask);
+        sm.ft = tabs.t;
+    } else {
+        score_smem_init(tabs, a.tables, a.lazymask);
+        sm.t = &tabs;
+    }
     const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
     const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
     const uint32_t n_items = items_per * a.n;
     Producer p;
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.scratch[a.n] = 0;  // pass-2 list length
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&sm.full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -555,16 +647,15 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
         mbar_wait(&sm.full[stage], (n / kStages) & 1u);
         const StageMeta m = sm.meta[stage];
         if (m.snap == 0xFFFFFFFFu) break;
-        uint16_t* wl = wlist[threadIdx.x >> 5];
         WarpPart* wp = wpart[n & 1u];
-        if (LB) {
+        if constexpr (kFast) {
             switch (m.prof) {
-                case 0: consume_lazy<0, DYN>(a, sm, stage, m, acc, wl, wp); break;
-                case 1: consume_lazy<1, DYN>(a, sm, stage, m, acc, wl, wp); break;
-                case 2: consume_lazy<2, DYN>(a, sm, stage, m, acc, wl, wp); break;
-                case 3: consume_lazy<3, DYN>(a, sm, stage, m, acc, wl, wp); break;
-                case 4: consume_lazy<4, DYN>(a, sm, stage, m, acc, wl, wp); break;
-                default: consume_lazy<5, DYN>(a, sm, stage, m, acc, wl, wp); break;
+                case 0: consume_fast<0>(a, sm, stage, m, acc, wp); break;
+                case 1: consume_fast<1>(a, sm, stage, m, acc, wp); break;
+                case 2: consume_fast<2>(a, sm, stage, m, acc, wp); break;
+                case 3: consume_fast<3>(a, sm, stage, m, acc, wp); break;
+                case 4: consume_fast<4>(a, sm, stage, m, acc, wp); break;
+                default: consume_fast<5>(a, sm, stage, m, acc, wp); break;
             }
         } else {
             switch (m.prof) {
@@ -598,70 +689,11 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
     }
 }
 
-// Pass 2 (after score_tma_kernel<true, DYN>): snapshots whose pass 1 found no
-// Lazy candidate are scored again over all words with the full key (Busy
-// GPUs compete; their candidates are counted), exactly as the register path.
-template <bool DYN>
-__device__ __forceinline__ void busy_item(const ScoreArgs& a, const ScoreSmem& sm, uint32_t snap, uint32_t first,
-                                          uint32_t end) {
-    ItemAcc acc{0xFFFFFFFFu, 0u, 0u};
-    const unsigned prof = a.profile[snap];
-    for (uint32_t c = first; c < end; ++c) {
-        const ChunkData d = load_chunk(a, snap, (uint64_t)c * kChunk);
-        const unsigned base = (c - first) * kChunk;
-        acc.anyx = 0;
-        switch (prof) {
-            case 0: score_chunk<0, true, DYN, false>(sm, d, base, acc); break;
-            case 1: score_chunk<1, true, DYN, false>(sm, d, base, acc); break;
-            case 2: score_chunk<2, true, DYN, false>(sm, d, base, acc); break;
-            case 3: score_chunk<3, true, DYN, false>(sm, d, base, acc); break;
-            case 4: score_chunk<4, true, DYN, false>(sm, d, base, acc); break;
-            default: score_chunk<5, true, DYN, false>(sm, d, base, acc); break;
-        }
-        if (DYN && __any_sync(0xffffffffu, acc.anyx != 0)) {
-            switch (prof) {
-                case 0: score_chunk<0, true, DYN, true>(sm, d, base, acc); break;
-                case 1: score_chunk<1, true, DYN, true>(sm, d, base, acc); break;
-                case 2: score_chunk<2, true, DYN, true>(sm, d, base, acc); break;
-                case 3: score_chunk<3, true, DYN, true>(sm, d, base, acc); break;
-                case 4: score_chunk<4, true, DYN, true>(sm, d, base, acc); break;
-                default: score_chunk<5, true, DYN, true>(sm, d, base, acc); break;
-            }
-        }
-    }
-    flush_item<true>(a, acc, snap, first);
-}
-
-// Pass 2 (after score_tma_kernel<true, DYN>): snapshots whose pass 1 found no
-// Lazy candidate are scored again over all words with the full key (Busy
-// GPUs compete; their candidates are counted), exactly as the register path.
-// score_reduce_kernel lists them between the passes, so with none listed
-// this kernel reads one word and ends.
-
-template <bool DYN>
-__global__ void __launch_bounds__(kScoreThreads) score_busy_kernel(ScoreArgs a) {
-    __shared__ __align__(16) ScoreSmem sm;
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of score_reduce_kernel
-    const uint32_t* list = a.scratch + a.n + 1;  // score_reduce_kernel
-    const uint32_t need = *(volatile const uint32_t*)(a.scratch + a.n);
-    if (need == 0) return;
-    score_smem_init(sm, a.tables, a.lazymask);
-    __syncthreads();
-    const uint32_t chunks_per = (uint32_t)((a.G + kChunk - 1) / kChunk);
-    const uint32_t items_per = (chunks_per + kItemChunks - 1) / kItemChunks;
-    for (uint64_t v = blockIdx.x; v < (uint64_t)need * items_per; v += gridDim.x) {
-        const uint32_t j = (uint32_t)(v / items_per), first = (uint32_t)(v - (uint64_t)j * items_per) * kItemChunks;
-        busy_item<DYN>(a, sm, list[j], first, min(first + kItemChunks, chunks_per));
-    }
-}
-
-// After pass 1 (TMA path): each snapshot's items merge into its output —
-// minimum key, summed counts — and, with load balancing, the snapshots left
-// without a Lazy candidate are listed for pass 2 (scratch[n] = count, then
-// the list; the order is irrelevant, every pass-2 block reads the same list).
+// After the scoring grid (TMA path): each snapshot's items merge into its
+// output — minimum key, summed Lazy/Busy candidate counts.
 __global__ void score_reduce_kernel(ScoreArgs a, uint32_t items_per) {
     asm volatile("griddepcontrol.launch_dependents;");
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of pass 1
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the scoring grid
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= a.n) return;
     uint64_t best = ~0ull, cnt = 0;
@@ -672,7 +704,6 @@ __global__ void score_reduce_kernel(ScoreArgs a, uint32_t items_per) {
     }
     a.out[2 * s] = best;
     a.out[2 * s + 1] = cnt;
-    if (a.lb && (cnt >> 32) == 0) a.scratch[a.n + 1 + atomicAdd(&a.scratch[a.n], 1u)] = s;
 }
 
 __global__ void score_init_kernel(uint64_t* out, uint32_t n) {
@@ -731,9 +762,9 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
     }
     if (!tma) return cudaGetLastError();
-    // The merge and pass 2 launch as programmatic dependents: their launch
-    // overlaps the previous kernel's tail; griddepcontrol.wait in each holds
-    // its reads until the previous grid has completed.
+    // The merge launches as a programmatic dependent: its launch overlaps
+    // the scoring grid's tail; griddepcontrol.wait holds its reads until the
+    // scoring grid has completed.
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -745,13 +776,6 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     lc.blockDim = dim3(256);
     cudaError_t e = cudaLaunchKernelEx(&lc, score_reduce_kernel, a, (uint32_t)(items / a.n));
     if (e != cudaSuccess) return e;
-    if (a.lb) {  // pass 2: snapshots without a Lazy candidate
-        lc.gridDim = dim3((unsigned)std::min<uint64_t>(items, (uint64_t)sms * 4));
-        lc.blockDim = block;
-        e = a.dyn ? cudaLaunchKernelEx(&lc, score_busy_kernel<true>, a)
-                  : cudaLaunchKernelEx(&lc, score_busy_kernel<false>, a);
-        if (e != cudaSuccess) return e;
-    }
     return cudaGetLastError();
 }
 

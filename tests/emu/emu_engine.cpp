@@ -130,6 +130,11 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
     cs.dev.init_off = 0;
     DevTables tables;
     build_tables(&tables);
+    static std::vector<uint16_t> stab = [&] {
+        std::vector<uint16_t> v(kScoreTab);
+        build_score_table(tables, v.data());
+        return v;
+    }();
     std::vector<int32_t> queue(N);
     std::vector<JobOut> jobs(N);
     std::vector<EventRec> evs(tr.ev_cap);
@@ -140,6 +145,7 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
     a.configs = &cs.dev;
     a.init_slots = cs.init.empty() ? nullptr : cs.init.data();
     a.tables = &tables;
+    a.score_tab = stab.data();
     a.arrival = ha.data();
     a.service = hs.data();
     a.profile = hp.data();
