@@ -72,14 +72,25 @@ def parse():
                     help="prefix timed on both engines for the same-prefix CPU comparison")
     ap.add_argument("--c4-peer-arrivals", type=int, default=2000,
                     help="prefix split over all ranks' GPUs (device groups) at N>1")
+    ap.add_argument("--one-gpu", action="store_true",
+                    help="N>1 test mode: every rank on cuda:0, gloo for the host-side collectives "
+                         "(exercises every N>1 leg on a one-GPU box; times are not scaling numbers)")
     return ap.parse_args()
+
+
+ONE_GPU = False  # --one-gpu: all ranks share cuda:0, collectives over gloo on host tensors
 
 
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if ONE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def coll_device():
+    """Device of the tensors handed to torch.distributed collectives."""
+    return "cpu" if ONE_GPU else "cuda"
 
 
 def host_cpu():
@@ -471,7 +482,7 @@ def c4_line(eng, args, rank, world):
         secs = time.perf_counter() - t0
     finally:
         group.close()
-    t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+    t = torch.tensor([secs], dtype=torch.float64, device=coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
         ev = int(res[0].summary["handler_events"])
@@ -554,14 +565,19 @@ def other_configs(eng, rank, world, allreduce_max, allreduce_sum):
 
 
 def main():
+    global ONE_GPU
     args = parse()
+    ONE_GPU = args.one_gpu
     rank, world, local = dist_env()
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if ONE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         if world > 1:
@@ -601,7 +617,7 @@ def main():
             return x
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_device())
         dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM}[op])
         return float(t.item())
 
@@ -638,7 +654,7 @@ def main():
     # e2e: the public C-ABI call with host buffers + the summary gather, every step
     h2d = allreduce(float(batch.n_jobs * (8 + 8 + 1) + batch.n_traces * 48), "sum")
     d2h = allreduce(float(batch.n_traces * 128 + batch.n_jobs * 24), "sum")
-    gdev = "cuda" if world > 1 else None
+    gdev = "cuda" if world > 1 and not ONE_GPU else None
 
     def e2e_step():
         out = eng.run_batch(batch, [cfg], abi.OUT_JOBS)
