@@ -241,6 +241,15 @@ msg_status msg_engine_device_info(const msg_engine* engine, char* name, size_t n
 msg_status msg_run_batch(msg_engine* engine, const msg_trace_batch* batch, const msg_config* cfgs,
                          uint32_t n_cfgs, uint32_t out_flags, msg_batch_result** out);
 
+/* Page-locked host memory for input batches.  When a batch's arrival_s,
+ * service_s and profile arrays live in such memory (this allocator, or any
+ * cudaHostAlloc / cudaHostRegister'ed range), msg_run_batch copies them to
+ * the device in place, with no host-side staging copy.  Any host memory
+ * works; this only removes a copy.  msg_host_alloc returns 64-byte aligned
+ * memory usable from every device of the process. */
+msg_status msg_host_alloc(size_t bytes, void** out);
+void msg_host_free(void* p);
+
 /* The same call split in three for device-resident benchmarking and
  * pipelining: msg_stage validates and copies host inputs to HBM;
  * msg_launch enqueues the simulation on the engine stream (asynchronous);

@@ -155,6 +155,8 @@ struct SimArgs {
     const double* arrival;   // rank order
     const double* service;
     const uint8_t* profile;
+    const int32_t* profile32;  // optional: the caller's int32 profiles (pipelined direct inputs); each
+                               // warp narrows its trace's into `profile` before its first event
     const uint32_t* perm;    // arrival order -> rank (only traces with has_perm)
     int32_t* queue;          // FCFS queue storage, n_jobs per trace
     JobOut* jobs;

@@ -32,6 +32,13 @@
 
 namespace msgk {
 
+#ifdef MSG_SIM_PHASES
+// Development build only: SM cycles of the event loop per phase, summed over
+// warps — 0 timer scan + advance, 1 arrival, 2 service start, 3 departure
+// (incl. planners and the dequeue pass), 4 timeline sample.
+__device__ unsigned long long g_simph[8];
+#endif
+
 constexpr unsigned NONE = 0xFFFFFFFFu;
 constexpr int MAX_JOB_BITS = 22;  // job ranks < 2^22 (inter key layout)
 
@@ -89,6 +96,8 @@ struct WarpSmem {
     uint32_t cseq[NS]; // instance creation order (vector order, gpu.cpp:88-111)
     uint32_t gw[NG];   // per-GPU mask word
     uint16_t mig[NS];  // migrations of the bound job
+    uint8_t act[NS];   // the armed slots as a list: act[0 .. n_act) (SPL >= 2)
+    uint8_t apos[NS];  // slot -> its index in act[] while armed
     uint8_t prof[NS];  // instance profile
     uint8_t st[NS];    // ST_*
 };
@@ -137,12 +146,20 @@ struct TraceSim {
     uint32_t a_idx, a_rank;
     int a_prof;
     double a_t, a_svc;
+    uint64_t a_key;  // time_key(a_t)
     uint32_t q_head, q_tail;
     uint32_t cseq_ctr, mseq_ctr;
     uint32_t n_ev, n_handler, n_tl;
     uint32_t n_mig, n_reconf, n_enq, n_deq;
     int max_arr, max_intra, max_inter;
     uint32_t n_plan_iter;
+    // The armed (timer-carrying: Running, WaitingStart, Draining) slots as a
+    // list in shared memory (act[0 .. n_act), apos: slot -> index), SPL >= 2
+    // only: C2 averages 6.6 armed slots of 64 and exceeds 16 in 0.1% of
+    // events, so the timer scan visits one list entry per lane instead of
+    // SPL slots.
+    static constexpr bool kAct = SPL >= 2;
+    unsigned n_act;
     bool snap_mode;
     double tl_sum, tl_mean;
     unsigned tl_from;  // first GPU whose cost changed since the last timeline sum (G: none)
@@ -198,6 +215,12 @@ struct TraceSim {
         svc = a.service + tr.job_off;
         prf = a.profile + tr.job_off;
         perm = tr.has_perm ? a.perm + tr.job_off : nullptr;
+        if (a.profile32) {  // direct inputs: the caller's int32 profiles, narrowed once per trace
+            uint8_t* dst = const_cast<uint8_t*>(prf);
+            const int32_t* src = a.profile32 + tr.job_off;
+            for (uint32_t j = L; j < N; j += 32) dst[j] = (uint8_t)src[j];
+            wp::sync();
+        }
         queue = a.queue + tr.job_off;
         jobs = a.jobs + tr.job_off;
         jobs_h = a.jobs_host ? a.jobs_host + tr.job_off : nullptr;
@@ -227,6 +250,7 @@ struct TraceSim {
         tl_sum = 0.0;
         tl_mean = 0.0;
         tl_from = 0;
+        n_act = 0;
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
             const int slot = L + 32 * i;
@@ -319,6 +343,23 @@ struct TraceSim {
         const unsigned mx = NONE - wp::rmin(NONE - maxseq);
         cseq_ctr = wp::ballot(any) ? mx + 1u : 0u;
         wp::sync();
+        n_act = 0;
+        if (kAct) {  // the snapshot's armed slots, in slot order
+            const unsigned lt = (1u << L) - 1u;
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                const int slot = L + 32 * k;
+                const bool armed = sm->st[slot] >= ST_RUN;
+                const unsigned bl = wp::ballot(armed);
+                const unsigned e = n_act + (unsigned)wp::popc(bl & lt);
+                if (armed) {
+                    sm->act[e] = (uint8_t)slot;
+                    sm->apos[slot] = (uint8_t)e;
+                }
+                n_act += (unsigned)wp::popc(bl);
+            }
+            wp::sync();
+        }
         for (int g = 0; g < G; ++g) refresh_gpu(g);
     }
 
@@ -345,6 +386,7 @@ struct TraceSim {
             const uint32_t r = perm ? perm[a_idx] : a_idx;
             a_rank = r;
             a_t = arr[r];
+            a_key = time_key(a_t);
             a_prof = prf[r];
             a_svc = svc[r];
         }
@@ -405,6 +447,26 @@ struct TraceSim {
         return w;
     }
 
+    // ------------------------------------------------ armed-slot list
+    MSG_DI void act_add(int slot) {
+        if (!kAct) return;
+        if (L == 0) {
+            sm->act[n_act] = (uint8_t)slot;
+            sm->apos[slot] = (uint8_t)n_act;
+        }
+        ++n_act;
+    }
+    // `slot` must be in the list: the last entry takes its place.
+    MSG_DI void act_remove(int slot) {
+        if (!kAct) return;
+        --n_act;
+        if (L == 0) {
+            const unsigned p = sm->apos[slot], last = sm->act[n_act];
+            sm->act[p] = (uint8_t)last;
+            sm->apos[last] = (uint8_t)p;
+        }
+    }
+
     // ------------------------------------------------- contention model
     // slowdown(k) = 1 + alpha*(k-1) (sim.cpp:26-31): DMUL then DADD.
     MSG_DI double factor(unsigned k) const {
@@ -457,14 +519,32 @@ struct TraceSim {
         unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
         int bsl = -1;
         double bt = 0.0;
+        // With SPL >= 2 the scan visits the armed-slot list (act), one
+        // entry per lane while n_act <= 32.
+        constexpr bool kCompact = kAct;
+        const unsigned na = n_act;
         // every load before the first store (the stores could alias them)
         uint8_t sv[SPL];
+        int slv[SPL];
         unsigned kv[SPL], jv[SPL], mv[SPL];
         double rv[SPL], tv[SPL], pv[SPL];
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
-            const int slot = L + 32 * i;
-            sv[i] = sm->st[slot];
+            sv[i] = ST_EMPTY;
+            slv[i] = 0;
+            kv[i] = 1u;
+            if (kCompact && i > 0 && na <= 32u * (unsigned)i) continue;
+            int slot;
+            if (kCompact) {
+                const bool valid = L + 32u * (unsigned)i < na;
+                slot = valid ? (int)sm->act[L + 32 * i] : 0;
+                const uint8_t x = sm->st[slot];
+                sv[i] = valid ? x : (uint8_t)ST_EMPTY;
+            } else {
+                slot = L + 32 * i;
+                sv[i] = sm->st[slot];
+            }
+            slv[i] = slot;
             kv[i] = sv[i] == ST_RUN ? w_k(sm->gw[slot >> 3]) : 1u;
             const typename WS::RT x = sm->rt[slot];
             rv[i] = x.rem;
@@ -475,9 +555,10 @@ struct TraceSim {
         }
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
-            // branch-free: every slot forms its key, unarmed ones an all-NONE
+            if (kCompact && i > 0 && na <= 32u * (unsigned)i) continue;
+            // branch-free: every entry forms its key, unarmed ones an all-NONE
             // key that never wins
-            const int slot = L + 32 * i;
+            const int slot = slv[i];
             const uint8_t s = sv[i];
             const bool run = s == ST_RUN, armed = s >= ST_RUN, drain = s == ST_DRAIN;
             const double f = wp::shfl(my_f, (int)kv[i] - 1);
@@ -531,12 +612,13 @@ struct TraceSim {
         if (adv) q = wp::ddiv(dt, my_f);
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {
+            if (kCompact && i > 0 && na <= 32u * (unsigned)i) continue;
             const double qk = wp::shfl(q, (int)kv[i] - 1);
             if (sv[i] == ST_RUN) {
                 typename WS::RT x;
                 x.rem = adv ? wp::dsub(rv[i], qk) : rv[i];
                 x.tkey = pv[i];
-                sm->rt[L + 32 * i] = x;
+                sm->rt[slv[i]] = x;
             }
         }
         return kind;
@@ -675,6 +757,7 @@ struct TraceSim {
         // the destination held no instance or an idle one, and create only
         // destroys idle ones: the GPU gains exactly the new instance's share
         const unsigned w = sm->gw[g] + share(delay > 0.0 ? ST_WAIT : ST_RUN, p, s);
+        act_add(slot);
         if (L == 0) {
             sm->jm[slot].job = r;
             sm->mig[slot] = 0;
@@ -753,6 +836,8 @@ struct TraceSim {
             }
         }
         if (overlap > 0.0) ++mseq_ctr;
+        act_add(tg * 8 + ts);
+        if (overlap <= 0.0) act_remove(from_slot);
         set_gpu(fg, nwf);
         const unsigned nwt = tg != fg ? set_gpu(tg, wt + sh_to) : nwf;
         const uint64_t costs = (uint64_t)fcb | ((uint64_t)k2w(nwf) << 16) | ((uint64_t)tcb << 32) |
@@ -819,11 +904,15 @@ struct TraceSim {
             const unsigned pl = tb->placeable[km0];
             unsigned kmin = NONE, cnt = 0;
             int bsl = -1;
+            const unsigned na = n_act;
 #pragma unroll
             for (int i = 0; i < SPL; ++i) {
-                const int slot = L + 32 * i;
+                // sources are busy slots: with the armed-slot list, one entry per lane
+                if (kAct && i > 0 && na <= 32u * (unsigned)i) continue;
+                const bool in = !kAct || L + 32u * (unsigned)i < na;
+                const int slot = kAct ? (in ? (int)sm->act[L + 32 * i] : 0) : L + 32 * i;
                 const int g = slot >> 3, s = slot & 7;
-                if (g < G && g != g0) {
+                if (in && g < G && g != g0) {
                     const uint8_t st = sm->st[slot];
                     if (st == ST_RUN || st == ST_WAIT) {
                         const unsigned w = sm->gw[g];
@@ -908,6 +997,7 @@ struct TraceSim {
         const int32_t r = sm->jm[slot].job;
         const int m = sm->mig[slot];
         const unsigned w = sm->gw[g] - share(sm->st[slot], sm->prof[slot], slot & 7);
+        act_remove(slot);
         wp::sync();
         if (L == 0) {
             sm->st[slot] = ST_IDLE;  // release_job / finish_draining: the instance stays, idle
@@ -937,18 +1027,39 @@ struct TraceSim {
     }
 
     MSG_DI void run() {  // Engine::execute (sim.cpp:123-141)
+#ifdef MSG_SIM_PHASES
+        unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long c0 = clock64();
+#define MSG_SIM_PH(k) do { const long long c1 = clock64(); ph[k] += (unsigned long long)(c1 - c0); c0 = c1; } while (0)
+#else
+#define MSG_SIM_PH(k) ((void)0)
+#endif
         for (;;) {
             int slot = -1;
             // reschedules the previous handler's completions, pops the next
             // timer and advances every running job to it
             const int kind = resched_next(slot);
+            MSG_SIM_PH(0);
             if (kind < 0) break;
             ++n_handler;
-            if (kind == 3) handle_arrival();
-            else if (kind == 2) handle_service_start(slot);
-            else handle_departure(slot, kind == 0);
+            if (kind == 3) {
+                handle_arrival();
+                MSG_SIM_PH(1);
+            } else if (kind == 2) {
+                handle_service_start(slot);
+                MSG_SIM_PH(2);
+            } else {
+                handle_departure(slot, kind == 0);
+                MSG_SIM_PH(3);
+            }
             sample();
+            MSG_SIM_PH(4);
         }
+#ifdef MSG_SIM_PHASES
+        if (L == 0)
+            for (int k = 0; k < 5; ++k) atomicAdd(&g_simph[k], ph[k]);
+#endif
+#undef MSG_SIM_PH
     }
 
     // metrics (sim.cpp:414-502): sums in job-id order, then divide.

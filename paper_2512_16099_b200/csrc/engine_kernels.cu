@@ -19,6 +19,14 @@ namespace msgk {
 #endif
 constexpr int kWarpsPerBlock = MSG_SIM_WPB;
 
+#ifdef MSG_TRACE_TIMES
+// Development aid (-DMSG_TRACE_TIMES): per-trace start / end globaltimer and
+// SM of the event-loop kernel, read back with msg_debug_trace_times.
+constexpr uint32_t kTraceTimesCap = 1u << 16;
+__device__ unsigned long long g_ttimes[4 * kTraceTimesCap];
+__device__ unsigned g_tt_n;
+#endif
+
 template <int SPL, bool DETAIL>
 #ifndef MSG_SIM_MINB
 #define MSG_SIM_MINB 7
@@ -33,10 +41,26 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MSG_SIM_MINB) sim_kernel(
     }
     __syncthreads();
     const unsigned w = threadIdx.x >> 5;
+    WarpSmem<SPL>* ws = reinterpret_cast<WarpSmem<SPL>*>(smem + sizeof(DevTables) + w * sizeof(WarpSmem<SPL>));
     const uint32_t t = blockIdx.x * kWarpsPerBlock + w;
     if (t >= a.n_traces || a.traces[t].large) return;
-    WarpSmem<SPL>* ws = reinterpret_cast<WarpSmem<SPL>*>(smem + sizeof(DevTables) + w * sizeof(WarpSmem<SPL>));
+#ifdef MSG_TRACE_TIMES
+    const uint64_t t0 = wp::gtime_ns();
+#endif
     simulate_trace<SPL, DETAIL>(a, tb, ws, t);
+#ifdef MSG_TRACE_TIMES
+    if (wp::lane() == 0) {
+        const unsigned k = atomicAdd(&g_tt_n, 1u);
+        if (k < kTraceTimesCap) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_ttimes[4 * k] = t0;
+            g_ttimes[4 * k + 1] = wp::gtime_ns();
+            g_ttimes[4 * k + 2] = sm;
+            g_ttimes[4 * k + 3] = a.traces[t].job_off;  // identifies the trace across chunked launches
+        }
+    }
+#endif
 }
 
 template <int SPL, bool DETAIL>
@@ -183,5 +207,31 @@ extern "C" int msg_debug_phase(unsigned long long* out, int n, int reset) {
         cudaMemcpyToSymbol(msgk::g_phase, z, sizeof(z));
     }
     return n;
+}
+#endif
+
+#ifdef MSG_TRACE_TIMES
+extern "C" int msg_debug_trace_times(unsigned long long* out, unsigned n) {
+    // (start ns, end ns, SM, job offset) per finished trace in completion
+    // order since the last call; resets the record counter
+    unsigned k = 0;
+    if (cudaMemcpyFromSymbol(&k, msgk::g_tt_n, sizeof(k)) != cudaSuccess) return -1;
+    if (k > n) k = n;
+    if (k > msgk::kTraceTimesCap) k = msgk::kTraceTimesCap;
+    if (cudaMemcpyFromSymbol(out, msgk::g_ttimes, 4ull * k * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    const unsigned z = 0;
+    cudaMemcpyToSymbol(msgk::g_tt_n, &z, sizeof(z));
+    return (int)k;
+}
+#endif
+
+#ifdef MSG_SIM_PHASES
+extern "C" int msg_debug_sim_phases(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, msgk::g_simph, 8 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(msgk::g_simph, z, sizeof(z));
+    }
+    return 8;
 }
 #endif

@@ -66,9 +66,11 @@ struct msg_staged {
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
     HostBuf h_done;           // run_pipelined: per-trace completion flags (mapped, written by the kernel)
+    HostBuf h_traces;         // run_pipelined: pinned copy of the trace descriptors (async H2D)
     uint32_t done_epoch = 0;  // the flag value of the current run
     // device
     DevBuf d_arrival, d_service, d_profile, d_perm, d_traces, d_configs, d_init, d_tables_unused;
+    DevBuf d_prof32;  // run_pipelined, direct inputs: the caller's int32 profiles (narrowed in-kernel)
     DevBuf d_queue, d_jobs, d_events, d_timeline, d_summary;
     DevBuf d_inbox;  // device-group exchange inboxes (MSG_VDEV > 1)
 };
@@ -159,8 +161,9 @@ inline void put_row(msg_job_row* dst, int64_t id, double arrival, const JobOut& 
 // = 9 aligned vectors): the row buffer is far larger than the caches and is
 // not read back here, so the stores skip the read-for-ownership.
 // nt false (MSG_ROWS_NT=0): plain stores.
+template <class P>
 inline void put_rows(msg_job_row* rows, uint32_t n, const int64_t* ids, const double* ha, const JobOut* hj,
-                     const uint8_t* hp, bool nt) {
+                     const P* hp, bool nt) {
     uint32_t r = 0;
     if (nt) {
         if (n && (reinterpret_cast<uintptr_t>(rows) & 15)) {
@@ -178,6 +181,22 @@ inline void put_rows(msg_job_row* rows, uint32_t n, const int64_t* ids, const do
     }
     for (; r < n; ++r) put_row(rows + r, ids[r], ha[r], hj[r], hp[r]);
     if (nt) _mm_sfence();
+}
+
+// True when [p, p + bytes) is page-locked host memory this process has
+// registered with CUDA (cudaHostAlloc / msg_host_alloc / cudaHostRegister):
+// the copy engines can read it directly.
+bool host_pinned(const void* p, size_t bytes) {
+    if (!p || !bytes) return false;
+    for (const void* q : {p, static_cast<const void*>(static_cast<const char*>(p) + bytes - 1)}) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+            cudaGetLastError();  // clear the sticky "not a CUDA pointer" on old drivers
+            return false;
+        }
+        if (at.type != cudaMemoryTypeHost) return false;
+    }
+    return true;
 }
 
 msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
@@ -716,13 +735,28 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     uint32_t* hperm = s->any_perm ? s->h_perm.as<uint32_t>() : nullptr;
     SimArgs a = make_args(eng, s);
     auto joff = [&](uint32_t d) { return d < T ? s->traces[d].job_off : s->n_jobs; };
+    // Direct inputs: when the caller's arrival / service / profile arrays are
+    // page-locked (msg_host_alloc), the copy engines read them in place —
+    // the host only validates (read-only) and there is no staging copy.
+    // Requires the device layout to be the batch's own job order: every
+    // input trace on the device, in order.  A chunk holding a trace whose
+    // ids are not increasing (rank order differs from input order) is
+    // staged as usual.  MSG_NO_DIRECT=1 disables it.
+    const uint64_t jbase = T ? b->offsets[0] : 0, jall = T ? b->offsets[b->n_traces] - jbase : 0;
+    const bool direct = T && jall && s->traces.size() == s->n_in && std::getenv("MSG_NO_DIRECT") == nullptr &&
+                        host_pinned(b->arrival_s + jbase, jall * sizeof(double)) &&
+                        host_pinned(b->service_s + jbase, jall * sizeof(double)) &&
+                        host_pinned(b->profile + jbase, jall * sizeof(int32_t));
+    if (direct) CK(s->d_prof32.ensure(N * sizeof(int32_t)));
+    CK(s->h_traces.ensure(std::max<uint32_t>(T, 1) * sizeof(DevTrace)));
+    uint8_t chunk_direct[kMaxPipeChunks] = {};
     for (int k = 0; k < n_chunks; ++k) {
         const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
         if (d0 == d1) continue;
         cudaStream_t st = eng->pstream[k];
-        // Check (sim.cpp:97-116) and stage each trace of the chunk while its
-        // inputs are hot; a failing trace runs as an empty one and is
-        // reported from its check.
+        // Check (sim.cpp:97-116) each trace of the chunk and, unless the
+        // chunk goes direct, stage it while its inputs are hot; a failing
+        // trace runs as an empty one and is reported from its check.
         std::atomic<uint32_t> n_perm{0};
         parallel_for(d1 - d0, 32, [&](uint32_t i) {
             const uint32_t d = d0 + i, t = s->src_of[d];
@@ -737,12 +771,28 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             }
             tr.has_perm = c.identity ? 0 : 1;
             if (tr.has_perm) n_perm.fetch_add(1, std::memory_order_relaxed);
-            stage_trace_arrays(b, t, tr, ha, hs, hp, hid, hperm, false);  // ids stay in the batch
+            if (!direct) stage_trace_arrays(b, t, tr, ha, hs, hp, hid, hperm, false);  // ids stay in the batch
         });
-        CK(cudaMemcpyAsync(s->d_traces.as<DevTrace>() + d0, s->traces.data() + d0, (d1 - d0) * sizeof(DevTrace),
+        const bool cdirect = direct && n_perm.load() == 0;
+        if (direct && !cdirect)
+            parallel_for(d1 - d0, 32, [&](uint32_t i) {
+                const uint32_t d = d0 + i, t = s->src_of[d];
+                if (s->status[t] == MSG_OK) stage_trace_arrays(b, t, s->traces[d], ha, hs, hp, hid, hperm, false);
+            });
+        chunk_direct[k] = cdirect;
+        DevTrace* htr = s->h_traces.as<DevTrace>();
+        std::memcpy(htr + d0, s->traces.data() + d0, (d1 - d0) * sizeof(DevTrace));
+        CK(cudaMemcpyAsync(s->d_traces.as<DevTrace>() + d0, htr + d0, (d1 - d0) * sizeof(DevTrace),
                            cudaMemcpyHostToDevice, st));
         const uint64_t j0 = joff(d0), j1 = joff(d1), nj = j1 - j0;
-        if (nj) {
+        if (nj && cdirect) {
+            CK(cudaMemcpyAsync(s->d_arrival.as<double>() + j0, b->arrival_s + jbase + j0, nj * sizeof(double),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(s->d_service.as<double>() + j0, b->service_s + jbase + j0, nj * sizeof(double),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(s->d_prof32.as<int32_t>() + j0, b->profile + jbase + j0, nj * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, st));
+        } else if (nj) {
             CK(cudaMemcpyAsync(s->d_arrival.as<double>() + j0, ha + j0, nj * sizeof(double), cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(s->d_service.as<double>() + j0, hs + j0, nj * sizeof(double), cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(s->d_profile.as<uint8_t>() + j0, hp + j0, nj, cudaMemcpyHostToDevice, st));
@@ -751,6 +801,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
                                    cudaMemcpyHostToDevice, st));
         }
         SimArgs c = a;
+        c.profile32 = cdirect ? s->d_prof32.as<int32_t>() : nullptr;
         c.traces = s->d_traces.as<DevTrace>() + d0;
         c.summary = s->d_summary.as<DevSummary>() + d0;
         c.n_traces = d1 - d0;
@@ -830,6 +881,8 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             fill_summary(o, tr, x);
             handler += x.handler_events;
             const int64_t* ids = tr.has_perm ? hid + tr.job_off : b->job_id + b->offsets[t];
+            int kc = 0;
+            while (kc + 1 < n_chunks && d >= d0s[kc + 1]) ++kc;
             if (x.status == MSG_ERR_JOBS_PENDING) {
                 const int64_t jid = x.pending_rank >= 0 ? ids[x.pending_rank] : -1;
                 res->messages[t] = "JobsPending: job " + std::to_string(jid) + " did not complete";
@@ -837,8 +890,12 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
                 return;
             }
             if (!want_jobs) return;
-            put_rows(res->jobs.p.get() + res->job_off[t], tr.n_jobs, ids, ha + tr.job_off, hj + tr.job_off,
-                     hp + tr.job_off, rows_nt);
+            if (chunk_direct[kc])  // arrival and profile straight from the caller's batch
+                put_rows(res->jobs.p.get() + res->job_off[t], tr.n_jobs, ids, b->arrival_s + b->offsets[t],
+                         hj + tr.job_off, b->profile + b->offsets[t], rows_nt);
+            else
+                put_rows(res->jobs.p.get() + res->job_off[t], tr.n_jobs, ids, ha + tr.job_off, hj + tr.job_off,
+                         hp + tr.job_off, rows_nt);
         });
         pt.mark("  chunk decoded");
     }
@@ -1004,6 +1061,21 @@ msg_status msg_run_batch(msg_engine* eng, const msg_trace_batch* batch, const ms
     st = collect_impl(eng, s, out);
     pt.mark("collect (D2H+decode)");
     return st;
+}
+
+msg_status msg_host_alloc(size_t bytes, void** out) {
+    if (!out) return MSG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (cudaHostAlloc(out, std::max<size_t>(bytes, 64), cudaHostAllocPortable) != cudaSuccess) {
+        *out = nullptr;
+        cudaGetLastError();
+        return MSG_ERR_CUDA;
+    }
+    return MSG_OK;
+}
+
+void msg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
 }
 
 msg_status msg_engine_sync(msg_engine* eng) {

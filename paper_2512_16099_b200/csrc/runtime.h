@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <condition_variable>
 #include <functional>
@@ -21,9 +22,13 @@
 namespace msgk {
 
 // Persistent fork-join pool for the host-side staging / decoding loops: the
-// workers are created once (threads_for_this_process() - 1) and woken per call, so
-// a batch pays no thread creation.  One parallel region at a time (calls
-// from several host threads serialise on the pool).
+// workers are created once (threads_for_this_process() - 1).  A parallel
+// region is published through an atomic generation counter; workers spin on
+// it for a short while after each region (kSpinNs) before blocking on a
+// condition variable, so the back-to-back regions of one msg_run_batch call
+// (a validation pass per pipeline chunk, then the decode) cost no futex
+// wake-ups, and an idle engine costs no CPU.  One parallel region at a time
+// (calls from several host threads serialise on the pool).
 class HostPool {
   public:
     static HostPool& get() {
@@ -40,30 +45,36 @@ class HostPool {
             body();
             return;
         }
-        {
+        std::function<void()> fn = [&body]() { body(); };
+        body_ = &fn;
+        left_.store(n - 1, std::memory_order_relaxed);
+        want_.store((int)n - 1, std::memory_order_release);  // publishes body_ and left_ to the claimers
+        gen_.fetch_add(1);  // seq_cst with the sleeper count below (Dekker pair with loop())
+        if (sleeping_.load() > 0) {
             std::lock_guard<std::mutex> lk(m_);
-            body_ = [&body]() { body(); };
-            want_ = n - 1;
-            left_ = n - 1;
-            ++gen_;
+            cv_.notify_all();
         }
-        cv_.notify_all();
         body();
-        std::unique_lock<std::mutex> lk(m_);
-        done_.wait(lk, [&] { return left_ == 0; });
+        while (left_.load(std::memory_order_acquire) != 0) pause();
         body_ = nullptr;
     }
     ~HostPool() {
+        stop_.store(true, std::memory_order_release);
+        gen_.fetch_add(1, std::memory_order_release);
         {
             std::lock_guard<std::mutex> lk(m_);
-            stop_ = true;
-            ++gen_;
+            cv_.notify_all();
         }
-        cv_.notify_all();
         for (auto& t : workers_) t.join();
     }
 
   private:
+    static constexpr int64_t kSpinNs = 300000;  // 0.3 ms of spinning after a region
+    static void pause() {
+#if defined(__x86_64__) || defined(__i386__)
+        __builtin_ia32_pause();
+#endif
+    }
     HostPool() {
         const unsigned hw = threads_for_this_process();
         for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
@@ -86,29 +97,43 @@ class HostPool {
         return n;
     }
     void loop() {
-        uint64_t seen = 0;
+        uint64_t seen = 0;  // the constructor's generation: a region published before this thread ran is still claimed
         for (;;) {
-            std::function<void()> b;
-            {
-                std::unique_lock<std::mutex> lk(m_);
-                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && want_ > 0); });
-                if (stop_) return;
-                seen = gen_;
-                --want_;
-                b = body_;
+            // wait for the next generation: spin, then block
+            uint64_t g = gen_.load(std::memory_order_acquire);
+            if (g == seen) {
+                const auto t0 = std::chrono::steady_clock::now();
+                unsigned k = 0;
+                while ((g = gen_.load(std::memory_order_acquire)) == seen) {
+                    pause();
+                    if ((++k & 255u) == 0 &&
+                        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
+                                .count() > kSpinNs) {
+                        std::unique_lock<std::mutex> lk(m_);
+                        sleeping_.fetch_add(1);  // seq_cst: run() either sees the sleeper or we see its generation
+                        cv_.wait(lk, [&] { return gen_.load() != seen; });
+                        sleeping_.fetch_sub(1, std::memory_order_acq_rel);
+                        g = gen_.load(std::memory_order_acquire);
+                        break;
+                    }
+                }
             }
-            b();
-            std::lock_guard<std::mutex> lk(m_);
-            if (--left_ == 0) done_.notify_one();
+            seen = g;
+            if (stop_.load(std::memory_order_acquire)) return;
+            if (want_.fetch_sub(1, std::memory_order_acq_rel) <= 0) continue;  // region already fully staffed
+            (*body_)();
+            left_.fetch_sub(1, std::memory_order_acq_rel);
         }
     }
     std::vector<std::thread> workers_;
     std::mutex m_, region_;
-    std::condition_variable cv_, done_;
-    std::function<void()> body_;
-    uint64_t gen_ = 0;
-    unsigned want_ = 0, left_ = 0;
-    bool stop_ = false;
+    std::condition_variable cv_;
+    std::function<void()>* body_ = nullptr;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<int> want_{0};
+    std::atomic<unsigned> left_{0};
+    std::atomic<int> sleeping_{0};
+    std::atomic<bool> stop_{false};
 };
 
 template <class F>

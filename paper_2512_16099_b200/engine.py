@@ -49,6 +49,8 @@ def lib():
         "msg_engine_sync": (C.c_int, [vp]),
         "msg_time_launch": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
         "msg_engine_flush_l2": (C.c_int, [vp]),
+        "msg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+        "msg_host_free": (None, [vp]),
         "msg_result_n_traces": (u32, [vp]),
         "msg_result_summary": (vp, [vp, u32]),
         "msg_result_jobs": (vp, [vp, u32, C.POINTER(u64)]),
@@ -212,6 +214,44 @@ def _view(ptr, n, dtype, owner):
     v = np.asarray(_Mem(ptr, n * dtype.itemsize, owner)).view(dtype)
     v.flags.writeable = False
     return v
+
+
+class _Pinned:
+    """Page-locked host memory from msg_host_alloc, freed with its last view."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        _check(lib().msg_host_alloc(max(int(nbytes), 1), C.byref(p)))
+        self.ptr = p.value
+
+    def __del__(self):
+        try:
+            lib().msg_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """Writable numpy array of n elements in page-locked host memory."""
+    dt = np.dtype(dtype)
+    mem = _Pinned(n * dt.itemsize)
+    if n == 0:
+        return np.zeros(0, dt)
+    return np.asarray(_Mem(mem.ptr, n * dt.itemsize, mem)).view(dt)
+
+
+def pin_batch(batch: TraceBatch) -> TraceBatch:
+    """A copy of `batch` whose job arrays live in page-locked host memory:
+    msg_run_batch then copies them to the device in place (no host staging
+    copy).  Results are identical either way."""
+    arrs = {}
+    for name in ("job_id", "arrival_s", "profile", "service_s"):
+        src = getattr(batch, name)
+        dst = pinned_empty(len(src), src.dtype)
+        dst[:] = src
+        arrs[name] = dst
+    return TraceBatch(batch.offsets.copy(), arrs["job_id"], arrs["arrival_s"], arrs["profile"], arrs["service_s"],
+                      None if batch.config_index is None else batch.config_index.copy())
 
 
 class BatchResult:

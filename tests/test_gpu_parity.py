@@ -207,6 +207,13 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
     assert piped.summaries.tobytes() == plain.summaries.tobytes()
     assert piped.jobs.tobytes() == plain.jobs.tobytes()
     assert np.array_equal(piped.job_offsets, plain.job_offsets)
+    from paper_2512_16099_b200.engine import pin_batch
+
+    monkeypatch.delenv("MSG_NO_PIPELINE")
+    pinned = engine.run_batch(pin_batch(b), cfgs, abi.OUT_JOBS)  # direct inputs (chunk 0 staged: trace 7)
+    assert pinned.summaries.tobytes() == piped.summaries.tobytes()
+    assert pinned.jobs.tobytes() == piped.jobs.tobytes()
+    assert [pinned[t].message for t in range(len(traces))] == [piped[t].message for t in range(len(traces))]
     assert piped[300].code == "JobsPending" and piped[5].code == "TraceUnsorted"
     assert piped[400].code == "BadSpec" and piped[450].code == "BadSpec" and piped[7].ok
     bad = []
@@ -218,7 +225,8 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"MSG_PIPE_POLL": "0"}, {"MSG_JOBS_D2H": "1"}, {"MSG_ROWS_NT": "0"},
-                                 {"MSG_PIPE_W": "1,2,3,1,1,1,1,1"}, {"MSG_NO_PIPELINE": "1"}])
+                                 {"MSG_PIPE_W": "1,2,3,1,1,1,1,1"}, {"MSG_NO_PIPELINE": "1"}, {"PINNED": "1"},
+                                 {"PINNED": "1", "MSG_PIPE_POLL": "0"}])
 def test_pipeline_variants_agree(engine, monkeypatch, env):
     """The pipelined msg_run_batch's variants — chunk-by-chunk decode after
     each chunk's event, job records by copy, plain row stores, other chunk
@@ -226,11 +234,15 @@ def test_pipeline_variants_agree(engine, monkeypatch, env):
     and a completion flag published per trace in mapped host memory)."""
     from paper_2512_16099_b200.engine import generate_batch
 
+    from paper_2512_16099_b200.engine import pin_batch
+
     b = generate_batch(preset("normal25"), 5, 700)
     cfg = [SimConfig(gpu_count=8)]
     want = engine.run_batch(b, cfg, abi.OUT_JOBS)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
+    if env.get("PINNED"):  # inputs in page-locked memory: copied to the device in place
+        b = pin_batch(b)
     got = engine.run_batch(b, cfg, abi.OUT_JOBS)
     assert got.summaries.tobytes() == want.summaries.tobytes()
     assert got.jobs.tobytes() == want.jobs.tobytes()
