@@ -86,6 +86,7 @@ struct BlockScratch {
     unsigned hi[2][32], lo[2][32], tie[2][32], ms[2][32];
     int pay[2][32];
     unsigned sum[2][32];
+    unsigned kh[2][32], kl[2][32], nl[2][32], nb[2][32];  // next_event: the fused placement search's partials
     double q[8];       // dt / slowdown(k), k = 1..7
     double f[8];       // slowdown(k)
     unsigned u[8];     // small broadcasts from one thread / warp 0
@@ -674,7 +675,52 @@ struct ClusterSim {
                 bi = (int)i;
             }
         }
-        block_lexmin(bhi, blo, btie, bms, bi);
+        // The pending arrival's placement search rides in the next-event
+        // exchange when it would dispatch at once (empty queue): the masks
+        // it reads do not change before handle_arrival.  Its scan shares the
+        // timer scan's pass and block reduction (one barrier for both).
+        spec = NS > 1 && a_idx < N && q_head == q_tail;
+        uint64_t skey = ~0ull;
+        unsigned snl = 0, snb = 0;
+        if (spec) {
+            MSG_PH(1);
+            scan_dispatch(a_prof, skey, snl, snb);
+            MSG_PH(0);
+            warp_lexmin(bhi, blo, btie, bms, bi);
+            const unsigned kh = wp::rmin((unsigned)(skey >> 32));
+            const unsigned kl = wp::rmin((unsigned)(skey >> 32) == kh ? (unsigned)skey : NONE);
+            snl = wp::radd(snl);
+            snb = wp::radd(snb);
+            if (L == 0) {
+                sc->hi[bph][W] = bhi;
+                sc->lo[bph][W] = blo;
+                sc->tie[bph][W] = btie;
+                sc->ms[bph][W] = bms;
+                sc->pay[bph][W] = bi;
+                sc->kh[bph][W] = kh;
+                sc->kl[bph][W] = kl;
+                sc->nl[bph][W] = snl;
+                sc->nb[bph][W] = snb;
+            }
+            wp::bsync();
+            const bool v = L < w;
+            bhi = v ? sc->hi[bph][L] : NONE;
+            blo = v ? sc->lo[bph][L] : NONE;
+            btie = v ? sc->tie[bph][L] : NONE;
+            bms = v ? sc->ms[bph][L] : NONE;
+            bi = v ? sc->pay[bph][L] : -1;
+            const unsigned h2 = v ? sc->kh[bph][L] : NONE, l2 = v ? sc->kl[bph][L] : NONE;
+            snl = wp::radd(v ? sc->nl[bph][L] : 0u);
+            snb = wp::radd(v ? sc->nb[bph][L] : 0u);
+            bph ^= 1;
+            warp_lexmin(bhi, blo, btie, bms, bi);
+            const unsigned mh = wp::rmin(h2);
+            const unsigned ml = wp::rmin(h2 == mh ? l2 : NONE);
+            skey = ((uint64_t)mh << 32) | ml;
+            if (!(cflags & CF_LB)) snl = snb = 0;
+        } else {
+            block_lexmin(bhi, blo, btie, bms, bi);
+        }
         double tmin = 0.0;
         slot = -1;
         unsigned winfo = 0;
@@ -685,16 +731,10 @@ struct ClusterSim {
         }
         if (NS > 1) {
             XRec r = xnone();
-            // The pending arrival's placement search rides in the same
-            // exchange when it would dispatch at once (empty queue): the
-            // masks it reads do not change before handle_arrival.
-            spec = a_idx < N && q_head == q_tail;
             if (spec) {
-                MSG_PH(1);
-                uint64_t k;
-                local_dispatch(a_prof, k, r.c[0], r.c[1]);
-                r.pad2 = k;
-                MSG_PH(0);
+                r.pad2 = skey;
+                r.c[0] = snl;
+                r.c[1] = snb;
             }
             r.hi = bhi;
             r.lo = blo;
@@ -743,6 +783,29 @@ struct ClusterSim {
     // the block-wide minimum packed key and the Lazy / Busy candidate counts.
     MSG_DI void local_dispatch(int p, uint64_t& key, unsigned& NL, unsigned& NB) {
         wp::bsync();
+        uint64_t kmin;
+        unsigned nl, nb;
+        scan_dispatch(p, kmin, nl, nb);
+        unsigned hi = (unsigned)(kmin >> 32), lo = (unsigned)kmin, z0 = 0, z1 = 0;
+        int pay = 0;
+        block_lexmin(hi, lo, z0, z1, pay);
+        NL = NB = 0;
+        if (cflags & CF_LB) {
+            if ((g_hi - g_lo) * 7 < 65536) {  // both counts in one reduction
+                const unsigned x = block_sum(nl | (nb << 16));
+                NL = x & 0xFFFFu;
+                NB = x >> 16;
+            } else {
+                NL = block_sum(nl);
+                NB = block_sum(nb);
+            }
+        }
+        key = ((uint64_t)hi << 32) | lo;
+    }
+
+    // This thread's part of local_dispatch: its GPUs' minimum key and
+    // Lazy / Busy candidate counts (no barrier).
+    MSG_DI void scan_dispatch(int p, uint64_t& kmin_out, unsigned& nl_out, unsigned& nb_out) {
         const unsigned n = count_of(p), stride = stride_of(p);
         const unsigned pb = pidx(p, 0);
         const bool dyn = (cflags & CF_DYN) != 0;
@@ -795,21 +858,9 @@ struct ClusterSim {
                 }
             }
         }
-        unsigned hi = (unsigned)(kmin >> 32), lo = (unsigned)kmin, z0 = 0, z1 = 0;
-        int pay = 0;
-        block_lexmin(hi, lo, z0, z1, pay);
-        NL = NB = 0;
-        if (lb) {
-            if ((g_hi - g_lo) * 7 < 65536) {  // both counts in one reduction
-                const unsigned x = block_sum(nl | (nb << 16));
-                NL = x & 0xFFFFu;
-                NB = x >> 16;
-            } else {
-                NL = block_sum(nl);
-                NB = block_sum(nb);
-            }
-        }
-        key = ((uint64_t)hi << 32) | lo;
+        kmin_out = kmin;
+        nl_out = nl;
+        nb_out = nb;
     }
 
     // The decision from the global minimum key and counts.

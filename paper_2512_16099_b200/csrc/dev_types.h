@@ -57,7 +57,8 @@ enum : uint32_t {
     CF_DYN = 2u,     // FeatureFlags::dynamic_partitioning
     CF_MIG = 4u      // FeatureFlags::migration
 };
-enum : uint32_t { OF_JOBS = 1u, OF_EVENTS = 2u, OF_TIMELINE = 4u };
+enum : uint32_t { OF_JOBS = 1u, OF_EVENTS = 2u, OF_TIMELINE = 4u, OF_ZC = 8u /* in-kernel: zero-copy inputs */,
+                   OF_PROG = 16u /* in-kernel: progressive row flushes */ };
 
 struct DevConfig {
     double alpha;     // SimConfig::contention_alpha
@@ -158,6 +159,15 @@ struct SimArgs {
     const int32_t* profile32;  // optional: the caller's int32 profiles (pipelined direct inputs); each
                                // warp narrows its trace's into `profile` before its first event
     const uint32_t* perm;    // arrival order -> rank (only traces with has_perm)
+    // optional (pipelined msg_run_batch, page-locked caller arrays, every
+    // trace in input order): the caller's arrival / service / int32 profile
+    // arrays as mapped host memory, indexed like `arrival`.  Each warp reads
+    // its trace over PCIe one 32-job block at a time as its arrivals reach
+    // the block and publishes the block into arrival / service / profile
+    // (no H2D copy and no host staging before the launch).
+    const double* zc_arrival;
+    const double* zc_service;
+    const int32_t* zc_profile;
     int32_t* queue;          // FCFS queue storage, n_jobs per trace
     JobOut* jobs;
     JobOut* jobs_host;       // optional (pipelined msg_run_batch): a finished trace's records, also
@@ -168,6 +178,13 @@ struct SimArgs {
     DevSummary* summary_host;  // optional (pipelined msg_run_batch): the summary, also in mapped host memory,
     uint32_t* done_host;       // then done_host[t] = done_epoch once the trace's host records are visible
     uint32_t done_epoch;
+    // optional (with jobs_host and done_host): progressive row publication.
+    // prog_host[t] = done_epoch << 32 | n once the records of the trace's
+    // first n jobs (all completed) are in jobs_host; the warp flushes the
+    // completed prefix every 32 arrivals, so the host decodes rows while the
+    // trace still runs.
+    uint64_t* prog_host;
+    uint32_t prog_mask;  // flush when the arrival index is a multiple of prog_mask + 1 (a power of two >= 32)
     uint32_t n_traces;
     uint32_t out_flags;
     // block engine (G > 32): cluster arena, indexed by GPU (cl_goff + g) or
@@ -243,6 +260,7 @@ struct SnapArgs {
     int32_t reserved;
 };
 
+constexpr int kProfileCount = 6;  // profiles.cpp:8-15
 // Constant geometry (profiles.cpp:8-15), packed per profile id.
 constexpr uint32_t kCsPack = 0x112347u;               // nibble p: compute slices
 constexpr uint32_t kMsPack = 0x122448u;               // nibble p: memory slices

@@ -78,7 +78,7 @@ MSG_DI uint64_t time_key(double t) {
 }
 
 template <int SPL>
-struct WarpSmem {
+struct alignas(16) WarpSmem {
     static constexpr int NS = 32 * SPL;  // slots
     static constexpr int NG = 4 * SPL;   // GPUs
     struct alignas(16) RT {
@@ -100,6 +100,14 @@ struct WarpSmem {
     uint8_t apos[NS];  // slot -> its index in act[] while armed
     uint8_t prof[NS];  // instance profile
     uint8_t st[NS];    // ST_*
+    // zero-copy inputs (SimArgs::zc_*): this trace's caller arrays
+    const double* zc_a;
+    const double* zc_s;
+    const int32_t* zc_p;
+    // progressive row flushes (SimArgs::prog_host): rows published so far
+    uint64_t* prog_h;
+    uint32_t prog;
+    uint32_t prog_epoch;
 };
 
 
@@ -118,10 +126,65 @@ struct Decision {
     unsigned evals;
 };
 
+// Zero-copy inputs (SimArgs::zc_*): jobs j0 .. j0+31 read from the
+// caller's page-locked arrays (three independent loads per lane: one PCIe
+// round trip per 32 arrivals) and published into the trace's device
+// arrays, which every later read (arrival prefetch, queue heads, metrics)
+// uses.  Out-of-range profiles and non-positive services are clamped only
+// to keep the kernel in bounds: the host check (staging.h check_trace), run
+// concurrently, rejects such a trace and its results are discarded.  Only
+// in the IO instantiation (TraceSim IO = true), which keeps this code out of
+// the plain kernel's register allocation.
+template <class WS>
+MSG_DI void zc_fetch_block(WS* sm, double* arr, double* svc, uint8_t* prf, uint32_t j0, uint32_t N) {
+    const uint32_t j = j0 + wp::lane();
+    if (j < N) {
+        const double t = sm->zc_a[j];
+        double v = sm->zc_s[j];
+        int p = sm->zc_p[j];
+        if ((unsigned)p >= (unsigned)kProfileCount) p = 0;
+        if (!(v > 0.0)) v = 1.0;
+        arr[j] = t;
+        svc[j] = v;
+        prf[j] = (uint8_t)p;
+    }
+    wp::sync();
+}
+
+// Progressive rows (SimArgs::prog_host): extend the completed prefix (jobs
+// whose record has its gpu set at completion) and, when it grew by a block
+// or more, copy those records to the host, fence, then publish the count.
+template <class WS>
+MSG_DI void rows_flush_block(WS* sm, const JobOut* jobs, JobOut* jobs_h, uint32_t N) {
+    const unsigned L = wp::lane();
+    wp::sync();
+    const uint32_t p = sm->prog;
+    uint32_t q = p;
+    for (;;) {
+        const uint32_t j = q + L;
+        const unsigned nf = ~wp::ballot(j < N && jobs[j].gpu >= 0);
+        const uint32_t adv = nf ? (uint32_t)(wp::ffs(nf) - 1) : 32u;
+        q += adv;
+        if (adv < 32u) break;
+    }
+    if (q - p < 32u) return;  // amortise the system-scope fence
+    for (uint32_t j = p + L; j < q; j += 32) jobs_h[j] = jobs[j];
+    wp::gfence_sys();
+    wp::sync();
+    if (L == 0) {
+        sm->prog = q;
+        *(volatile uint64_t*)sm->prog_h = ((uint64_t)sm->prog_epoch << 32) | q;
+    }
+    wp::sync();
+}
+
+// IO: the pipelined msg_run_batch's host-I/O instantiation (summary / job
+// rows only): zero-copy inputs and progressive row flushes (SimArgs::zc_*,
+// prog_host).
 // SPL: slots per lane (ceil(8G/32)).  DETAIL: the kernel writes the event
 // log / timeline records when requested; the summary-only instantiation has
 // no emission code at all (smaller hot loop, fewer I-cache misses).
-template <int SPL, bool DETAIL = true>
+template <int SPL, bool DETAIL = true, bool IO = false>
 struct TraceSim {
     using WS = WarpSmem<SPL>;
     WS* sm;
@@ -136,6 +199,7 @@ struct TraceSim {
     EventRec* evs;
     double* tl;
     uint32_t N, ev_cap, tl_cap, oflags;
+    uint32_t prog_mask;  // IO: progressive row flush cadence (SimArgs::prog_mask)
     // SimConfig
     int G;
     uint32_t cflags, lazymask;
@@ -215,7 +279,16 @@ struct TraceSim {
         svc = a.service + tr.job_off;
         prf = a.profile + tr.job_off;
         perm = tr.has_perm ? a.perm + tr.job_off : nullptr;
-        if (a.profile32) {  // direct inputs: the caller's int32 profiles, narrowed once per trace
+        oflags = a.out_flags;
+        if (IO && a.zc_arrival) {  // zero-copy inputs: blocks fetched by load_arrival (zc_fetch_block)
+            oflags |= OF_ZC;
+            perm = nullptr;
+            if (L == 0) {
+                sm->zc_a = a.zc_arrival + tr.job_off;
+                sm->zc_s = a.zc_service + tr.job_off;
+                sm->zc_p = a.zc_profile + tr.job_off;
+            }
+        } else if (a.profile32) {  // direct inputs: the caller's int32 profiles, narrowed once per trace
             uint8_t* dst = const_cast<uint8_t*>(prf);
             const int32_t* src = a.profile32 + tr.job_off;
             for (uint32_t j = L; j < N; j += 32) dst[j] = (uint8_t)src[j];
@@ -224,11 +297,20 @@ struct TraceSim {
         queue = a.queue + tr.job_off;
         jobs = a.jobs + tr.job_off;
         jobs_h = a.jobs_host ? a.jobs_host + tr.job_off : nullptr;
+        if (IO && jobs_h && a.prog_host) {
+            oflags |= OF_PROG;
+            prog_mask = a.prog_mask | 31u;
+            if (L == 0) {
+                sm->prog_h = a.prog_host + t;
+                sm->prog = 0;
+                sm->prog_epoch = a.done_epoch;
+            }
+            for (uint32_t j = L; j < N; j += 32) jobs[j].gpu = -1;  // not completed (rows_flush)
+        }
         evs = a.events ? a.events + tr.ev_off : nullptr;
         tl = a.timeline ? a.timeline + 2 * tr.tl_off : nullptr;
         ev_cap = tr.ev_cap;
         tl_cap = tr.tl_cap;
-        oflags = a.out_flags;
         if (!evs) oflags &= ~OF_EVENTS;
         if (!tl) oflags &= ~OF_TIMELINE;
         G = c.G;
@@ -383,6 +465,12 @@ struct TraceSim {
     // (time, job id) order: sim.cpp:118-120 with TimerLater).
     MSG_DI void load_arrival() {
         if (a_idx < N) {
+            if (IO && (oflags & (OF_ZC | OF_PROG)) && (a_idx & 31u) == 0) {
+                if (oflags & OF_ZC)
+                    zc_fetch_block(sm, const_cast<double*>(arr), const_cast<double*>(svc), const_cast<uint8_t*>(prf),
+                                   a_idx, N);
+                if ((oflags & OF_PROG) && a_idx && (a_idx & prog_mask) == 0) rows_flush_block(sm, jobs, jobs_h, N);
+            }
             const uint32_t r = perm ? perm[a_idx] : a_idx;
             a_rank = r;
             a_t = arr[r];
@@ -728,6 +816,12 @@ struct TraceSim {
     // Reconfig events of one create_instance: destroys in instance-vector
     // (creation) order, then the create (gpu.cpp:88-98, sim.cpp:183-195).
     MSG_DI void emit_reconfig(int g, int p, int s, const CreateRes& cr) {
+        if (!DETAIL || !(oflags & OF_EVENTS)) {  // no records: only the count (destroy order is irrelevant)
+            const uint32_t n = (uint32_t)wp::popc(cr.dmask) + (cr.reused ? 0u : 1u);
+            n_reconf += n;
+            n_ev += n;  // emit() counts every event, stored or not
+            return;
+        }
         unsigned m = cr.dmask;
         while (m) {
             int lw;
@@ -1071,35 +1165,45 @@ struct TraceSim {
         s.pending_rank = -1;
         double sw = 0.0, se = 0.0, st = 0.0, first = 0.0, lastc = 0.0;
         if (s.status == STATUS_OK) {
+            const uint32_t pub = (IO && (oflags & OF_PROG)) ? sm->prog : 0u;  // rows already on the host
+            double fa = 0.0, lc = 0.0;      // min arrival / max completion so far (this lane's jobs)
+            unsigned fj = NONE, lj = NONE;  // ... and the first job holding it
             for (uint32_t base = 0; base < N; base += 32) {
                 const uint32_t j = base + L;
                 double w = 0.0, e = 0.0, t = 0.0, a = 0.0, d = 0.0;
                 if (j < N) {
                     a = arr[j];
                     const JobOut jo = jobs[j];
-                    if (jobs_h) jobs_h[j] = jo;  // coalesced: a warp stores 32 consecutive records
+                    if (jobs_h && j >= pub) jobs_h[j] = jo;  // coalesced: a warp stores 32 consecutive records
                     const double sc = jo.sched;
                     d = jo.done;
                     w = wp::dsub(sc, a);
                     e = wp::dsub(d, sc);
                     t = wp::dadd(w, e);
                 }
+                if (j < N) {  // lane-local: jobs j ascend, so a strict compare keeps the earliest on ties
+                    if (fj == NONE || a < fa) fa = a, fj = j;
+                    if (lj == NONE || lc < d) lc = d, lj = j;
+                }
                 const uint32_t n = N - base < 32 ? N - base : 32;
-                for (uint32_t k = 0; k < n; ++k) {
+                for (uint32_t k = 0; k < n; ++k) {  // the sums: sequential, in job-id order
                     const double wk = wp::shfl(w, (int)k), ek = wp::shfl(e, (int)k), tk = wp::shfl(t, (int)k);
-                    const double ak = wp::shfl(a, (int)k), dk = wp::shfl(d, (int)k);
                     sw = wp::dadd(sw, wk);
                     se = wp::dadd(se, ek);
                     st = wp::dadd(st, tk);
-                    if (base + k == 0) {
-                        first = ak;
-                        lastc = dk;
-                    } else {
-                        first = ak < first ? ak : first;  // std::min(first, a)
-                        lastc = lastc < dk ? dk : lastc;  // std::max(last, c)
-                    }
                 }
             }
+            // std::min(first, a) / std::max(last, c) over job-id order keep the
+            // earliest job among equal values: a (value, job) tree with that rule
+            for (int off = 16; off > 0; off >>= 1) {
+                const int src = (int)(L ^ (unsigned)off);
+                const double oa = wp::shfl(fa, src), oc = wp::shfl(lc, src);
+                const unsigned oj = wp::shfl(fj, src), ol = wp::shfl(lj, src);
+                if (oj != NONE && (fj == NONE || oa < fa || (!(fa < oa) && oj < fj))) fa = oa, fj = oj;
+                if (ol != NONE && (lj == NONE || lc < oc || (!(oc < lc) && ol < lj))) lc = oc, lj = ol;
+            }
+            first = fa;
+            lastc = lc;
         } else {
             unsigned mn = NONE;
             for (uint32_t i = q_head + L; i < q_tail; i += 32) {
@@ -1137,9 +1241,9 @@ struct TraceSim {
 
 // One warp, one trace: the body shared by the CUDA kernel and the CPU-side
 // unit-test emulation.
-template <int SPL, bool DETAIL = true>
+template <int SPL, bool DETAIL = true, bool IO = false>
 MSG_DI void simulate_trace(const SimArgs& a, const DevTables* tables, WarpSmem<SPL>* ws, uint32_t t) {
-    TraceSim<SPL, DETAIL> sim;
+    TraceSim<SPL, DETAIL, IO> sim;
     sim.setup(a, tables, ws, t);
     sim.run();
     sim.finish(a.summary + t, a.summary_host ? a.summary_host + t : nullptr);

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cmath>
 #include <immintrin.h>
+#include <sys/mman.h>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -66,6 +67,7 @@ struct msg_staged {
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
     HostBuf h_done;           // run_pipelined: per-trace completion flags (mapped, written by the kernel)
+    HostBuf h_prog;           // run_pipelined: per-trace published row prefixes (epoch << 32 | jobs)
     HostBuf h_traces;         // run_pipelined: pinned copy of the trace descriptors (async H2D)
     uint32_t done_epoch = 0;  // the flag value of the current run
     // device
@@ -93,8 +95,11 @@ namespace {
 // Recycled per-job row buffers: a batch result's rows (72 B per job) go back
 // here when the result is freed, so repeated batches of similar size write
 // into already-faulted pages instead of fresh allocations.
+struct FreeRows {
+    void operator()(msg_job_row* p) const { std::free(p); }
+};
 struct RowBuf {
-    std::unique_ptr<msg_job_row[]> p;
+    std::unique_ptr<msg_job_row[], FreeRows> p;
     uint64_t cap = 0;
 };
 std::mutex g_rows_m;
@@ -113,7 +118,15 @@ RowBuf take_rows(uint64_t n) {
     }
     RowBuf b;
     b.cap = std::max<uint64_t>(n, 1);
-    b.p.reset(new msg_job_row[b.cap]);
+    // 2 MiB-aligned and backed by transparent huge pages where the kernel
+    // offers them (madvise mode): ~36x fewer first-touch faults for a C2
+    // result (59 MB of rows).
+    constexpr size_t kHuge = 2u << 20;
+    const size_t bytes = (b.cap * sizeof(msg_job_row) + kHuge - 1) & ~(kHuge - 1);
+    void* m = std::aligned_alloc(kHuge, bytes);
+    if (!m) throw std::bad_alloc();
+    madvise(m, bytes, MADV_HUGEPAGE);
+    b.p.reset(static_cast<msg_job_row*>(m));
     return b;
 }
 
@@ -197,6 +210,18 @@ bool host_pinned(const void* p, size_t bytes) {
         if (at.type != cudaMemoryTypeHost) return false;
     }
     return true;
+}
+
+// Device view of page-locked host memory (mapped: with unified addressing
+// the host address itself), or null when `p` is not CUDA-registered.
+template <class T>
+const T* dev_view(const T* p) {
+    cudaPointerAttributes at{};
+    if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? static_cast<const T*>(at.devicePointer) : nullptr;
 }
 
 msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
@@ -694,12 +719,13 @@ void fill_summary(msg_trace_summary& o, const DevTrace& tr, const DevSummary& x)
     o.timeline_sum = x.tl_sum;
 }
 
-msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* s, msg_batch_result** out) {
+msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* s, msg_batch_result** out,
+                         bool allow_zc = true) {
     const uint32_t T = (uint32_t)s->traces.size();
     const bool want_jobs = (s->out_flags & MSG_OUT_JOBS) != 0;
     PhaseTimer pt;
     uint32_t d0s[kMaxPipeChunks + 1];
-    const int n_chunks = pipe_bounds(T, d0s);
+    int n_chunks = pipe_bounds(T, d0s);
     // Job records reach the host through the kernel's own stores into mapped
     // pinned memory as each trace finishes (MSG_JOBS_D2H=1: one copy per chunk
     // after its kernel instead).
@@ -728,6 +754,23 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         if (++s->done_epoch == 0) s->done_epoch = 1;  // 0 is the zeroed buffer
     }
     volatile uint32_t* hdone = poll ? s->h_done.as<uint32_t>() : nullptr;
+    // Progressive rows (MSG_PIPE_PROG=0 disables): each warp also publishes
+    // the completed prefix of its trace's records as it goes, so the host
+    // decodes rows while the kernels run instead of after each trace ends
+    // (the decode is host-memory-bound: ~95 MB of traffic for C2).
+    const bool prog = poll && want_jobs && !jobs_d2h && !env_off("MSG_PIPE_PROG");
+    if (prog) {
+        const void* had = s->h_prog.p;
+        CK(s->h_prog.ensure(std::max<uint32_t>(T, 1) * sizeof(uint64_t)));
+        if (s->h_prog.p != had) std::memset(s->h_prog.p, 0, s->h_prog.cap);  // epoch 0 is never current
+    }
+    volatile uint64_t* hprog = prog ? s->h_prog.as<uint64_t>() : nullptr;
+    // flush cadence in arrivals (MSG_PROG_EVERY, a power of two >= 32; tuning)
+    uint32_t prog_mask = 63;
+    if (const char* e = std::getenv("MSG_PROG_EVERY")) {
+        const unsigned long v = std::strtoul(e, nullptr, 10);
+        if (v >= 32 && (v & (v - 1)) == 0) prog_mask = (uint32_t)v - 1;
+    }
     double* ha = s->h_arrival.as<double>();
     double* hs = s->h_service.as<double>();
     uint8_t* hp = s->h_profile.as<uint8_t>();
@@ -750,7 +793,70 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     if (direct) CK(s->d_prof32.ensure(N * sizeof(int32_t)));
     CK(s->h_traces.ensure(std::max<uint32_t>(T, 1) * sizeof(DevTrace)));
     uint8_t chunk_direct[kMaxPipeChunks] = {};
-    for (int k = 0; k < n_chunks; ++k) {
+    // Zero copy (direct inputs; MSG_NO_ZC=1 disables): the kernel reads the
+    // caller's arrays in place over PCIe as each trace's arrivals reach them
+    // (engine_core.cuh zc_fetch), so the whole batch launches at once, before
+    // any host pass over the jobs, and the checks run on the host threads
+    // under the kernel.  A trace failing its check is reported as such (its
+    // device results are ignored); a valid trace whose ids are not increasing
+    // needs the rank permutation, so then the batch re-runs staged.
+    const double* zc_a = direct && allow_zc && !std::getenv("MSG_NO_ZC") ? dev_view(b->arrival_s + jbase) : nullptr;
+    const double* zc_s = zc_a ? dev_view(b->service_s + jbase) : nullptr;
+    const int32_t* zc_p = zc_s ? dev_view(b->profile + jbase) : nullptr;
+    if (zc_p) {
+        cudaStream_t st = eng->pstream[0];
+        n_chunks = 1;
+        d0s[1] = T;
+        DevTrace* htr = s->h_traces.as<DevTrace>();
+        std::memcpy(htr, s->traces.data(), T * sizeof(DevTrace));
+        CK(cudaMemcpyAsync(s->d_traces.as<DevTrace>(), htr, T * sizeof(DevTrace), cudaMemcpyHostToDevice, st));
+        SimArgs c = a;
+        c.perm = nullptr;
+        c.zc_arrival = zc_a;
+        c.zc_service = zc_s;
+        c.zc_profile = zc_p;
+        if (want_jobs && !jobs_d2h) c.jobs_host = s->h_jobs.as<JobOut>();
+        if (poll) {
+            c.summary_host = s->h_summary.as<DevSummary>();
+            c.done_host = s->h_done.as<uint32_t>();
+            c.done_epoch = s->done_epoch;
+            if (prog) {
+                c.prog_host = s->h_prog.as<uint64_t>();
+                c.prog_mask = prog_mask;
+            }
+        }
+        if (pt.on) CK(cudaEventRecord(eng->ev0, st));
+        cudaError_t e = launch_sim(s->spl, c, st);
+        if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim (zero copy)");
+        if (pt.on) CK(cudaEventRecord(eng->ev1, st));
+        ++eng->launches;
+        if (!poll)
+            CK(cudaMemcpyAsync(s->h_summary.as<DevSummary>(), s->d_summary.as<DevSummary>(), T * sizeof(DevSummary),
+                               cudaMemcpyDeviceToHost, st));
+        if (want_jobs && jobs_d2h)
+            CK(cudaMemcpyAsync(s->h_jobs.as<JobOut>(), s->d_jobs.as<JobOut>(), s->n_jobs * sizeof(JobOut),
+                               cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(eng->pevent[0], st));
+        pt.mark("  zero-copy launch");
+        std::atomic<uint32_t> n_perm{0};
+        parallel_for(T, 32, [&](uint32_t d) {
+            const uint32_t t = s->src_of[d];
+            TraceCheck ck = check_trace(b, t);
+            if (ck.status != MSG_OK) {
+                s->status[t] = ck.status;
+                s->message[t] = std::move(ck.message);
+            } else if (!ck.identity) {
+                n_perm.fetch_add(1, std::memory_order_relaxed);
+            }
+        });
+        pt.mark("  checks (under the kernel)");
+        if (n_perm.load()) {
+            CK(cudaEventSynchronize(eng->pevent[0]));
+            return run_pipelined(eng, b, s, out, false);
+        }
+        chunk_direct[0] = 1;
+    }
+    for (int k = 0; k < n_chunks && !zc_p; ++k) {
         const uint32_t d0 = d0s[k], d1 = d0s[k + 1];
         if (d0 == d1) continue;
         cudaStream_t st = eng->pstream[k];
@@ -810,6 +916,10 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             c.summary_host = s->h_summary.as<DevSummary>() + d0;
             c.done_host = s->h_done.as<uint32_t>() + d0;
             c.done_epoch = s->done_epoch;
+            if (prog) {
+                c.prog_host = s->h_prog.as<uint64_t>() + d0;
+                c.prog_mask = prog_mask;
+            }
         }
         cudaError_t e = launch_sim(s->spl, c, st);
         if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim (pipelined)");
@@ -866,7 +976,101 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         std::atomic_thread_fence(std::memory_order_acquire);
         return true;
     };
-    for (int k = 0; k < (poll ? 1 : n_chunks); ++k) {
+    auto chunk_of = [&](uint32_t d) {
+        int kc = 0;
+        while (kc + 1 < n_chunks && d >= d0s[kc + 1]) ++kc;
+        return kc;
+    };
+    // Rows [from, to) of device trace d into the result.
+    const bool skip_decode = std::getenv("MSG_DEBUG_SKIP_DECODE") != nullptr;  // timing experiments only: no rows
+    auto rows_range = [&](uint32_t d, uint32_t from, uint32_t to) {
+        if (skip_decode) return;
+        const uint32_t t = s->src_of[d];
+        const DevTrace& tr = s->traces[d];
+        const int64_t* ids = (tr.has_perm ? hid + tr.job_off : b->job_id + b->offsets[t]) + from;
+        msg_job_row* dst = res->jobs.p.get() + res->job_off[t] + from;
+        const JobOut* jo = hj + tr.job_off + from;
+        if (chunk_direct[chunk_of(d)])  // arrival and profile straight from the caller's batch
+            put_rows(dst, to - from, ids, b->arrival_s + b->offsets[t] + from, jo, b->profile + b->offsets[t] + from,
+                     rows_nt);
+        else
+            put_rows(dst, to - from, ids, ha + tr.job_off + from, jo, hp + tr.job_off + from, rows_nt);
+    };
+    // Device trace d has finished (summary and records visible): its summary
+    // and its rows from `from` on.
+    auto finish_trace = [&](uint32_t d, uint32_t from) {
+        const uint32_t t = s->src_of[d];
+        const DevTrace& tr = s->traces[d];
+        const DevSummary& x = ds[d];
+        fill_summary(res->summaries[t], tr, x);
+        handler += x.handler_events;
+        if (x.status == MSG_ERR_JOBS_PENDING) {
+            const int64_t* ids = tr.has_perm ? hid + tr.job_off : b->job_id + b->offsets[t];
+            const int64_t jid = x.pending_rank >= 0 ? ids[x.pending_rank] : -1;
+            res->messages[t] = "JobsPending: job " + std::to_string(jid) + " did not complete";
+            pending = true;
+            return;
+        }
+        if (want_jobs && from < tr.n_jobs) rows_range(d, from, tr.n_jobs);
+    };
+    if (prog) {
+        // Each host thread polls its share of the traces: new published
+        // prefixes are decoded as they appear, a finished trace gets its tail
+        // and summary.
+        HostPool& pool = HostPool::get();
+        const unsigned nth = std::min(pool.size(), std::max(1u, T / 32));
+        std::atomic<unsigned> next_id{0};
+        pool.run(nth, [&] {
+            // blocks of 16 traces dealt round-robin: every thread gets traces
+            // of every pipeline chunk (the chunks start at different times)
+            const unsigned i = next_id.fetch_add(1);
+            std::vector<uint32_t> open, dec;
+            for (uint32_t b0 = 16 * i; b0 < T; b0 += 16 * nth)
+                for (uint32_t d = b0; d < std::min(T, b0 + 16); ++d)
+                    if (s->status[s->src_of[d]] == MSG_OK) open.push_back(d);
+            dec.assign(open.size(), 0);
+            for (uint32_t idle = 1; !open.empty();) {
+                bool moved = false;
+                for (size_t k = 0; k < open.size();) {
+                    const uint32_t d = open[k];
+                    if (hdone[d] == s->done_epoch) {
+                        std::atomic_thread_fence(std::memory_order_acquire);
+                        finish_trace(d, dec[k]);
+                        open[k] = open.back();
+                        dec[k] = dec.back();
+                        open.pop_back();
+                        dec.pop_back();
+                        moved = true;
+                        continue;
+                    }
+                    const uint64_t pw = hprog[d];
+                    if ((uint32_t)(pw >> 32) == s->done_epoch && (uint32_t)pw > dec[k]) {
+                        std::atomic_thread_fence(std::memory_order_acquire);
+                        rows_range(d, dec[k], (uint32_t)pw);
+                        dec[k] = (uint32_t)pw;
+                        moved = true;
+                    }
+                    ++k;
+                }
+                if (moved) {
+                    idle = 1;
+                    continue;
+                }
+                _mm_pause();
+                if ((++idle & 4095u) == 0) {  // every kernel ended and a trace never published: failure
+                    bool all = true;
+                    for (int k = 0; k < n_chunks && all; ++k)
+                        all = d0s[k] == d0s[k + 1] || cudaEventQuery(eng->pevent[k]) != cudaErrorNotReady;
+                    if (all && hdone[open[0]] != s->done_epoch) {
+                        lost = true;
+                        return;
+                    }
+                }
+            }
+        });
+        pt.mark("  progressive decode");
+    }
+    for (int k = 0; k < (poll ? 1 : n_chunks) && !prog; ++k) {
         const uint32_t d0 = poll ? 0 : d0s[k], d1 = poll ? T : d0s[k + 1];
         if (d0 == d1) continue;
         if (!poll) CK(cudaEventSynchronize(eng->pevent[k]));
@@ -875,27 +1079,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             const uint32_t d = d0 + i, t = s->src_of[d];
             if (s->status[t] != MSG_OK) return;  // failed its check: reported as such, no rows
             if (poll && !wait_done(d)) return;
-            const DevTrace& tr = s->traces[d];
-            const DevSummary& x = ds[d];
-            msg_trace_summary& o = res->summaries[t];
-            fill_summary(o, tr, x);
-            handler += x.handler_events;
-            const int64_t* ids = tr.has_perm ? hid + tr.job_off : b->job_id + b->offsets[t];
-            int kc = 0;
-            while (kc + 1 < n_chunks && d >= d0s[kc + 1]) ++kc;
-            if (x.status == MSG_ERR_JOBS_PENDING) {
-                const int64_t jid = x.pending_rank >= 0 ? ids[x.pending_rank] : -1;
-                res->messages[t] = "JobsPending: job " + std::to_string(jid) + " did not complete";
-                pending = true;
-                return;
-            }
-            if (!want_jobs) return;
-            if (chunk_direct[kc])  // arrival and profile straight from the caller's batch
-                put_rows(res->jobs.p.get() + res->job_off[t], tr.n_jobs, ids, b->arrival_s + b->offsets[t],
-                         hj + tr.job_off, b->profile + b->offsets[t], rows_nt);
-            else
-                put_rows(res->jobs.p.get() + res->job_off[t], tr.n_jobs, ids, ha + tr.job_off, hj + tr.job_off,
-                         hp + tr.job_off, rows_nt);
+            finish_trace(d, 0);
         });
         pt.mark("  chunk decoded");
     }
@@ -906,6 +1090,12 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             eng->last_error = "CudaError: a pipelined chunk completed without publishing a trace";
             return MSG_ERR_CUDA;
         }
+    }
+    if (pt.on && zc_p) {
+        float ms = 0.f;
+        CK(cudaEventSynchronize(eng->ev1));
+        CK(cudaEventElapsedTime(&ms, eng->ev0, eng->ev1));
+        std::fprintf(stderr, "[msg]   zero-copy kernel       %8.3f ms (device)\n", ms);
     }
     if (pending && want_jobs) {  // the reference throws for these traces: drop their rows
         uint64_t w = 0;
@@ -922,6 +1112,69 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     }
     s->handler_events = handler.load();
     *out = res.release();
+    return MSG_OK;
+}
+
+uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
+// Warm start (msg_engine_create): the pipeline's streams, every event-loop
+// kernel loaded, the host thread pool started, and a workspace for
+// MSG_RESERVE_JOBS jobs (default 2^20; 0: none) in MSG_RESERVE_TRACES traces
+// (default 8192) — pinned and device buffers plus a pre-faulted row buffer —
+// so that the first msg_run_batch of up to that size pays no lazy kernel
+// load, stream creation, allocation or first-touch page fault.
+msg_status warm_engine(msg_engine* eng) {
+    PhaseTimer pt;
+    for (int k = 0; k < kMaxPipeChunks; ++k) {
+        CK(cudaStreamCreateWithFlags(&eng->pstream[k], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&eng->pevent[k], cudaEventDisableTiming));
+    }
+    pt.mark("warm: streams");
+    CK(preload_engine_kernels());
+    pt.mark("warm: kernels loaded");
+    parallel_for(1u << 12, 1, [](uint32_t) {});
+    pt.mark("warm: host pool");
+    const uint64_t J = env_u64("MSG_RESERVE_JOBS", 1ull << 20);
+    const uint64_t T = std::max<uint64_t>(env_u64("MSG_RESERVE_TRACES", 8192), 1);
+    if (!J) return MSG_OK;
+    eng->cached = new msg_staged();
+    msg_staged* s = eng->cached;
+    // the sizes stage_impl / run_pipelined ask for at J jobs and T traces
+    CK(s->h_arrival.ensure(J * sizeof(double)));
+    CK(s->h_service.ensure(J * sizeof(double)));
+    CK(s->h_profile.ensure(J));
+    CK(s->h_ids.ensure(J * sizeof(int64_t)));
+    CK(s->h_perm.ensure(J * sizeof(uint32_t)));
+    CK(s->h_jobs.ensure(J * sizeof(JobOut)));
+    CK(s->h_summary.ensure(T * sizeof(DevSummary)));
+    CK(s->h_traces.ensure(T * sizeof(DevTrace)));
+    CK(s->h_done.ensure(T * sizeof(uint32_t)));
+    std::memset(s->h_done.p, 0, s->h_done.cap);
+    CK(s->h_prog.ensure(T * sizeof(uint64_t)));
+    std::memset(s->h_prog.p, 0, s->h_prog.cap);
+    pt.mark("warm: pinned buffers");
+    CK(s->d_arrival.ensure(J * sizeof(double)));
+    CK(s->d_service.ensure(J * sizeof(double)));
+    CK(s->d_profile.ensure(J));
+    CK(s->d_prof32.ensure(J * sizeof(int32_t)));
+    CK(s->d_perm.ensure(J * sizeof(uint32_t)));
+    CK(s->d_queue.ensure(J * sizeof(int32_t)));
+    CK(s->d_jobs.ensure(J * sizeof(JobOut)));
+    CK(s->d_traces.ensure(T * sizeof(DevTrace)));
+    CK(s->d_summary.ensure(T * sizeof(DevSummary)));
+    pt.mark("warm: device buffers");
+    RowBuf rows = take_rows(J);
+    msg_job_row* r = rows.p.get();
+    const uint64_t per_page = 4096 / sizeof(msg_job_row) + 1;
+    parallel_for((uint32_t)((J + 8191) / 8192), 1, [&](uint32_t i) {  // first touch, in parallel
+        const uint64_t hi = std::min<uint64_t>(J, (uint64_t)(i + 1) * 8192);
+        for (uint64_t j = (uint64_t)i * 8192; j < hi; j += per_page) r[j].id = 0;
+    });
+    give_rows(std::move(rows));
+    pt.mark("warm: row buffer");
     return MSG_OK;
 }
 
@@ -948,7 +1201,9 @@ msg_status msg_engine_create(int device, msg_engine** out) {
     if (err != cudaSuccess || device < 0 || device >= n) {
         return MSG_ERR_CUDA;  // no usable device: there is no CPU fallback
     }
+    PhaseTimer pt;
     CK(cudaSetDevice(device));
+    pt.mark("create: context");
     cudaDeviceProp prop{};
     CK(cudaGetDeviceProperties(&prop, device));
     e->sm_count = prop.multiProcessorCount;
@@ -967,6 +1222,8 @@ msg_status msg_engine_create(int device, msg_engine** out) {
     build_score_table(t, stab.data());
     CK(e->score_tab.ensure(sizeof(uint16_t) * kScoreTab));
     CK(cudaMemcpy(e->score_tab.p, stab.data(), sizeof(uint16_t) * kScoreTab, cudaMemcpyHostToDevice));
+    const msg_status ws = warm_engine(eng);
+    if (ws != MSG_OK) return ws;
     *out = e.release();
     return MSG_OK;
 }
@@ -1066,7 +1323,7 @@ msg_status msg_run_batch(msg_engine* eng, const msg_trace_batch* batch, const ms
 msg_status msg_host_alloc(size_t bytes, void** out) {
     if (!out) return MSG_ERR_INVALID_ARGUMENT;
     *out = nullptr;
-    if (cudaHostAlloc(out, std::max<size_t>(bytes, 64), cudaHostAllocPortable) != cudaSuccess) {
+    if (cudaHostAlloc(out, std::max<size_t>(bytes, 64), cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
         *out = nullptr;
         cudaGetLastError();
         return MSG_ERR_CUDA;

@@ -16,6 +16,7 @@
 #if defined(__CUDACC__)
 
 #define MSG_DI __device__ __forceinline__
+#define MSG_DNI __device__ __noinline__
 #define MSG_GLOBAL __global__
 
 namespace wp {

@@ -19,6 +19,7 @@ struct uint4 {
 };
 
 #define MSG_DI inline
+#define MSG_DNI inline
 
 namespace wp {
 

@@ -216,6 +216,29 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
     assert [pinned[t].message for t in range(len(traces))] == [piped[t].message for t in range(len(traces))]
     assert piped[300].code == "JobsPending" and piped[5].code == "TraceUnsorted"
     assert piped[400].code == "BadSpec" and piped[450].code == "BadSpec" and piped[7].ok
+    # Every valid trace in id order: the zero-copy launch (the kernel reads
+    # the page-locked inputs in place, checks run under it); the failing
+    # traces run sanitized on the device and are reported from their checks.
+    traces_zc = list(traces)
+    traces_zc[7] = [Job(1, 0.0, 5, 2.0), Job(3, 1.0, 4, 1.0), Job(4, 1.0, 5, 3.0), Job(9, 1.0, 0, 0.5)]
+    traces_zc[8] = [Job(0, 0.0, 9, 1.0), Job(1, 0.5, 2, 1.0)]  # UnknownProfile (clamped in-kernel)
+    traces_zc[9] = [Job(0, 0.0, 2, float("nan"))]  # NaN service
+    bz = TraceBatch.from_traces(traces_zc, config_index=[1 if t == 300 else 0 for t in range(len(traces))])
+    zc = engine.run_batch(pin_batch(bz), cfgs, abi.OUT_JOBS)
+    monkeypatch.setenv("MSG_NO_ZC", "1")
+    nozc = engine.run_batch(pin_batch(bz), cfgs, abi.OUT_JOBS)
+    monkeypatch.delenv("MSG_NO_ZC")
+    plain_z = engine.run_batch(bz, cfgs, abi.OUT_JOBS)
+    for other in (nozc, plain_z):
+        assert zc.summaries.tobytes() == other.summaries.tobytes()
+        assert zc.jobs.tobytes() == other.jobs.tobytes()
+        assert [zc[t].message for t in range(len(traces))] == [other[t].message for t in range(len(traces))]
+    assert zc[8].code == "UnknownProfile" and zc[9].code == "BadSpec" and zc[7].ok and zc[5].code == "TraceUnsorted"
+    ref_z = rb.ref_run_batch_results(bz, cfgs)
+    for t in (7, 8, 10):  # (9: the reference accepts NaN times, this engine rejects them: DESIGN §8)
+        r = ref_z[t]
+        r.events = r.frag_timeline = None
+        assert not diff_results(r, zc[t]), t
     bad = []
     for t, (r, g) in enumerate(zip(ref, piped)):
         r.events = r.frag_timeline = None
@@ -226,7 +249,9 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
 
 @pytest.mark.parametrize("env", [{"MSG_PIPE_POLL": "0"}, {"MSG_JOBS_D2H": "1"}, {"MSG_ROWS_NT": "0"},
                                  {"MSG_PIPE_W": "1,2,3,1,1,1,1,1"}, {"MSG_NO_PIPELINE": "1"}, {"PINNED": "1"},
-                                 {"PINNED": "1", "MSG_PIPE_POLL": "0"}])
+                                 {"PINNED": "1", "MSG_PIPE_POLL": "0"}, {"PINNED": "1", "MSG_NO_ZC": "1"},
+                                 {"PINNED": "1", "MSG_JOBS_D2H": "1"}, {"MSG_PIPE_PROG": "0"},
+                                 {"PINNED": "1", "MSG_PIPE_PROG": "0"}])
 def test_pipeline_variants_agree(engine, monkeypatch, env):
     """The pipelined msg_run_batch's variants — chunk-by-chunk decode after
     each chunk's event, job records by copy, plain row stores, other chunk

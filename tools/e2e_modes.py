@@ -51,19 +51,17 @@ def timeit(flags, n=15, batch=None):
     return f"median {1e3*ts[n//2]:.3f} min {1e3*ts[0]:.3f} ms"
 
 
-modes = [("jobs", {}, abi.OUT_JOBS), ("PINNED jobs", {}, abi.OUT_JOBS), ("PINNED summaries", {}, 0),
-         ("PINNED jobs 4 chunks", {"MSG_PIPE_W": "1,1,1,1"}, abi.OUT_JOBS),
-         ("PINNED jobs 16 chunks?", {"MSG_PIPE_W": "1,1,1,1,1,1,1,1"}, abi.OUT_JOBS),
-         ("PINNED jobs front-light", {"MSG_PIPE_W": "0.5,1,1,1,1,1,1,1.5"}, abi.OUT_JOBS), ("summaries only", {}, 0), ("jobs rows_nt=0", {"MSG_ROWS_NT": "0"}, abi.OUT_JOBS),
-         ("jobs 4 chunks", {"MSG_PIPE_W": "1,1,1,1"}, abi.OUT_JOBS),
-         ("jobs 2 chunks", {"MSG_PIPE_W": "1,1"}, abi.OUT_JOBS),
-         ("jobs 8 chunks front-light", {"MSG_PIPE_W": "1,1,1.5,1.5,1.5,1.5,1.5,1.5"}, abi.OUT_JOBS),
-         ("jobs no poll", {"MSG_PIPE_POLL": "0"}, abi.OUT_JOBS),
-         ("jobs", {}, abi.OUT_JOBS)]
+modes = [("jobs", {}, abi.OUT_JOBS), ("PINNED jobs (zero copy)", {}, abi.OUT_JOBS),
+         ("PINNED jobs zc, no progressive rows", {"MSG_PIPE_PROG": "0"}, abi.OUT_JOBS),
+         ("PINNED jobs staged chunks", {"MSG_NO_ZC": "1"}, abi.OUT_JOBS),
+         ("PINNED jobs staged chunks, no prog", {"MSG_NO_ZC": "1", "MSG_PIPE_PROG": "0"}, abi.OUT_JOBS),
+         ("PINNED summaries", {}, 0), ("summaries only", {}, 0),
+         ("jobs, no progressive rows", {"MSG_PIPE_PROG": "0"}, abi.OUT_JOBS),
+         ("PINNED jobs (zero copy)", {}, abi.OUT_JOBS), ("jobs", {}, abi.OUT_JOBS)]
 for name, env, flags in modes:
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
-    print(f"{name:28s} {timeit(flags, batch=bp if name.startswith('PINNED') else None)}", flush=True)
+    print(f"{name:40s} {timeit(flags, batch=bp if name.startswith('PINNED') else None)}", flush=True)
     for k2, v in old.items():
         if v is None:
             del os.environ[k2]
