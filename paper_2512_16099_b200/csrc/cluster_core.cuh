@@ -103,6 +103,137 @@ struct BlockScratch {
     uint64_t xbar[2];         // mbarriers counting the pushed bytes, by round parity
 };
 
+// ---- pieces of the block engine used at several call sites -----------------
+// Free functions.  All kept out of line (MSG_DNI) they cut the C4 kernel
+// from 25,880 to 13,744 SASS instructions (r02f ncu: 79% i-cache hit rate,
+// 'no_instruction' the third stall), but most calls cost more than the
+// misses they save: 20K-arrival C4 prefix 0.367 s vs 0.341 s inlined
+// (profiles/r02, c4_variants_r02t.log); only the exchange reduction pays
+// (r02u).  CL_OOL_* select each for A/B builds.
+#ifndef CL_OOL_WORD
+#define CL_OOL_WORD MSG_DI
+#endif
+#ifndef CL_OOL_TL
+#define CL_OOL_TL MSG_DI
+#endif
+#ifndef CL_OOL_XRED
+#define CL_OOL_XRED MSG_DNI  // out of line: 0.332 vs 0.337 s inlined (r02u)
+#endif
+
+// Idle-exact bit of placement (p, s): the profile's first bit + the start's
+// index among its legal starts (strides are powers of two).
+MSG_DI unsigned cl_pidx(int p, int s) {
+    return ((0x00B74210u >> (4 * p)) & 0xFu) + ((unsigned)s >> ((0x011233u >> (4 * p)) & 0xFu));
+}
+
+// GPU word (busy/blocked masks, running count), idle-exact bits and 4-mask
+// cost id from the GPU's 8 slots (gpu.cpp:10-48).
+struct GpuWord {
+    unsigned w, x, id;
+};
+CL_OOL_WORD GpuWord cl_gpu_word(const uint8_t* st8, const uint8_t* pr8, const DevTables* tb) {
+    unsigned bc = 0, bm = 0, km = 0, k = 0, x = 0;
+    for (int s = 0; s < 8; ++s) {
+        const uint8_t v = st8[s];
+        if (v == ST_EMPTY) continue;
+        const int p = pr8[s];
+        const unsigned m = fpm(p, s);
+        if (v == ST_IDLE) {
+            x |= 1u << cl_pidx(p, s);
+        } else if (v == ST_DRAIN) {
+            km |= m;
+        } else {
+            bc |= fpc(p, s);
+            bm |= m;
+            km |= m;
+            k += v == ST_RUN;
+        }
+    }
+    GpuWord r;
+    r.w = bc | (bm << 8) | (km << 16) | (k << 24);
+    r.x = x;
+    const unsigned row = (unsigned)wp::popc(bc) * 9u + (unsigned)wp::popc(bm);
+    r.id = tb->cost4pair[tb->idealid[row] * 32u + tb->feasid[km]];
+    return r;
+}
+
+// Timeline mean of a cost total (numerators over 25200) over G GPUs.
+CL_OOL_TL double cl_tl_mean(unsigned long long ktot, double inv_g, int G) {
+    const double tot = wp::ddiv((double)ktot, 25200.0);
+    return inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
+}
+
+// dt / slowdown(k)
+CL_OOL_TL double cl_ddiv(double a, double b) { return wp::ddiv(a, b); }
+
+// Lexicographic (hi, lo, tie, ms) minimum within the warp; every lane ends
+// with the winning tuple and its payload.
+MSG_DI void cl_warp_lexmin(unsigned& hi, unsigned& lo, unsigned& tie, unsigned& ms, int& pay) {
+    const unsigned mhi = wp::rmin(hi);
+    const unsigned mlo = wp::rmin(hi == mhi ? lo : NONE);
+    const unsigned mtie = wp::rmin((hi == mhi && lo == mlo) ? tie : NONE);
+    const bool m3 = hi == mhi && lo == mlo && tie == mtie;
+    const unsigned mms = wp::rmin(m3 ? ms : NONE);
+    const int wl = wp::ffs(wp::ballot(m3 && ms == mms)) - 1;
+    pay = wp::shfl(pay, wl < 0 ? 0 : wl);
+    hi = mhi;
+    lo = mlo;
+    tie = mtie;
+    ms = mms;
+}
+
+MSG_DI XRec cl_xnone() {
+    XRec r;
+    r.hi = r.lo = r.tie = r.ms = NONE;
+    r.slot = -1;
+    r.job = -1;
+    r.info = 0;
+    r.w = 0;
+    r.rem = r.tkey = 0.0;
+    r.c[0] = r.c[1] = r.c[2] = r.c[3] = 0;
+    r.mx = 0;
+    r.pad = 0;
+    r.ks[0] = r.ks[1] = 0;
+    r.pad2 = ~0ull;
+    return r;
+}
+
+// One warp: the identical reduction of records in[0 .. n) (one per lane;
+// lanes >= n contribute cl_xnone()) — lexicographic minimum with the
+// winner's payload, sums, OR, max — stored by lane 0 into *out.
+CL_OOL_XRED void cl_xreduce(const XRec* in, unsigned n, XRec* out) {
+    const unsigned L = wp::lane();
+    const XRec x = L < n ? in[L] : cl_xnone();
+    int pay = (int)L;
+    unsigned hi = x.hi, lo = x.lo, tie = x.tie, ms = x.ms;
+    cl_warp_lexmin(hi, lo, tie, ms, pay);
+    XRec o;
+    o.hi = hi;
+    o.lo = lo;
+    o.tie = tie;
+    o.ms = ms;
+    o.slot = wp::shfl(x.slot, pay);
+    o.job = wp::shfl(x.job, pay);
+    o.info = wp::shfl(x.info, pay);
+    o.rem = wp::shfl(x.rem, pay);
+    o.tkey = wp::shfl(x.tkey, pay);
+    o.w = wp::ror(x.w);
+    for (int k = 0; k < 4; ++k) o.c[k] = wp::radd(x.c[k]);
+    o.mx = wp::rmax(x.mx);
+    o.pad = 0;
+    {  // pad2: a second 64-bit minimum (the speculative arrival decision key)
+        const unsigned h = wp::rmin((unsigned)(x.pad2 >> 32));
+        const unsigned l = wp::rmin((unsigned)(x.pad2 >> 32) == h ? (unsigned)x.pad2 : NONE);
+        o.pad2 = ((uint64_t)h << 32) | l;
+    }
+    for (int k = 0; k < 2; ++k) {  // parts < 2^35: 20-bit split keeps the lane sums in 32 bits
+        const unsigned lo20 = wp::radd((unsigned)(x.ks[k] & 0xFFFFFu));
+        const unsigned hi20 = wp::radd((unsigned)(x.ks[k] >> 20));
+        o.ks[k] = ((unsigned long long)hi20 << 20) + lo20;
+    }
+    if (L == 0) *out = o;
+}
+
 template <bool DETAIL>
 struct ClusterSim {
     BlockScratch* sc;
@@ -166,12 +297,16 @@ struct ClusterSim {
     bool spec;
     uint64_t spec_key;
     unsigned spec_nl, spec_nb;
+    // next_event -> advance_all: this thread's first kHeld active entries
+    static constexpr int kHeld = 4;
+    double held_rem[kHeld];
+    unsigned held_k[kHeld];  // running count of the entry's GPU, 0: not Running
 
     // ------------------------------------------------------------- tables
     MSG_DI unsigned rank2(unsigned bc, unsigned bm) const { return tb->cost2rank[wp::popc(bc) * 256 + bm]; }
     MSG_DI unsigned k2w(unsigned wd) const { return tb->rank2k[rank2(w_bc(wd), w_bm(wd))]; }
     MSG_DI static unsigned pidx(int p, int s) {  // idle-exact bit of placement (p, s)
-        return ((0x00B74210u >> (4 * p)) & 0xFu) + (unsigned)s / stride_of(p);
+        return cl_pidx(p, s);
     }
     MSG_DI bool own(int g) const { return g >= g_lo && g < g_hi; }
     MSG_DI unsigned& W_(int g) { return gw[g - g_lo]; }  // owned GPU's mask word
@@ -180,17 +315,7 @@ struct ClusterSim {
     // Lexicographic (hi, lo, tie, ms) minimum within the warp; every lane
     // ends with the winning tuple and its payload.
     MSG_DI void warp_lexmin(unsigned& hi, unsigned& lo, unsigned& tie, unsigned& ms, int& pay) {
-        const unsigned mhi = wp::rmin(hi);
-        const unsigned mlo = wp::rmin(hi == mhi ? lo : NONE);
-        const unsigned mtie = wp::rmin((hi == mhi && lo == mlo) ? tie : NONE);
-        const bool m3 = hi == mhi && lo == mlo && tie == mtie;
-        const unsigned mms = wp::rmin(m3 ? ms : NONE);
-        const int wl = wp::ffs(wp::ballot(m3 && ms == mms)) - 1;
-        pay = wp::shfl(pay, wl < 0 ? 0 : wl);
-        hi = mhi;
-        lo = mlo;
-        tie = mtie;
-        ms = mms;
+        cl_warp_lexmin(hi, lo, tie, ms, pay);
     }
     // ... and over the whole block (one __syncthreads).
     MSG_DI void block_lexmin(unsigned& hi, unsigned& lo, unsigned& tie, unsigned& ms, int& pay) {
@@ -222,54 +347,7 @@ struct ClusterSim {
     }
 
     // ----------------------------------------------------------- exchange
-    MSG_DI static XRec xnone() {
-        XRec r;
-        r.hi = r.lo = r.tie = r.ms = NONE;
-        r.slot = -1;
-        r.job = -1;
-        r.info = 0;
-        r.w = 0;
-        r.rem = r.tkey = 0.0;
-        r.c[0] = r.c[1] = r.c[2] = r.c[3] = 0;
-        r.mx = 0;
-        r.pad = 0;
-        r.ks[0] = r.ks[1] = 0;
-        r.pad2 = ~0ull;
-        return r;
-    }
-    // Identical reduction of one record per lane (lanes beyond the senders
-    // hold xnone()) in every CTA: lexicographic minimum with the winner's
-    // payload, sums, OR, max.
-    MSG_DI XRec warp_reduce(const XRec& x) {
-        int pay = (int)L;
-        unsigned hi = x.hi, lo = x.lo, tie = x.tie, ms = x.ms;
-        warp_lexmin(hi, lo, tie, ms, pay);
-        XRec o;
-        o.hi = hi;
-        o.lo = lo;
-        o.tie = tie;
-        o.ms = ms;
-        o.slot = wp::shfl(x.slot, pay);
-        o.job = wp::shfl(x.job, pay);
-        o.info = wp::shfl(x.info, pay);
-        o.rem = wp::shfl(x.rem, pay);
-        o.tkey = wp::shfl(x.tkey, pay);
-        o.w = wp::ror(x.w);
-        for (int k = 0; k < 4; ++k) o.c[k] = wp::radd(x.c[k]);
-        o.mx = wp::rmax(x.mx);
-        o.pad = 0;
-        {  // pad2: a second 64-bit minimum (the speculative arrival decision key)
-            const unsigned h = wp::rmin((unsigned)(x.pad2 >> 32));
-            const unsigned l = wp::rmin((unsigned)(x.pad2 >> 32) == h ? (unsigned)x.pad2 : NONE);
-            o.pad2 = ((uint64_t)h << 32) | l;
-        }
-        for (int k = 0; k < 2; ++k) {  // parts < 2^35: 20-bit split keeps the lane sums in 32 bits
-            const unsigned lo20 = wp::radd((unsigned)(x.ks[k] & 0xFFFFFu));
-            const unsigned hi20 = wp::radd((unsigned)(x.ks[k] >> 20));
-            o.ks[k] = ((unsigned long long)hi20 << 20) + lo20;
-        }
-        return o;
-    }
+    MSG_DI static XRec xnone() { return cl_xnone(); }
 
     // Cluster-wide reduction of one record per shard (see the header).  The
     // caller passes a block-uniform record; every thread of every shard
@@ -292,8 +370,7 @@ struct ClusterSim {
                     wp::xpush(&sc->xin[par][sh], reinterpret_cast<const uint4*>(&r), (int)(sizeof(XRec) / 16), L,
                               &sc->xbar[par]);
                 wp::xwait(&sc->xbar[par], use, S);
-                const XRec o = warp_reduce(L < S ? sc->xin[par][L] : xnone());
-                if (L == 0) sc->xr = o;
+                cl_xreduce(sc->xin[par], S, &sc->xr);
             }
             wp::bsync();
             r = sc->xr;
@@ -308,19 +385,16 @@ struct ClusterSim {
                     for (int i = 0; i < (int)(sizeof(XRec) / 16); ++i) q[i] = src[i];
                     wp::st_release_sys(&dst->stamp[par][sh][dv], stamp);
                 }
-                XRec x = xnone();
+                XInbox* me = sc->ib[dv];
                 if (L < D) {
-                    XInbox* me = sc->ib[dv];
                     const uint64_t t0 = wp::gtime_ns();
                     unsigned spins = 0;
                     while (wp::ld_acquire_sys(&me->stamp[par][sh][L]) != stamp) {
                         wp::spin_pause();
                         if ((++spins & 1023u) == 0 && wp::gtime_ns() - t0 > 30000000000ull) wp::fail_stop();
                     }
-                    x = me->rec[par][sh][L];
                 }
-                const XRec o = warp_reduce(x);
-                if (L == 0) sc->xr2 = o;
+                cl_xreduce(me->rec[par][sh], D, &sc->xr2);
             }
             wp::bsync();
             r = sc->xr2;
@@ -528,30 +602,12 @@ struct ClusterSim {
     // busy/blocked masks (gpu.cpp:10-48), running count, idle-exact
     // placements, 4-mask cost id; keeps the shard's integer cost total current.
     MSG_DI void refresh_gpu(int g) {
-        unsigned bc = 0, bm = 0, km = 0, k = 0, x = 0;
-        for (int s = 0; s < 8; ++s) {
-            const uint8_t v = st[8 * g + s];
-            if (v == ST_EMPTY) continue;
-            const int p = prof[8 * g + s];
-            const unsigned m = fpm(p, s);
-            if (v == ST_IDLE) {
-                x |= 1u << pidx(p, s);
-            } else if (v == ST_DRAIN) {
-                km |= m;
-            } else {
-                bc |= fpc(p, s);
-                bm |= m;
-                km |= m;
-                k += v == ST_RUN;
-            }
-        }
+        const GpuWord r = cl_gpu_word(st + 8 * g, prof + 8 * g, tb);
         const int l = g - g_lo;
-        gw[l] = bc | (bm << 8) | (km << 16) | (k << 24);
-        gx[l] = x;
-        const unsigned row = (unsigned)wp::popc(bc) * 9u + (unsigned)wp::popc(bm);
-        const uint8_t id = tb->cost4pair[tb->idealid[row] * 32u + tb->feasid[km]];
-        sc->ksum += (unsigned long long)tb->cost4k[id] - (unsigned long long)tb->cost4k[gcid[l]];
-        gcid[l] = id;
+        gw[l] = r.w;
+        gx[l] = r.x;
+        sc->ksum += (unsigned long long)tb->cost4k[r.id] - (unsigned long long)tb->cost4k[gcid[l]];
+        gcid[l] = (uint8_t)r.id;
     }
 
     // ------------------------------------------ active list (single thread)
@@ -585,18 +641,27 @@ struct ClusterSim {
         const double dt = wp::dsub(now, t_prev);
         t_prev = now;
         if (!(dt > 0.0)) return;
-        if (T < 7) sc->q[T] = wp::ddiv(dt, sc->f[T]);
+        // dt / slowdown(k): lane k-1 of every warp, fetched by shuffle
+        const double q = L < 7 ? cl_ddiv(dt, sc->f[L]) : 0.0;
+#pragma unroll
+        for (int h = 0; h < kHeld; ++h) {
+            const uint32_t i = T + (uint32_t)h * NT;
+            const unsigned k = i < n_act ? held_k[h] : 0u;
+            const double qk = wp::shfl(q, k ? (int)k - 1 : 0);
+            if (k) arem[i] = wp::dsub(held_rem[h], qk);
+        }
+        if (n_act <= (uint32_t)kHeld * NT) return;
+        if (W == 0 && L < 7) sc->q[L] = q;
         wp::bsync();
 #pragma unroll 4
-        for (uint32_t i = T; i < n_act; i += NT)
+        for (uint32_t i = T + (uint32_t)kHeld * NT; i < n_act; i += NT)
             if (ast[i] == ST_RUN) arem[i] = wp::dsub(arem[i], sc->q[w_k(W_(aslot[i] >> 3)) - 1]);
         // no trailing barrier: every reader of arem starts with one, and
         // the next timer scan revisits entry i on the same thread
     }
 
     MSG_DI void record_sample(double t, unsigned long long ktot) {
-        const double tot = wp::ddiv((double)ktot, 25200.0);
-        tl_mean = inv_g != 0.0 ? wp::dmul(tot, inv_g) : wp::ddiv(tot, (double)G);
+        tl_mean = cl_tl_mean(ktot, inv_g, G);
         if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && T == 0 && gs == 0) {
             tl[2 * n_tl] = t;
             tl[2 * n_tl + 1] = tl_mean;
@@ -648,17 +713,27 @@ struct ClusterSim {
         wp::bsync();
         unsigned bhi = NONE, blo = NONE, btie = NONE, bms = NONE;
         int bi = -1;
+        // This thread's first kHeld entries keep (remaining work, running
+        // count) in registers for advance_all (nothing changes them between
+        // the scan and the advance): its update needs no reload, no barrier.
 #pragma unroll 4
-        for (uint32_t i = T; i < n_act; i += NT) {
+        for (uint32_t i = T, j = 0; i < n_act; i += NT, ++j) {
             const uint8_t s = ast[i];
             double t;
             if (s == ST_RUN) {
-                double r = arem[i];
-                if (r < 0.0) r = 0.0;
-                t = wp::dadd(now, wp::dmul(r, sc->f[w_k(W_(aslot[i] >> 3)) - 1]));
+                const double r0 = arem[i];
+                const unsigned k = w_k(W_(aslot[i] >> 3));
+                const double r = r0 < 0.0 ? 0.0 : r0;
+                t = wp::dadd(now, wp::dmul(r, sc->f[k - 1]));
                 atkey[i] = t;
+#pragma unroll
+                for (int h = 0; h < kHeld; ++h)
+                    if (j == (uint32_t)h) held_rem[h] = r0, held_k[h] = k;
             } else {
                 t = atkey[i];
+#pragma unroll
+                for (int h = 0; h < kHeld; ++h)
+                    if (j == (uint32_t)h) held_k[h] = 0;
             }
             const uint64_t tk = time_key(t);
             const unsigned hi = (unsigned)(tk >> 32), lo = (unsigned)tk;

@@ -185,6 +185,10 @@ struct SimArgs {
     // trace still runs.
     uint64_t* prog_host;
     uint32_t prog_mask;  // flush when the arrival index is a multiple of prog_mask + 1 (a power of two >= 32)
+    // IO kernel: jobs_host holds SoA columns over the batch's rows_soa jobs —
+    // sched f64 [rows_soa], done f64 [rows_soa], gpu | migrations << 32 u64
+    // [rows_soa] — so each warp store covers whole 128-byte lines over PCIe
+    uint64_t rows_soa;
     uint32_t n_traces;
     uint32_t out_flags;
     // block engine (G > 32): cluster arena, indexed by GPU (cl_goff + g) or

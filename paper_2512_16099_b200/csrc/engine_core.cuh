@@ -104,6 +104,10 @@ struct alignas(16) WarpSmem {
     const double* zc_a;
     const double* zc_s;
     const int32_t* zc_p;
+    // IO kernel: this trace's SoA host columns (SimArgs::rows_soa)
+    double* rows_s;
+    double* rows_d;
+    uint64_t* rows_gm;
     // progressive row flushes (SimArgs::prog_host): rows published so far
     uint64_t* prog_h;
     uint32_t prog;
@@ -126,15 +130,16 @@ struct Decision {
     unsigned evals;
 };
 
-// Zero-copy inputs (SimArgs::zc_*): jobs j0 .. j0+31 read from the
-// caller's page-locked arrays (three independent loads per lane: one PCIe
-// round trip per 32 arrivals) and published into the trace's device
-// arrays, which every later read (arrival prefetch, queue heads, metrics)
-// uses.  Out-of-range profiles and non-positive services are clamped only
-// to keep the kernel in bounds: the host check (staging.h check_trace), run
-// concurrently, rejects such a trace and its results are discarded.  Only
-// in the IO instantiation (TraceSim IO = true), which keeps this code out of
-// the plain kernel's register allocation.
+// Zero-copy inputs (SimArgs::zc_*), IO kernel only: jobs j0 .. j0+31 read
+// from the caller's page-locked arrays when the trace's arrivals reach the
+// block (three independent loads per lane: one PCIe round trip per 32
+// arrivals) and published into the trace's device arrays, which every
+// later read (arrival prefetch, queue heads, metrics) uses.  Out-of-range
+// profiles and non-positive services are clamped only to keep the kernel
+// in bounds: the host check (staging.h check_trace), run concurrently,
+// rejects such a trace and its results are discarded.  (Staging the next
+// block asynchronously with cp.async into shared memory was slower on the
+// B200: profiles/r02, e2e_zc_r02p.log.)
 template <class WS>
 MSG_DI void zc_fetch_block(WS* sm, double* arr, double* svc, uint8_t* prf, uint32_t j0, uint32_t N) {
     const uint32_t j = j0 + wp::lane();
@@ -151,11 +156,19 @@ MSG_DI void zc_fetch_block(WS* sm, double* arr, double* svc, uint8_t* prf, uint3
     wp::sync();
 }
 
+// One job's record into the IO kernel's SoA host columns.
+template <class WS>
+MSG_DI void store_row_host(WS* sm, uint32_t j, const JobOut& jo) {
+    sm->rows_s[j] = jo.sched;
+    sm->rows_d[j] = jo.done;
+    sm->rows_gm[j] = (uint64_t)(uint32_t)jo.gpu | ((uint64_t)(uint32_t)jo.mig << 32);
+}
+
 // Progressive rows (SimArgs::prog_host): extend the completed prefix (jobs
 // whose record has its gpu set at completion) and, when it grew by a block
 // or more, copy those records to the host, fence, then publish the count.
 template <class WS>
-MSG_DI void rows_flush_block(WS* sm, const JobOut* jobs, JobOut* jobs_h, uint32_t N) {
+MSG_DI void rows_flush_block(WS* sm, const JobOut* jobs, uint32_t N) {
     const unsigned L = wp::lane();
     wp::sync();
     const uint32_t p = sm->prog;
@@ -168,7 +181,7 @@ MSG_DI void rows_flush_block(WS* sm, const JobOut* jobs, JobOut* jobs_h, uint32_
         if (adv < 32u) break;
     }
     if (q - p < 32u) return;  // amortise the system-scope fence
-    for (uint32_t j = p + L; j < q; j += 32) jobs_h[j] = jobs[j];
+    for (uint32_t j = p + L; j < q; j += 32) store_row_host(sm, j, jobs[j]);
     wp::gfence_sys();
     wp::sync();
     if (L == 0) {
@@ -297,6 +310,12 @@ struct TraceSim {
         queue = a.queue + tr.job_off;
         jobs = a.jobs + tr.job_off;
         jobs_h = a.jobs_host ? a.jobs_host + tr.job_off : nullptr;
+        if (IO && jobs_h && L == 0) {
+            double* base = reinterpret_cast<double*>(a.jobs_host);
+            sm->rows_s = base + tr.job_off;
+            sm->rows_d = base + a.rows_soa + tr.job_off;
+            sm->rows_gm = reinterpret_cast<uint64_t*>(base + 2 * a.rows_soa) + tr.job_off;
+        }
         if (IO && jobs_h && a.prog_host) {
             oflags |= OF_PROG;
             prog_mask = a.prog_mask | 31u;
@@ -469,7 +488,7 @@ struct TraceSim {
                 if (oflags & OF_ZC)
                     zc_fetch_block(sm, const_cast<double*>(arr), const_cast<double*>(svc), const_cast<uint8_t*>(prf),
                                    a_idx, N);
-                if ((oflags & OF_PROG) && a_idx && (a_idx & prog_mask) == 0) rows_flush_block(sm, jobs, jobs_h, N);
+                if ((oflags & OF_PROG) && a_idx && (a_idx & prog_mask) == 0) rows_flush_block(sm, jobs, N);
             }
             const uint32_t r = perm ? perm[a_idx] : a_idx;
             a_rank = r;
@@ -661,7 +680,8 @@ struct TraceSim {
             const unsigned ms = armed ? (drain ? mv[i] : 0u) : NONE;
             const uint64_t ka = ((uint64_t)hi << 32) | lo, kb = ((uint64_t)tie << 32) | ms;
             const uint64_t ba = ((uint64_t)bhi << 32) | blo, bb = ((uint64_t)btie << 32) | bms;
-            const bool better = ka < ba || (ka == ba && kb < bb);
+            // the first entry needs no compare (an unarmed one carries the all-NONE key)
+            const bool better = i == 0 || ka < ba || (ka == ba && kb < bb);
             bhi = better ? hi : bhi;
             blo = better ? lo : blo;
             btie = better ? tie : btie;
@@ -1174,7 +1194,10 @@ struct TraceSim {
                 if (j < N) {
                     a = arr[j];
                     const JobOut jo = jobs[j];
-                    if (jobs_h && j >= pub) jobs_h[j] = jo;  // coalesced: a warp stores 32 consecutive records
+                    if (IO && jobs_h && j >= pub)
+                        store_row_host(sm, j, jo);  // SoA: three coalesced 256-byte stores per warp
+                    else if (!IO && jobs_h)
+                        jobs_h[j] = jo;  // coalesced: a warp stores 32 consecutive records
                     const double sc = jo.sched;
                     d = jo.done;
                     w = wp::dsub(sc, a);

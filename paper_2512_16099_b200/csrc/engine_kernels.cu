@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MSG_SIM_MINB) sim_kernel(
     WarpSmem<SPL>* ws = reinterpret_cast<WarpSmem<SPL>*>(smem + sizeof(DevTables) + w * sizeof(WarpSmem<SPL>));
     const uint32_t t = blockIdx.x * kWarpsPerBlock + w;
     if (t >= a.n_traces || a.traces[t].large) return;
+
 #ifdef MSG_TRACE_TIMES
     const uint64_t t0 = wp::gtime_ns();
 #endif

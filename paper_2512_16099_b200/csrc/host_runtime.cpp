@@ -174,8 +174,27 @@ inline void put_row(msg_job_row* dst, int64_t id, double arrival, const JobOut& 
 // = 9 aligned vectors): the row buffer is far larger than the caches and is
 // not read back here, so the stores skip the read-for-ownership.
 // nt false (MSG_ROWS_NT=0): plain stores.
-template <class P>
-inline void put_rows(msg_job_row* rows, uint32_t n, const int64_t* ids, const double* ha, const JobOut* hj,
+// Job records as the kernels leave them on the host: AoS JobOut (event-loop
+// kernel) or SoA columns sched / done / gpu | migrations << 32 (the
+// pipelined IO kernel: every warp store then fills whole 128-byte lines).
+struct JobsAoS {
+    const JobOut* p;
+    JobOut operator[](uint64_t i) const { return p[i]; }
+    JobsAoS operator+(uint64_t i) const { return {p + i}; }
+};
+struct JobsSoA {
+    const double* sched;
+    const double* done;
+    const uint64_t* gm;
+    JobOut operator[](uint64_t i) const {
+        const uint64_t x = gm[i];
+        return JobOut{sched[i], done[i], (int32_t)(uint32_t)x, (int32_t)(uint32_t)(x >> 32)};
+    }
+    JobsSoA operator+(uint64_t i) const { return {sched + i, done + i, gm + i}; }
+};
+
+template <class P, class J>
+inline void put_rows(msg_job_row* rows, uint32_t n, const int64_t* ids, const double* ha, const J hj,
                      const P* hp, bool nt) {
     uint32_t r = 0;
     if (nt) {
@@ -398,8 +417,15 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     if (!s->init.empty())
         CK(cudaMemcpyAsync(s->d_init.p, s->init.data(), s->init.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                            st));
-    // The pageable vectors above must stay valid until the copies finish.
-    CK(cudaStreamSynchronize(st));
+    // Pageable sources: cudaMemcpyAsync returns once they are staged.  The
+    // pipelined path orders its streams after these copies with an event
+    // (no host wait); the plain path launches on this stream anyway, but its
+    // callers read the staged object right away, so it waits.
+    if (defer_arrays) {
+        CK(cudaEventRecord(eng->staged, st));
+    } else {
+        CK(cudaStreamSynchronize(st));
+    }
     return MSG_OK;
 }
 
@@ -719,6 +745,13 @@ void fill_summary(msg_trace_summary& o, const DevTrace& tr, const DevSummary& x)
     o.timeline_sum = x.tl_sum;
 }
 
+// Pauses between two idle polling sweeps over mapped host flags (tuning:
+// MSG_POLL_BACKOFF).
+int poll_backoff() {
+    const char* e = std::getenv("MSG_POLL_BACKOFF");
+    return e ? std::atoi(e) : 32;
+}
+
 msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* s, msg_batch_result** out,
                          bool allow_zc = true) {
     const uint32_t T = (uint32_t)s->traces.size();
@@ -739,6 +772,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     // kernels still running (MSG_PIPE_POLL=0: chunk by chunk after each
     // chunk's event).
     const bool poll = !jobs_d2h && !env_off("MSG_PIPE_POLL");
+    const int kPollBackoff = poll_backoff();
     const bool rows_nt = !env_off("MSG_ROWS_NT");
     for (int k = 0; k < n_chunks; ++k) {
         if (!eng->pstream[k]) CK(cudaStreamCreateWithFlags(&eng->pstream[k], cudaStreamNonBlocking));
@@ -754,23 +788,6 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         if (++s->done_epoch == 0) s->done_epoch = 1;  // 0 is the zeroed buffer
     }
     volatile uint32_t* hdone = poll ? s->h_done.as<uint32_t>() : nullptr;
-    // Progressive rows (MSG_PIPE_PROG=0 disables): each warp also publishes
-    // the completed prefix of its trace's records as it goes, so the host
-    // decodes rows while the kernels run instead of after each trace ends
-    // (the decode is host-memory-bound: ~95 MB of traffic for C2).
-    const bool prog = poll && want_jobs && !jobs_d2h && !env_off("MSG_PIPE_PROG");
-    if (prog) {
-        const void* had = s->h_prog.p;
-        CK(s->h_prog.ensure(std::max<uint32_t>(T, 1) * sizeof(uint64_t)));
-        if (s->h_prog.p != had) std::memset(s->h_prog.p, 0, s->h_prog.cap);  // epoch 0 is never current
-    }
-    volatile uint64_t* hprog = prog ? s->h_prog.as<uint64_t>() : nullptr;
-    // flush cadence in arrivals (MSG_PROG_EVERY, a power of two >= 32; tuning)
-    uint32_t prog_mask = 63;
-    if (const char* e = std::getenv("MSG_PROG_EVERY")) {
-        const unsigned long v = std::strtoul(e, nullptr, 10);
-        if (v >= 32 && (v & (v - 1)) == 0) prog_mask = (uint32_t)v - 1;
-    }
     double* ha = s->h_arrival.as<double>();
     double* hs = s->h_service.as<double>();
     uint8_t* hp = s->h_profile.as<uint8_t>();
@@ -803,6 +820,28 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     const double* zc_a = direct && allow_zc && !std::getenv("MSG_NO_ZC") ? dev_view(b->arrival_s + jbase) : nullptr;
     const double* zc_s = zc_a ? dev_view(b->service_s + jbase) : nullptr;
     const int32_t* zc_p = zc_s ? dev_view(b->profile + jbase) : nullptr;
+    // Progressive rows (default with zero copy; MSG_PIPE_PROG=0 / 1 forces
+    // off / on): each warp also publishes the completed prefix of its
+    // trace's records as it goes, so the host decodes rows while the kernel
+    // runs instead of after each trace ends (the decode is host-memory-bound:
+    // ~95 MB of traffic for C2).  With staged chunks the finish times are
+    // already spread by the chunks' staggered starts, and there the flushes
+    // cost more than they save (profiles/r02, e2e_zc logs).
+    const char* pe = std::getenv("MSG_PIPE_PROG");
+    const bool prog = poll && want_jobs && !jobs_d2h && (pe ? pe[0] != '0' : zc_p != nullptr);
+    if (prog) {
+        const void* had = s->h_prog.p;
+        CK(s->h_prog.ensure(std::max<uint32_t>(T, 1) * sizeof(uint64_t)));
+        if (s->h_prog.p != had) std::memset(s->h_prog.p, 0, s->h_prog.cap);  // epoch 0 is never current
+    }
+    volatile uint64_t* hprog = prog ? s->h_prog.as<uint64_t>() : nullptr;
+    // flush cadence in arrivals (MSG_PROG_EVERY, a power of two >= 32; tuning)
+    uint32_t prog_mask = 31;
+    if (const char* e = std::getenv("MSG_PROG_EVERY")) {
+        const unsigned long v = std::strtoul(e, nullptr, 10);
+        if (v >= 32 && (v & (v - 1)) == 0) prog_mask = (uint32_t)v - 1;
+    }
+    for (int k = 0; k < n_chunks; ++k) CK(cudaStreamWaitEvent(eng->pstream[k], eng->staged, 0));
     if (zc_p) {
         cudaStream_t st = eng->pstream[0];
         n_chunks = 1;
@@ -825,6 +864,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
                 c.prog_mask = prog_mask;
             }
         }
+        if (want_jobs && !jobs_d2h) c.rows_soa = s->n_jobs;
         if (pt.on) CK(cudaEventRecord(eng->ev0, st));
         cudaError_t e = launch_sim(s->spl, c, st);
         if (e != cudaSuccess) return cuda_fail(eng, e, "launch_sim (zero copy)");
@@ -919,6 +959,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
             if (prog) {
                 c.prog_host = s->h_prog.as<uint64_t>() + d0;
                 c.prog_mask = prog_mask;
+                if (want_jobs) c.rows_soa = s->n_jobs;  // the IO kernel
             }
         }
         cudaError_t e = launch_sim(s->spl, c, st);
@@ -964,6 +1005,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         while (k + 1 < n_chunks && d >= d0s[k + 1]) ++k;
         for (uint32_t spins = 1;; ++spins) {
             if (hdone[d] == s->done_epoch) break;
+            for (int k = 1; k < kPollBackoff / 8; ++k) _mm_pause();
             if ((spins & 4095u) == 0) {
                 const cudaError_t q = cudaEventQuery(eng->pevent[k]);
                 if (q != cudaErrorNotReady && hdone[d] != s->done_epoch) {
@@ -983,18 +1025,27 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     };
     // Rows [from, to) of device trace d into the result.
     const bool skip_decode = std::getenv("MSG_DEBUG_SKIP_DECODE") != nullptr;  // timing experiments only: no rows
+    // the IO kernel (zero copy or progressive rows) leaves SoA columns
+    const bool io_soa = want_jobs && !jobs_d2h && (zc_p || prog);
+    const double* hjd = s->h_jobs.as<double>();
     auto rows_range = [&](uint32_t d, uint32_t from, uint32_t to) {
         if (skip_decode) return;
         const uint32_t t = s->src_of[d];
         const DevTrace& tr = s->traces[d];
         const int64_t* ids = (tr.has_perm ? hid + tr.job_off : b->job_id + b->offsets[t]) + from;
         msg_job_row* dst = res->jobs.p.get() + res->job_off[t] + from;
-        const JobOut* jo = hj + tr.job_off + from;
-        if (chunk_direct[chunk_of(d)])  // arrival and profile straight from the caller's batch
-            put_rows(dst, to - from, ids, b->arrival_s + b->offsets[t] + from, jo, b->profile + b->offsets[t] + from,
-                     rows_nt);
+        auto put = [&](auto jo) {
+            if (chunk_direct[chunk_of(d)])  // arrival and profile straight from the caller's batch
+                put_rows(dst, to - from, ids, b->arrival_s + b->offsets[t] + from, jo,
+                         b->profile + b->offsets[t] + from, rows_nt);
+            else
+                put_rows(dst, to - from, ids, ha + tr.job_off + from, jo, hp + tr.job_off + from, rows_nt);
+        };
+        if (io_soa)
+            put(JobsSoA{hjd, hjd + s->n_jobs, reinterpret_cast<const uint64_t*>(hjd + 2 * s->n_jobs)} +
+                (tr.job_off + from));
         else
-            put_rows(dst, to - from, ids, ha + tr.job_off + from, jo, hp + tr.job_off + from, rows_nt);
+            put(JobsAoS{hj + tr.job_off + from});
     };
     // Device trace d has finished (summary and records visible): its summary
     // and its rows from `from` on.
@@ -1056,7 +1107,10 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
                     idle = 1;
                     continue;
                 }
-                _mm_pause();
+                // back off (~2 us) after a sweep without news: the flags and
+                // prefixes share cache lines with the kernel's ongoing
+                // PCIe writes, and tight polling slows those writes down
+                for (int k = 0; k < kPollBackoff; ++k) _mm_pause();
                 if ((++idle & 4095u) == 0) {  // every kernel ended and a trace never published: failure
                     bool all = true;
                     for (int k = 0; k < n_chunks && all; ++k)
@@ -1214,6 +1268,7 @@ msg_status msg_engine_create(int device, msg_engine** out) {
     CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&e->ev0));
     CK(cudaEventCreate(&e->ev1));
+    CK(cudaEventCreateWithFlags(&e->staged, cudaEventDisableTiming));
     DevTables t;
     if (build_tables(&t) != 31) return MSG_ERR_INVALID_ARGUMENT;
     CK(e->tables.ensure(sizeof(DevTables)));
@@ -1235,6 +1290,7 @@ void msg_engine_destroy(msg_engine* e) {
     if (e->stream) cudaStreamSynchronize(e->stream);
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
+    if (e->staged) cudaEventDestroy(e->staged);
     for (int k = 0; k < 8; ++k) {
         if (e->pstream[k]) {
             cudaStreamSynchronize(e->pstream[k]);

@@ -226,6 +226,7 @@ struct msg_engine {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t staged = nullptr;  // stage_impl's copies on `stream` (the pipelined path waits on it)
     msgk::DevBuf tables;
     msgk::DevBuf score_tab;  // the arrival scorer's per-word table (host_tables.h, build_score_table)
     msgk::DevBuf flush;

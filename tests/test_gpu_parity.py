@@ -251,7 +251,8 @@ def test_pipelined_batch_matches_reference_with_failures(engine, monkeypatch):
                                  {"MSG_PIPE_W": "1,2,3,1,1,1,1,1"}, {"MSG_NO_PIPELINE": "1"}, {"PINNED": "1"},
                                  {"PINNED": "1", "MSG_PIPE_POLL": "0"}, {"PINNED": "1", "MSG_NO_ZC": "1"},
                                  {"PINNED": "1", "MSG_JOBS_D2H": "1"}, {"MSG_PIPE_PROG": "0"},
-                                 {"PINNED": "1", "MSG_PIPE_PROG": "0"}])
+                                 {"PINNED": "1", "MSG_PIPE_PROG": "0"}, {"MSG_PIPE_PROG": "1"},
+                                 {"PINNED": "1", "MSG_PROG_EVERY": "128"}])
 def test_pipeline_variants_agree(engine, monkeypatch, env):
     """The pipelined msg_run_batch's variants — chunk-by-chunk decode after
     each chunk's event, job records by copy, plain row stores, other chunk

@@ -10,14 +10,15 @@ from paper_2512_16099_b200.model import SimConfig, preset  # noqa: E402
 eng = Engine(0)
 b = pin_batch(generate_batch(preset("normal25"), 0, 4096))
 cfg = [SimConfig(gpu_count=8)]
-for name, env, flags in (("zc + prog rows /32", {"MSG_PROG_EVERY": "32"}, abi.OUT_JOBS), ("zc summaries", {}, 0),
-                         ("zc + prog /32, no decode", {"MSG_PROG_EVERY": "32", "MSG_DEBUG_SKIP_DECODE": "1"}, abi.OUT_JOBS),
-                         ("zc rows no prog, no decode", {"MSG_PIPE_PROG": "0", "MSG_DEBUG_SKIP_DECODE": "1"}, abi.OUT_JOBS),
+for name, env, flags in (("zc + prog rows", {}, abi.OUT_JOBS), ("zc summaries", {}, 0),
+                         ("zc + prog rows, backoff 0", {"MSG_POLL_BACKOFF": "0"}, abi.OUT_JOBS),
+                         ("zc + prog rows, backoff 128", {"MSG_POLL_BACKOFF": "128"}, abi.OUT_JOBS),
+                         ("zc + prog rows /64", {"MSG_PROG_EVERY": "64"}, abi.OUT_JOBS),
                          ("zc rows, no prog", {"MSG_PIPE_PROG": "0"}, abi.OUT_JOBS),
-                         ("zc + prog /32, 8 host threads", {"MSG_PROG_EVERY": "32"}, abi.OUT_JOBS),
-                         ("staged no prog", {"MSG_NO_ZC": "1", "MSG_PIPE_PROG": "0"}, abi.OUT_JOBS)):
+                         ("staged no prog", {"MSG_NO_ZC": "1", "MSG_PIPE_PROG": "0"}, abi.OUT_JOBS),
+                         ("zc + prog rows", {}, abi.OUT_JOBS)):
     os.environ.update(env)
-    for i in range(4):
+    for i in range(8):
         print(f"--- {name} call {i}", file=sys.stderr, flush=True)
         t0 = time.perf_counter()
         r = eng.run_batch(b, cfg, flags)
