@@ -110,6 +110,23 @@ struct BlockScratch {
 // misses they save: 20K-arrival C4 prefix 0.367 s vs 0.341 s inlined
 // (profiles/r02, c4_variants_r02t.log); only the exchange reduction pays
 // (r02u).  CL_OOL_* select each for A/B builds.
+#ifndef C4_DISPATCH_UNROLL
+#define C4_DISPATCH_UNROLL 1
+#endif
+constexpr int kC4DispatchUnroll = C4_DISPATCH_UNROLL;
+#ifndef C4_SCAN_UNROLL
+#define C4_SCAN_UNROLL 8
+#endif
+constexpr int kC4ScanUnroll = C4_SCAN_UNROLL;
+#ifndef C4_HELD
+#define C4_HELD 8  // active entries per thread kept in registers from the timer scan to advance_all
+#endif
+#ifndef C4_FUSED_SUMS
+#define C4_FUSED_SUMS 1
+#endif
+#ifndef C4_DROP_BARRIERS
+#define C4_DROP_BARRIERS 1
+#endif
 #ifndef CL_OOL_WORD
 #define CL_OOL_WORD MSG_DI
 #endif
@@ -298,7 +315,7 @@ struct ClusterSim {
     uint64_t spec_key;
     unsigned spec_nl, spec_nb;
     // next_event -> advance_all: this thread's first kHeld active entries
-    static constexpr int kHeld = 4;
+    static constexpr int kHeld = C4_HELD;
     double held_rem[kHeld];
     unsigned held_k[kHeld];  // running count of the entry's GPU, 0: not Running
 
@@ -334,6 +351,33 @@ struct ClusterSim {
         tie = v ? sc->tie[bph][L] : NONE;
         ms = v ? sc->ms[bph][L] : NONE;
         pay = v ? sc->pay[bph][L] : -1;
+        warp_lexmin(hi, lo, tie, ms, pay);
+        bph ^= 1;
+    }
+    // block_lexmin and two block sums in one shared-memory round (one barrier).
+    MSG_DI void block_lexmin_sums(unsigned& hi, unsigned& lo, unsigned& tie, unsigned& ms, int& pay, unsigned& c0,
+                                  unsigned& c1) {
+        warp_lexmin(hi, lo, tie, ms, pay);
+        c0 = wp::radd(c0);
+        c1 = wp::radd(c1);
+        if (L == 0) {
+            sc->hi[bph][W] = hi;
+            sc->lo[bph][W] = lo;
+            sc->tie[bph][W] = tie;
+            sc->ms[bph][W] = ms;
+            sc->pay[bph][W] = pay;
+            sc->nl[bph][W] = c0;
+            sc->nb[bph][W] = c1;
+        }
+        wp::bsync();
+        const bool v = L < w;
+        hi = v ? sc->hi[bph][L] : NONE;
+        lo = v ? sc->lo[bph][L] : NONE;
+        tie = v ? sc->tie[bph][L] : NONE;
+        ms = v ? sc->ms[bph][L] : NONE;
+        pay = v ? sc->pay[bph][L] : -1;
+        c0 = wp::radd(v ? sc->nl[bph][L] : 0u);
+        c1 = wp::radd(v ? sc->nb[bph][L] : 0u);
         warp_lexmin(hi, lo, tie, ms, pay);
         bph ^= 1;
     }
@@ -660,14 +704,19 @@ struct ClusterSim {
         // the next timer scan revisits entry i on the same thread
     }
 
+    // A deferred sample (sharded engine): its mean and the running sum are
+    // kept by one thread of the last warp only (finish reads them back), off
+    // warp 0, which runs the exchanges and the owner's serial steps.
     MSG_DI void record_sample(double t, unsigned long long ktot) {
-        tl_mean = cl_tl_mean(ktot, inv_g, G);
-        if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && T == 0 && gs == 0) {
-            tl[2 * n_tl] = t;
-            tl[2 * n_tl + 1] = tl_mean;
+        if (T == NT - 1) {
+            tl_mean = cl_tl_mean(ktot, inv_g, G);
+            if (DETAIL && (oflags & OF_TIMELINE) && n_tl < tl_cap && gs == 0) {
+                tl[2 * n_tl] = t;
+                tl[2 * n_tl + 1] = tl_mean;
+            }
+            tl_sum = wp::dadd(tl_sum, tl_mean);
         }
         ++n_tl;
-        tl_sum = wp::dadd(tl_sum, tl_mean);
     }
 
     MSG_DI void sample() {  // sim.cpp:177-181
@@ -716,7 +765,7 @@ struct ClusterSim {
         // This thread's first kHeld entries keep (remaining work, running
         // count) in registers for advance_all (nothing changes them between
         // the scan and the advance): its update needs no reload, no barrier.
-#pragma unroll 4
+#pragma unroll kC4ScanUnroll
         for (uint32_t i = T, j = 0; i < n_act; i += NT, ++j) {
             const uint8_t s = ast[i];
             double t;
@@ -863,18 +912,19 @@ struct ClusterSim {
         scan_dispatch(p, kmin, nl, nb);
         unsigned hi = (unsigned)(kmin >> 32), lo = (unsigned)kmin, z0 = 0, z1 = 0;
         int pay = 0;
+#if C4_FUSED_SUMS
+        block_lexmin_sums(hi, lo, z0, z1, pay, nl, nb);
+        NL = (cflags & CF_LB) ? nl : 0u;
+        NB = (cflags & CF_LB) ? nb : 0u;
+#else
         block_lexmin(hi, lo, z0, z1, pay);
         NL = NB = 0;
         if (cflags & CF_LB) {
-            if ((g_hi - g_lo) * 7 < 65536) {  // both counts in one reduction
-                const unsigned x = block_sum(nl | (nb << 16));
-                NL = x & 0xFFFFu;
-                NB = x >> 16;
-            } else {
-                NL = block_sum(nl);
-                NB = block_sum(nb);
-            }
+            const unsigned x = block_sum(nl | (nb << 16));
+            NL = x & 0xFFFFu;
+            NB = x >> 16;
         }
+#endif
         key = ((uint64_t)hi << 32) | lo;
     }
 
@@ -893,6 +943,7 @@ struct ClusterSim {
         // post-placement rank, the starts reaching it, the candidate count);
         // the rest take the per-start loop below.
         const uint16_t* Tp = (lb && dyn && stab) ? stab + p * 2048 : nullptr;
+#pragma unroll kC4DispatchUnroll
         for (int g = g_lo + (int)T; g < g_hi; g += (int)NT) {
             if (Tp) {
                 const unsigned wd = gw[g - g_lo];
@@ -1013,7 +1064,11 @@ struct ClusterSim {
         cr.dprof = 0;
         cr.dseq = 0;
         if (!cr.reused) ++cseq_ctr;
+        // no trailing barrier: sc->u is next written by thread 0 after the
+        // leading barrier of a later create_instance
+#if !C4_DROP_BARRIERS
         wp::bsync();
+#endif
         return cr;
     }
 
@@ -1264,9 +1319,15 @@ struct ClusterSim {
                     ++cnt;
                 }
             }
+#if C4_FUSED_SUMS
+            unsigned zc = 0;
+            block_lexmin_sums(bhi, blo, z0, z1, bi, cnt, zc);
+#else
             block_lexmin(bhi, blo, z0, z1, bi);
+            cnt = block_sum(cnt);
+#endif
             XRec x = xnone();
-            x.c[0] = block_sum(cnt);
+            x.c[0] = cnt;
             x.hi = bhi;
             x.lo = blo;
             x.tie = x.ms = 0;
@@ -1342,11 +1403,18 @@ struct ClusterSim {
     MSG_DI void handle_departure(int slot, int ia, bool completion) {
         const int g = slot >> 3;
         if (own(g)) {
-            wp::bsync();
+            wp::bsync();  // advance_all's stores before act_remove moves an entry
+#if C4_DROP_BARRIERS
+            int32_t r = -1;  // only thread 0 needs the job (records, emit)
+            if (T == 0) {
+                r = ajob[ia];
+                const int m = mig[slot];
+#else
             const int32_t r = ajob[ia];
             const int m = mig[slot];
             wp::bsync();
             if (T == 0) {
+#endif
                 st[slot] = ST_IDLE;
                 act_remove(slot, n_act);
                 if (completion) {
@@ -1424,6 +1492,9 @@ struct ClusterSim {
             max_intra = (int)x.mx;
             if (S > 1) wp::cluster_sync();  // no CTA leaves while a push to it may be in flight
             if (gs != 0) return;
+            if (T == NT - 1) sc->tl = tl_sum;  // record_sample's thread
+            wp::bsync();
+            tl_sum = sc->tl;
         }
         if (s.status != STATUS_OK) {
             unsigned mn = NONE;
