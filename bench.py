@@ -720,6 +720,7 @@ def main():
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_ms,
+                "ms_median": 1e3 * statistics.median(e2e_s), "ms_min": 1e3 * min(e2e_s), "ms_max": 1e3 * max(e2e_s),
                 "path": "msg_run_batch(page-locked host SoA traces) -> per-job rows + summaries, then the per-trace summary "
                         "gather to rank 0"},
         "gpu_launches": int(gpu_launches),

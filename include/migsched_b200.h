@@ -235,18 +235,24 @@ msg_status msg_engine_device_info(const msg_engine* engine, char* name, size_t n
 
 /* ---- engine-level entry: replaces migsched::run (sim.hpp:114, sim.cpp:504)
  * for a batch of independent traces.  Each trace is validated exactly like
- * Engine::Engine (sim.cpp:73-116) before any GPU work; a trace that fails
- * validation gets its status set and is not simulated.  JobsPending
- * (sim.cpp:464-466) is reported per trace after the simulation. ----------- */
+ * Engine::Engine (sim.cpp:73-116); a trace that fails validation gets its
+ * status and the reference's message and no results.  (With page-locked
+ * inputs the validation runs on host threads while the kernel already
+ * simulates the batch; a failing trace's device results are discarded.)
+ * JobsPending (sim.cpp:464-466) is reported per trace after the
+ * simulation. -------------------------------------------------------------- */
 msg_status msg_run_batch(msg_engine* engine, const msg_trace_batch* batch, const msg_config* cfgs,
                          uint32_t n_cfgs, uint32_t out_flags, msg_batch_result** out);
 
 /* Page-locked host memory for input batches.  When a batch's arrival_s,
  * service_s and profile arrays live in such memory (this allocator, or any
- * cudaHostAlloc / cudaHostRegister'ed range), msg_run_batch copies them to
- * the device in place, with no host-side staging copy.  Any host memory
- * works; this only removes a copy.  msg_host_alloc returns 64-byte aligned
- * memory usable from every device of the process. */
+ * cudaHostAlloc / cudaHostRegister(..., Mapped) range), msg_run_batch
+ * launches the whole batch at once and the kernel reads the inputs in place
+ * over PCIe as each trace's arrivals reach them (zero copy; no staging, the
+ * checks run under the kernel), and job rows are decoded while it runs.
+ * Any host memory works; this removes the staging and its latency.
+ * msg_host_alloc returns mapped memory usable from every device of the
+ * process.  The arrays must stay unchanged until msg_run_batch returns. */
 msg_status msg_host_alloc(size_t bytes, void** out);
 void msg_host_free(void* p);
 

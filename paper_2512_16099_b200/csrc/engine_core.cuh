@@ -140,10 +140,19 @@ struct Decision {
 // rejects such a trace and its results are discarded.  (Staging the next
 // block asynchronously with cp.async into shared memory was slower on the
 // B200: profiles/r02, e2e_zc_r02p.log.)
+// Blocks [0, kZcFirst), [kZcFirst, 32), then 32 jobs each: every trace asks
+// for its first block at the same instant, so a small first block shortens
+// that burst (4096 traces x 8 jobs x 20 B) and with it the traces' start.
+#ifndef MSG_ZC_FIRST
+#define MSG_ZC_FIRST 8
+#endif
+constexpr uint32_t kZcFirst = MSG_ZC_FIRST;
 template <class WS>
 MSG_DI void zc_fetch_block(WS* sm, double* arr, double* svc, uint8_t* prf, uint32_t j0, uint32_t N) {
-    const uint32_t j = j0 + wp::lane();
-    if (j < N) {
+    const unsigned L = wp::lane();
+    const uint32_t j = j0 + L;
+    const uint32_t len = j0 == 0 ? kZcFirst : (j0 == kZcFirst ? 32u - kZcFirst : 32u);
+    if (j < N && L < len) {
         const double t = sm->zc_a[j];
         double v = sm->zc_s[j];
         int p = sm->zc_p[j];
@@ -484,7 +493,7 @@ struct TraceSim {
     // (time, job id) order: sim.cpp:118-120 with TimerLater).
     MSG_DI void load_arrival() {
         if (a_idx < N) {
-            if (IO && (oflags & (OF_ZC | OF_PROG)) && (a_idx & 31u) == 0) {
+            if (IO && (oflags & (OF_ZC | OF_PROG)) && ((a_idx & 31u) == 0 || a_idx == kZcFirst)) {
                 if (oflags & OF_ZC)
                     zc_fetch_block(sm, const_cast<double*>(arr), const_cast<double*>(svc), const_cast<uint8_t*>(prf),
                                    a_idx, N);
@@ -642,8 +651,9 @@ struct TraceSim {
             kv[i] = 1u;
             if (kCompact && i > 0 && na <= 32u * (unsigned)i) continue;
             int slot;
+            bool valid = true;
             if (kCompact) {
-                const bool valid = L + 32u * (unsigned)i < na;
+                valid = L + 32u * (unsigned)i < na;
                 slot = valid ? (int)sm->act[L + 32 * i] : 0;
                 const uint8_t x = sm->st[slot];
                 sv[i] = valid ? x : (uint8_t)ST_EMPTY;
@@ -653,12 +663,18 @@ struct TraceSim {
             }
             slv[i] = slot;
             kv[i] = sv[i] == ST_RUN ? w_k(sm->gw[slot >> 3]) : 1u;
-            const typename WS::RT x = sm->rt[slot];
-            rv[i] = x.rem;
-            tv[i] = x.tkey;
-            const typename WS::JM y = sm->jm[slot];
-            jv[i] = (unsigned)y.job;
-            mv[i] = y.mseq;
+            // a lane past the list reads nothing of slot 0's timer (another
+            // lane may own and rewrite it below)
+            rv[i] = tv[i] = 0.0;
+            jv[i] = mv[i] = 0u;
+            if (valid) {
+                const typename WS::RT x = sm->rt[slot];
+                rv[i] = x.rem;
+                tv[i] = x.tkey;
+                const typename WS::JM y = sm->jm[slot];
+                jv[i] = (unsigned)y.job;
+                mv[i] = y.mseq;
+            }
         }
 #pragma unroll
         for (int i = 0; i < SPL; ++i) {

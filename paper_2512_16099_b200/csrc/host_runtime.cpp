@@ -243,111 +243,11 @@ const T* dev_view(const T* p) {
     return at.type == cudaMemoryTypeHost ? static_cast<const T*>(at.devicePointer) : nullptr;
 }
 
-msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
-                      uint32_t flags, msg_staged* s, bool defer_arrays = false) {
-    if (!b || (b->n_traces && (!b->offsets || !b->job_id || !b->arrival_s || !b->profile || !b->service_s)) ||
-        (n_cfgs == 0 && b->n_traces)) {
-        eng->last_error = "InvalidArgument: null batch arrays or no configs";
-        return MSG_ERR_INVALID_ARGUMENT;
-    }
-    s->eng = eng;
-    s->n_in = b->n_traces;
-    s->out_flags = flags;
-    s->status.assign(s->n_in, MSG_OK);
-    s->message.assign(s->n_in, std::string());
-    s->dev_index.assign(s->n_in, -1);
-    s->gpu_count.assign(s->n_in, 0);
-    s->src_of.clear();
-    s->traces.clear();
-    s->configs.clear();
-    s->init.clear();
-    s->overlap.clear();
-    s->handler_events = 0;
-
-    // Configs referenced by the batch.
-    std::vector<CfgState> cs(n_cfgs);
-    for (uint32_t i = 0; i < n_cfgs; ++i) cs[i] = validate_config(cfgs[i]);
-    for (uint32_t i = 0; i < n_cfgs; ++i) {
-        cs[i].dev.init_off = (uint32_t)s->init.size();
-        s->init.insert(s->init.end(), cs[i].init.begin(), cs[i].init.end());
-        s->configs.push_back(cs[i].dev);
-    }
-
+// stage_impl's second half: pinned staging (unless deferred), device
+// buffers, the H2D copies of configs / init / traces, and the ordering event.
+msg_status stage_buffers(msg_engine* eng, msg_staged* s, const msg_trace_batch* b, bool defer_arrays) {
     PhaseTimer pt;
-    // Per-trace validation (parallel), in input order.
-    std::vector<TraceCheck> checks(s->n_in);
-    for (uint32_t t = 0; t < s->n_in; ++t) {
-        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
-        if (ci >= n_cfgs) {
-            eng->last_error = "InvalidArgument: config_index out of range";
-            return MSG_ERR_INVALID_ARGUMENT;
-        }
-    }
-    // defer_arrays (the pipelined path): only config errors here; each
-    // trace is checked by run_pipelined just before its chunk is staged,
-    // and a failing one keeps its (unused) slot in the layout.
-    parallel_for(s->n_in, defer_arrays ? 4096 : 64, [&](uint32_t t) {
-        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
-        if (cs[ci].status != MSG_OK) {
-            checks[t].status = cs[ci].status;
-            checks[t].message = cs[ci].message;
-            return;
-        }
-        if (!defer_arrays) checks[t] = check_trace(b, t);
-    });
-
-    pt.mark("  validate");
-    uint64_t njobs = 0;
-    int maxG = 1;
-    s->large_idx.clear();
-    s->large_gpus = 0;
-    s->large_max_g = 0;
-    s->large_min_g = 0;
-    s->any_small = false;
-    for (uint32_t t = 0; t < s->n_in; ++t) {
-        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
-        s->gpu_count[t] = cfgs[ci].gpu_count;
-        s->status[t] = checks[t].status;
-        s->message[t] = checks[t].message;
-        if (checks[t].status != MSG_OK) continue;
-        DevTrace tr{};
-        tr.job_off = njobs;
-        tr.n_jobs = (uint32_t)(b->offsets[t + 1] - b->offsets[t]);
-        tr.cfg = ci;
-        tr.has_perm = checks[t].identity ? 0 : 1;
-        tr.large = cfgs[ci].gpu_count > (int)kMaxGpusEnsemble ? 1u : 0u;
-        if (tr.large) {
-            tr.cl_goff = s->large_gpus;
-            s->large_gpus += (uint64_t)cfgs[ci].gpu_count;
-            s->large_max_g = std::max(s->large_max_g, (uint32_t)cfgs[ci].gpu_count);
-            s->large_min_g = s->large_min_g ? std::min(s->large_min_g, (uint32_t)cfgs[ci].gpu_count)
-                                            : (uint32_t)cfgs[ci].gpu_count;
-            s->large_idx.push_back((uint32_t)s->traces.size());
-        } else {
-            s->any_small = true;
-            maxG = std::max(maxG, cfgs[ci].gpu_count);
-        }
-        s->dev_index[t] = (int32_t)s->traces.size();
-        s->src_of.push_back(t);
-        s->traces.push_back(tr);
-        s->overlap.push_back(cfgs[ci].migration_overlap_s);
-        njobs += tr.n_jobs;
-    }
-    s->n_jobs = njobs;
-    s->spl = maxG <= 4 ? 1 : maxG <= 8 ? 2 : maxG <= 16 ? 4 : 8;
-    // Output capacities.
-    uint64_t ev = 0, tl = 0;
-    for (auto& tr : s->traces) {
-        tr.ev_off = ev;
-        tr.tl_off = tl;
-        tr.ev_cap = (flags & MSG_OUT_EVENTS) ? s->ev_per_job * tr.n_jobs + 256 : 0;
-        tr.tl_cap = (flags & MSG_OUT_TIMELINE) ? s->tl_per_job * tr.n_jobs + 64 : 0;
-        ev += tr.ev_cap;
-        tl += tr.tl_cap;
-    }
-    s->ev_total = ev;
-    s->tl_total = tl;
-
+    const uint64_t njobs = s->n_jobs;
     // Host staging into pinned buffers, rank (job-id) order.
     const size_t N = std::max<uint64_t>(njobs, 1);
     CK(s->h_arrival.ensure(N * sizeof(double)));
@@ -427,6 +327,149 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         CK(cudaStreamSynchronize(st));
     }
     return MSG_OK;
+}
+
+msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_config* cfgs, uint32_t n_cfgs,
+                      uint32_t flags, msg_staged* s, bool defer_arrays = false) {
+    if (!b || (b->n_traces && (!b->offsets || !b->job_id || !b->arrival_s || !b->profile || !b->service_s)) ||
+        (n_cfgs == 0 && b->n_traces)) {
+        eng->last_error = "InvalidArgument: null batch arrays or no configs";
+        return MSG_ERR_INVALID_ARGUMENT;
+    }
+    s->eng = eng;
+    // messages: clear only the previous call's (failing traces), keep the
+    // vector (no per-call construction of n empty strings)
+    for (size_t t = 0; t < s->status.size() && t < s->message.size(); ++t)
+        if (s->status[t] != MSG_OK) s->message[t].clear();
+    s->n_in = b->n_traces;
+    s->out_flags = flags;
+    s->status.assign(s->n_in, MSG_OK);
+    s->message.resize(s->n_in);
+    s->dev_index.assign(s->n_in, -1);
+    s->gpu_count.assign(s->n_in, 0);
+    s->src_of.clear();
+    s->traces.clear();
+    s->configs.clear();
+    s->init.clear();
+    s->overlap.clear();
+    s->handler_events = 0;
+
+    // Configs referenced by the batch.
+    std::vector<CfgState> cs(n_cfgs);
+    for (uint32_t i = 0; i < n_cfgs; ++i) cs[i] = validate_config(cfgs[i]);
+    for (uint32_t i = 0; i < n_cfgs; ++i) {
+        cs[i].dev.init_off = (uint32_t)s->init.size();
+        s->init.insert(s->init.end(), cs[i].init.begin(), cs[i].init.end());
+        s->configs.push_back(cs[i].dev);
+    }
+
+    PhaseTimer pt;
+    // Fast layout for the pipelined path (checks deferred) with one valid
+    // small-cluster config and no event log / timeline: every trace on the
+    // device in input order, so the layout is the batch's own offsets and is
+    // filled in parallel.
+    if (defer_arrays && n_cfgs == 1 && cs[0].status == MSG_OK && cfgs[0].gpu_count <= (int)kMaxGpusEnsemble &&
+        !(flags & (MSG_OUT_EVENTS | MSG_OUT_TIMELINE))) {
+        const uint32_t n = s->n_in;
+        const uint64_t j0 = n ? b->offsets[0] : 0;
+        s->traces.resize(n);
+        s->src_of.resize(n);
+        s->overlap.assign(n, cfgs[0].migration_overlap_s);
+        std::fill(s->gpu_count.begin(), s->gpu_count.end(), cfgs[0].gpu_count);
+        parallel_for(n, 512, [&](uint32_t t) {
+            DevTrace tr{};
+            tr.job_off = b->offsets[t] - j0;
+            tr.n_jobs = (uint32_t)(b->offsets[t + 1] - b->offsets[t]);
+            s->traces[t] = tr;  // cfg 0, identity order until the checks say otherwise
+            s->src_of[t] = t;
+            s->dev_index[t] = (int32_t)t;
+        });
+        s->large_idx.clear();
+        s->large_gpus = 0;
+        s->large_max_g = s->large_min_g = 0;
+        s->any_small = n > 0;
+        s->n_jobs = n ? b->offsets[n] - j0 : 0;
+        const int maxG = cfgs[0].gpu_count;
+        s->spl = maxG <= 4 ? 1 : maxG <= 8 ? 2 : maxG <= 16 ? 4 : 8;
+        s->ev_total = s->tl_total = 0;
+        s->any_perm = true;  // deferred checks: identity order is not known yet
+        pt.mark("  layout (parallel)");
+        return stage_buffers(eng, s, b, true);
+    }
+    // Per-trace validation (parallel), in input order.
+    std::vector<TraceCheck> checks(s->n_in);
+    for (uint32_t t = 0; t < s->n_in; ++t) {
+        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
+        if (ci >= n_cfgs) {
+            eng->last_error = "InvalidArgument: config_index out of range";
+            return MSG_ERR_INVALID_ARGUMENT;
+        }
+    }
+    // defer_arrays (the pipelined path): only config errors here; each
+    // trace is checked by run_pipelined just before its chunk is staged,
+    // and a failing one keeps its (unused) slot in the layout.
+    parallel_for(s->n_in, defer_arrays ? 4096 : 64, [&](uint32_t t) {
+        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
+        if (cs[ci].status != MSG_OK) {
+            checks[t].status = cs[ci].status;
+            checks[t].message = cs[ci].message;
+            return;
+        }
+        if (!defer_arrays) checks[t] = check_trace(b, t);
+    });
+
+    pt.mark("  validate");
+    uint64_t njobs = 0;
+    int maxG = 1;
+    s->large_idx.clear();
+    s->large_gpus = 0;
+    s->large_max_g = 0;
+    s->large_min_g = 0;
+    s->any_small = false;
+    for (uint32_t t = 0; t < s->n_in; ++t) {
+        const uint32_t ci = b->config_index ? b->config_index[t] : 0;
+        s->gpu_count[t] = cfgs[ci].gpu_count;
+        s->status[t] = checks[t].status;
+        s->message[t] = checks[t].message;
+        if (checks[t].status != MSG_OK) continue;
+        DevTrace tr{};
+        tr.job_off = njobs;
+        tr.n_jobs = (uint32_t)(b->offsets[t + 1] - b->offsets[t]);
+        tr.cfg = ci;
+        tr.has_perm = checks[t].identity ? 0 : 1;
+        tr.large = cfgs[ci].gpu_count > (int)kMaxGpusEnsemble ? 1u : 0u;
+        if (tr.large) {
+            tr.cl_goff = s->large_gpus;
+            s->large_gpus += (uint64_t)cfgs[ci].gpu_count;
+            s->large_max_g = std::max(s->large_max_g, (uint32_t)cfgs[ci].gpu_count);
+            s->large_min_g = s->large_min_g ? std::min(s->large_min_g, (uint32_t)cfgs[ci].gpu_count)
+                                            : (uint32_t)cfgs[ci].gpu_count;
+            s->large_idx.push_back((uint32_t)s->traces.size());
+        } else {
+            s->any_small = true;
+            maxG = std::max(maxG, cfgs[ci].gpu_count);
+        }
+        s->dev_index[t] = (int32_t)s->traces.size();
+        s->src_of.push_back(t);
+        s->traces.push_back(tr);
+        s->overlap.push_back(cfgs[ci].migration_overlap_s);
+        njobs += tr.n_jobs;
+    }
+    s->n_jobs = njobs;
+    s->spl = maxG <= 4 ? 1 : maxG <= 8 ? 2 : maxG <= 16 ? 4 : 8;
+    // Output capacities.
+    uint64_t ev = 0, tl = 0;
+    for (auto& tr : s->traces) {
+        tr.ev_off = ev;
+        tr.tl_off = tl;
+        tr.ev_cap = (flags & MSG_OUT_EVENTS) ? s->ev_per_job * tr.n_jobs + 256 : 0;
+        tr.tl_cap = (flags & MSG_OUT_TIMELINE) ? s->tl_per_job * tr.n_jobs + 64 : 0;
+        ev += tr.ev_cap;
+        tl += tr.tl_cap;
+    }
+    s->ev_total = ev;
+    s->tl_total = tl;
+    return stage_buffers(eng, s, b, defer_arrays);
 }
 
 // CTAs per large trace (cluster_core.cuh): >= 1024 GPUs per shard, up to

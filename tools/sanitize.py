@@ -7,7 +7,8 @@ seconds.  Usage (GPU box):
 Cases:
   sim       sim_kernel: C1/C5-shaped batches (8 GPUs, events + timeline), the
             pipelined msg_run_batch (>= 512 traces, mapped-host completion
-            flags polled by host threads), ties at 32 GPUs
+            flags polled by host threads), the zero-copy IO kernel on
+            page-locked inputs (progressive rows), ties at 32 GPUs
   score     score_tma_kernel + merge + score_busy_kernel (bulk-async ring,
             mbarriers), thresholds 0.0 / 0.4 / 1.0
   snapshot  snapshot kernels: schedule / first fit / try_dequeue / planners
@@ -48,6 +49,13 @@ def case_sim(eng):
     sp.job_count = 40
     r = eng.run_batch(generate_batch(sp, 0, 600), [SimConfig(gpu_count=8)], abi.OUT_JOBS)  # pipelined
     assert all(x.ok for x in r)
+    from paper_2512_16099_b200.engine import pin_batch
+
+    # page-locked inputs: the zero-copy IO kernel (inputs read over PCIe,
+    # progressive SoA job rows + prefix words in mapped host memory)
+    pb = pin_batch(generate_batch(sp, 0, 600))
+    rz = eng.run_batch(pb, [SimConfig(gpu_count=8)], abi.OUT_JOBS)
+    assert all(x.ok for x in rz) and rz.jobs.tobytes() == r.jobs.tobytes()
     print("sim ok")
 
 
