@@ -748,6 +748,7 @@ def main():
             ws.launch()
         eng.sync()
         wms = device_steps(ws, args.steps)
+        ws.collect()  # handler_events is counted from the collected summaries
         wev = allreduce(float(ws.handler_events), "sum")
         line["weak"] = {"value": wev / (wms * 1e-3), "unit": UNIT, "ms_per_step": wms,
                         "traces_per_gpu": args.traces, "scaling": "weak"}
