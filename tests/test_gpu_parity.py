@@ -292,3 +292,36 @@ def test_report_files_from_gpu_results_match_reference(engine):
         for r, g in zip(ref, gpu):
             for kind, want in zip(kinds, r.texts):
                 assert g.text(kind, cfg) == want, kind
+
+def test_zero_copy_ragged_traces(engine, monkeypatch):
+    """Zero copy over page-locked inputs with trace lengths around the fetch
+    blocks (the first block holds 8 jobs, then 24, then 32 each) and 512+
+    traces (pipelined): the same bytes as the staged path and as the plain
+    stage / launch / collect path, and the reference's results."""
+    from paper_2512_16099_b200.engine import generate_batch, pin_batch
+
+    lens = [1, 7, 8, 9, 31, 32, 33, 40, 63, 64, 65, 200, 1000, 3000]
+    traces = []
+    for t in range(520):
+        n = lens[t % len(lens)]
+        sp = preset("normal25")
+        sp.job_count = n
+        b1 = generate_batch(sp, 1000 + t, 1)
+        traces.append([Job(int(b1.job_id[i]), float(b1.arrival_s[i]), int(b1.profile[i]), float(b1.service_s[i]))
+                       for i in range(n)])
+    b = TraceBatch.from_traces(traces)
+    cfg = [SimConfig(gpu_count=8)]
+    zc = engine.run_batch(pin_batch(b), cfg, abi.OUT_JOBS)
+    monkeypatch.setenv("MSG_NO_ZC", "1")
+    staged = engine.run_batch(pin_batch(b), cfg, abi.OUT_JOBS)
+    monkeypatch.delenv("MSG_NO_ZC")
+    monkeypatch.setenv("MSG_NO_PIPELINE", "1")
+    plain = engine.run_batch(b, cfg, abi.OUT_JOBS)
+    monkeypatch.delenv("MSG_NO_PIPELINE")
+    for other in (staged, plain):
+        assert zc.summaries.tobytes() == other.summaries.tobytes()
+        assert zc.jobs.tobytes() == other.jobs.tobytes()
+    ref = rb.ref_run_batch_results(TraceBatch.from_traces(traces[:len(lens)]), cfg)
+    for t, r in enumerate(ref):
+        r.events = r.frag_timeline = None
+        assert not diff_results(r, zc[t]), (t, lens[t])
