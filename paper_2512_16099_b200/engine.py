@@ -269,14 +269,30 @@ class BatchResult:
         self._h = handle
         self.flags = flags
         self.n = int(L.msg_result_n_traces(handle))
-        cnt = C.c_uint64()
         self.summaries = _view(L.msg_result_summaries(handle), self.n, abi.SUMMARY_DTYPE, self._owner)
-        offp = C.POINTER(C.c_uint64)()
-        jp = L.msg_result_all_jobs(handle, C.byref(offp), C.byref(cnt))
-        self.jobs = self.job_offsets = None
-        if jp:
-            self.jobs = _view(jp, cnt.value, abi.JOB_DTYPE, self._owner)
-            self.job_offsets = np.ctypeslib.as_array(offp, shape=(self.n + 1,)).copy()
+        self._jobs = None  # (jobs view, job_offsets), built on first use
+
+    def _job_views(self):
+        if self._jobs is None:
+            cnt = C.c_uint64()
+            offp = C.POINTER(C.c_uint64)()
+            jp = lib().msg_result_all_jobs(self._h, C.byref(offp), C.byref(cnt))
+            if jp:
+                self._jobs = (_view(jp, cnt.value, abi.JOB_DTYPE, self._owner),
+                              np.ctypeslib.as_array(offp, shape=(self.n + 1,)).copy())
+            else:
+                self._jobs = (None, None)
+        return self._jobs
+
+    @property
+    def jobs(self):
+        """Every valid trace's job rows (JOB_DTYPE), trace-major; None without OUT_JOBS."""
+        return self._job_views()[0]
+
+    @property
+    def job_offsets(self):
+        """Row offsets per trace (n + 1), or None without OUT_JOBS."""
+        return self._job_views()[1]
 
     def __len__(self):
         return self.n
