@@ -1223,6 +1223,8 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 // (default 8192) — pinned and device buffers plus a pre-faulted row buffer —
 // so that the first msg_run_batch of up to that size pays no lazy kernel
 // load, stream creation, allocation or first-touch page fault.
+msg_status reserve_workspace(msg_engine* eng, msg_staged* s, uint64_t J, uint64_t T);
+
 msg_status warm_engine(msg_engine* eng) {
     PhaseTimer pt;
     for (int k = 0; k < kMaxPipeChunks; ++k) {
@@ -1238,7 +1240,19 @@ msg_status warm_engine(msg_engine* eng) {
     const uint64_t T = std::max<uint64_t>(env_u64("MSG_RESERVE_TRACES", 8192), 1);
     if (!J) return MSG_OK;
     eng->cached = new msg_staged();
-    msg_staged* s = eng->cached;
+    // Best effort: a reservation that does not fit (pinned or device memory)
+    // only costs the first call its allocations.
+    const msg_status rs = reserve_workspace(eng, eng->cached, J, T);
+    if (rs != MSG_OK) {
+        cudaGetLastError();
+        eng->last_error.clear();
+    }
+    pt.mark("warm: workspace");
+    return MSG_OK;
+}
+
+msg_status reserve_workspace(msg_engine* eng, msg_staged* s, uint64_t J, uint64_t T) {
+    PhaseTimer pt;
     // the sizes stage_impl / run_pipelined ask for at J jobs and T traces
     CK(s->h_arrival.ensure(J * sizeof(double)));
     CK(s->h_service.ensure(J * sizeof(double)));
@@ -1265,7 +1279,7 @@ msg_status warm_engine(msg_engine* eng) {
     pt.mark("warm: device buffers");
     RowBuf rows = take_rows(J);
     msg_job_row* r = rows.p.get();
-    const uint64_t per_page = 4096 / sizeof(msg_job_row) + 1;
+    const uint64_t per_page = 4096 / sizeof(msg_job_row);  // a row in every 4 KiB page
     parallel_for((uint32_t)((J + 8191) / 8192), 1, [&](uint32_t i) {  // first touch, in parallel
         const uint64_t hi = std::min<uint64_t>(J, (uint64_t)(i + 1) * 8192);
         for (uint64_t j = (uint64_t)i * 8192; j < hi; j += per_page) r[j].id = 0;
