@@ -8,6 +8,9 @@ from paper_2512_16099_b200 import abi  # noqa: E402
 from paper_2512_16099_b200.engine import Engine, generate_batch, pin_batch  # noqa: E402
 from paper_2512_16099_b200.model import SimConfig, preset  # noqa: E402
 
+if os.environ.get("WITH_TORCH"):  # as bench.py: torch's CUDA context first
+    import torch
+    torch.cuda.set_device(0)
 eng = Engine(0)
 b = pin_batch(generate_batch(preset("normal25"), 0, 4096))
 cfg = [SimConfig(gpu_count=8)]
