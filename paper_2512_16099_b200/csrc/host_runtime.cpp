@@ -1048,7 +1048,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         while (k + 1 < n_chunks && d >= d0s[k + 1]) ++k;
         for (uint32_t spins = 1;; ++spins) {
             if (hdone[d] == s->done_epoch) break;
-            for (int k = 1; k < kPollBackoff / 8; ++k) _mm_pause();
+            for (int i = 1; i < kPollBackoff / 8; ++i) _mm_pause();
             if ((spins & 4095u) == 0) {
                 const cudaError_t q = cudaEventQuery(eng->pevent[k]);
                 if (q != cudaErrorNotReady && hdone[d] != s->done_epoch) {
@@ -1067,12 +1067,10 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         return kc;
     };
     // Rows [from, to) of device trace d into the result.
-    const bool skip_decode = std::getenv("MSG_DEBUG_SKIP_DECODE") != nullptr;  // timing experiments only: no rows
     // the IO kernel (zero copy or progressive rows) leaves SoA columns
     const bool io_soa = want_jobs && !jobs_d2h && (zc_p || prog);
     const double* hjd = s->h_jobs.as<double>();
     auto rows_range = [&](uint32_t d, uint32_t from, uint32_t to) {
-        if (skip_decode) return;
         const uint32_t t = s->src_of[d];
         const DevTrace& tr = s->traces[d];
         const int64_t* ids = (tr.has_perm ? hid + tr.job_off : b->job_id + b->offsets[t]) + from;
@@ -1153,11 +1151,11 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
                 // back off (~2 us) after a sweep without news: the flags and
                 // prefixes share cache lines with the kernel's ongoing
                 // PCIe writes, and tight polling slows those writes down
-                for (int k = 0; k < kPollBackoff; ++k) _mm_pause();
+                for (int i = 0; i < kPollBackoff; ++i) _mm_pause();
                 if ((++idle & 4095u) == 0) {  // every kernel ended and a trace never published: failure
                     bool all = true;
-                    for (int k = 0; k < n_chunks && all; ++k)
-                        all = d0s[k] == d0s[k + 1] || cudaEventQuery(eng->pevent[k]) != cudaErrorNotReady;
+                    for (int c = 0; c < n_chunks && all; ++c)
+                        all = d0s[c] == d0s[c + 1] || cudaEventQuery(eng->pevent[c]) != cudaErrorNotReady;
                     if (all && hdone[open[0]] != s->done_epoch) {
                         lost = true;
                         return;
