@@ -47,14 +47,14 @@
 namespace msgk {
 
 #ifndef MSG_SCORE_THREADS
-#define MSG_SCORE_THREADS 256
+#define MSG_SCORE_THREADS 512  // 2 blocks x 16 warps per SM: room for the key-form table (48 KiB) + a 64 KiB ring
 #endif
 constexpr int kScoreThreads = MSG_SCORE_THREADS;
 #ifndef MSG_SCORE_WPT
 #define MSG_SCORE_WPT 8
 #endif
 #ifndef MSG_SCORE_MINB
-#define MSG_SCORE_MINB 4
+#define MSG_SCORE_MINB 2
 #endif
 #ifndef MSG_SCORE_ITEM
 #define MSG_SCORE_ITEM 4
@@ -251,6 +251,78 @@ __device__ __forceinline__ bool score_word_fast(const uint16_t* T, uint64_t w, u
     acc.best = min(acc.best, key);
     acc.cnt += (e & 7u) << ((~e >> 11) & 16u);  // Lazy (pass 0) candidates in the high half
     return plain;
+}
+
+// The per-word table in key form (MSG_SCORE_T32, the TMA kernel's default
+// path): one 32-bit entry per (profile, popc busy_c, busy_m), built per block
+// from the 16-bit table and the launch's threshold.  Bits: 31 pass (Busy),
+// 30..26 cost rank, 25 !reused, 2..0 the first minimum-rank start — i.e. the
+// key of a word without an idle-exact instance, less its index; 21..15 the
+// minimum-rank starts (reuse check); 14..9 / 8..3 the candidate count when
+// the row is Busy / Lazy (summed per chunk in these fields).  A word then
+// costs one LOP3 for its key and one AND + ADD for its counts.
+constexpr int kScoreTab32Bytes = kScoreTabEntries * 4;
+constexpr unsigned kNoCand32 = 0xFE000007u;  // key >= kNoCandKey, no counts, no starts
+
+__device__ __forceinline__ void fast_tab32_init(uint32_t* t, const uint16_t* g, unsigned lazymask) {
+    for (unsigned i = threadIdx.x; i < (unsigned)kScoreTabEntries; i += blockDim.x) {
+        const unsigned e = __ldg(g + i);
+        const unsigned p = i >> 11, pc = (i >> 8) & 7u;
+        const unsigned cnt = e & 7u, mm = (e >> 3) & 0x7Fu, rank = (e >> 10) & 0x1Fu;
+        const unsigned busy = ((lazymask >> pc) & 1u) ^ 1u;
+        const unsigned stride = (kStridePack >> (4 * p)) & 0xFu;
+        unsigned v = kNoCand32;
+        if (cnt) {
+            const unsigned j0 = (unsigned)__ffs(mm) - 1u;
+            v = (busy << 31) | (rank << 26) | (1u << 25) | (mm << 15) | (cnt << (busy ? 9 : 3)) | (j0 * stride);
+        }
+        t[i] = v;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ bool score_word_fast32(const uint32_t* T, uint64_t w, unsigned lk3, ItemAcc& acc,
+                                                  unsigned& cnt) {
+    using Q = Prof<P>;
+    const unsigned lo = (unsigned)w;
+    const unsigned pc = (unsigned)__popc(lo & 0x7Fu);
+    const unsigned bm = (lo >> 8) & 0xFFu;
+    const bool plain = ((lo ^ (lo >> 8)) & 0xFF00u) == 0;  // blocked memory == busy memory: no draining
+    unsigned e = T[pc * 256u + bm];
+    e = plain ? e : kNoCand32;
+    unsigned key = (e & 0xFE000007u) | lk3;
+    // minimum-rank starts with an idle-exact instance: reuse it (cleared
+    // !reused bit, its lowest start; scheduler.cpp:62-66)
+    const unsigned r = (e >> 15) & (unsigned)(w >> (24 + Q::pbase)) & 0x7Fu;
+    if (r) key = (key & ~0x02000007u) | (((unsigned)__ffs(r) - 1u) * Q::stride);
+    acc.best = min(acc.best, key);
+    cnt += e & 0x7FF8u;
+    return plain;
+}
+
+template <int P, int NW2>
+__device__ __forceinline__ void score_words_fast32(const uint32_t* T, const DevTables* tb, const ulonglong2 (&x)[NW2],
+                                                   unsigned l0, unsigned lazymask, ItemAcc& acc) {
+    unsigned slow = 0, cnt = 0;
+#pragma unroll
+    for (int k = 0; k < NW2; ++k) {
+        const unsigned l3 = (l0 + (unsigned)k * 2 * kScoreThreads) << 3;
+        slow |= (score_word_fast32<P>(T, x[k].x, l3, acc, cnt) ? 0u : 1u) << (2 * k);
+        slow |= (score_word_fast32<P>(T, x[k].y, l3 + 8u, acc, cnt) ? 0u : 1u) << (2 * k + 1);
+    }
+    acc.cnt += (((cnt >> 3) & 63u) << 16) + ((cnt >> 9) & 63u);  // Lazy in the high half
+    if (__builtin_expect(__any_sync(0xffffffffu, slow != 0), 0)) {
+#pragma unroll
+        for (int k = 0; k < 2 * NW2; ++k) {  // static indices: the words stay in registers
+            if ((slow >> k) & 1u) {
+                const uint64_t w = (k & 1) ? x[k >> 1].y : x[k >> 1].x;
+                const uint2 g = score_word_generic<P>(tb, w, l0 + (unsigned)(k >> 1) * 2 * kScoreThreads + (k & 1),
+                                                      lazymask);
+                acc.best = min(acc.best, g.x);
+                acc.cnt += g.y;
+            }
+        }
+    }
 }
 
 // The thread's words of one chunk (x[k].x at local index l_k, x[k].y at
@@ -486,11 +558,18 @@ struct StageMeta {
 struct TmaSmem {
     const ScoreSmem* t;       // static: the per-start scoring tables (generic variants)
     const uint16_t* ft;       // static: the per-word table (load balancing + dynamic partitioning)
+    const uint32_t* ft32;     // dynamic: the same in key form (MSG_SCORE_T32)
     uint64_t (*buf)[kChunk];  // [kStages][kChunk]
     uint64_t* full;           // [kStages]
     StageMeta* meta;          // [kStages]
 };
 constexpr size_t kTmaDynBytes = sizeof(uint64_t) * kChunk * kStages + 8 * kStages + sizeof(StageMeta) * kStages;
+#ifndef MSG_SCORE_T32
+#define MSG_SCORE_T32 1
+#endif
+// the default-path kernel (load balancing + dynamic partitioning) keeps the
+// key-form table in front of its ring
+constexpr size_t kTmaDynBytesFast = kTmaDynBytes + (MSG_SCORE_T32 ? (size_t)kScoreTab32Bytes : 0);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
@@ -603,7 +682,11 @@ __device__ __forceinline__ void consume_fast(const ScoreArgs& a, const TmaSmem& 
     ulonglong2 x[kWordsPerThread / 2];
 #pragma unroll
     for (int k = 0; k < kWordsPerThread / 2; ++k) x[k] = v[threadIdx.x + (unsigned)k * kScoreThreads];
+#if MSG_SCORE_T32
+    score_words_fast32<P>(sm.ft32 + P * 2048, a.tables, x, m.base + threadIdx.x * 2u, a.lazymask, acc);
+#else
     score_words_fast<P>(sm.ft + P * 2048, a.tables, x, m.base + threadIdx.x * 2u, a.lazymask, acc);
+#endif
     if (m.last) {
         stash_item<true>(acc, wpart);
         acc = ItemAcc{0xFFFFFFFFu, 0u, 0u};
@@ -613,15 +696,21 @@ __device__ __forceinline__ void consume_fast(const ScoreArgs& a, const TmaSmem& 
 template <bool LB, bool DYN>
 __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kernel(ScoreArgs a) {
     constexpr bool kFast = LB && DYN;
-    __shared__ __align__(16) std::conditional_t<kFast, FastTab, ScoreSmem> tabs;
+    constexpr bool kT32 = kFast && MSG_SCORE_T32;
+    __shared__ __align__(16) std::conditional_t<kT32, NoTab, std::conditional_t<kFast, FastTab, ScoreSmem>> tabs;
     __shared__ WarpPart wpart[2][kScoreThreads / 32];  // item ends, by stage parity
-    extern __shared__ __align__(128) unsigned char ring[];
-    TmaSmem sm{nullptr, nullptr, reinterpret_cast<uint64_t(*)[kChunk]>(ring),
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    unsigned char* ring = dyn_smem + (kT32 ? kScoreTab32Bytes : 0);
+    TmaSmem sm{nullptr, nullptr, nullptr, reinterpret_cast<uint64_t(*)[kChunk]>(ring),
                reinterpret_cast<uint64_t*>(ring + sizeof(uint64_t) * kChunk * kStages),
                reinterpret_cast<StageMeta*>(ring + sizeof(uint64_t) * kChunk * kStages + 8 * kStages)};
     // the merge kernel may launch now: it waits for this grid (griddepcontrol.wait)
     asm volatile("griddepcontrol.launch_dependents;");
-    if constexpr (kFast) {
+    if constexpr (kT32) {
+        uint32_t* t32 = reinterpret_cast<uint32_t*>(dyn_smem);
+        fast_tab32_init(t32, a.stab, a.lazymask);
+        sm.ft32 = t32;
+    } else if constexpr (kFast) {
         fast_tab_init(tabs, a.stab, a.lazymask);
         sm.ft = tabs.t;
     } else {
@@ -730,7 +819,8 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         cudaFuncSetAttribute(score_tma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         cudaFuncSetAttribute(score_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         cudaFuncSetAttribute(score_tma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-        cudaFuncSetAttribute(score_tma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(score_tma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kTmaDynBytesFast);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], score_kernel<false, false>, kScoreThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], score_kernel<false, true>, kScoreThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], score_kernel<true, false>, kScoreThreads, 0);
@@ -738,7 +828,8 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[4], score_tma_kernel<false, false>, kScoreThreads, dyn);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[5], score_tma_kernel<false, true>, kScoreThreads, dyn);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[6], score_tma_kernel<true, false>, kScoreThreads, dyn);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[7], score_tma_kernel<true, true>, kScoreThreads, dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[7], score_tma_kernel<true, true>, kScoreThreads,
+                                                      kTmaDynBytesFast);
     }
     const uint64_t chunks_per = (a.G + kChunk - 1) / kChunk;
     const uint64_t items = ((chunks_per + kItemChunks - 1) / kItemChunks) * a.n;
@@ -759,7 +850,7 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         case 4: score_tma_kernel<false, false><<<grid, block, kTmaDynBytes, stream>>>(a); break;
         case 5: score_tma_kernel<false, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
         case 6: score_tma_kernel<true, false><<<grid, block, kTmaDynBytes, stream>>>(a); break;
-        default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytes, stream>>>(a); break;
+        default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytesFast, stream>>>(a); break;
     }
     if (!tma) return cudaGetLastError();
     // The merge launches as a programmatic dependent: its launch overlaps
