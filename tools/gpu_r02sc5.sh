@@ -1,4 +1,4 @@
-D=gpurun_out/r02sc5; mkdir -p $D
+D=gpurun_out/${TAG:-r02sc5}; mkdir -p $D
 timeout 600 python tools/score_variant_bench.py > $D/score_variants.log 2>&1; echo "sv rc=$?" >> $D/rc.txt
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $D/tests.log 2>&1; echo "tests rc=$?" >> $D/rc.txt
 for tool in memcheck racecheck synccheck initcheck; do timeout 600 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 python tools/sanitize.py score > $D/${tool}_score.log 2>&1; echo "$tool score rc=$?" >> $D/rc.txt; done
