@@ -44,3 +44,37 @@ def test_emulated_kernel_vs_port_randomized():
         want = rb.port_run_batch_results(b, [cfg])[0]
         got = emu_run_batch_results(b, [cfg])[0]
         assert diff_results(want, got) == "", (G, feats, cfg)
+
+
+@pytest.mark.parametrize("name", sorted(golden_runs().keys()))
+def test_emulated_io_kernel_matches_golden(name, monkeypatch):
+    """The pipelined msg_run_batch's IO instantiation of the event loop
+    (zero-copy input blocks read from the caller's arrays, job records
+    published progressively into SoA host columns, completion flag) in the
+    warp emulation: the same summary and job rows as the reference, and the
+    host columns equal to the device records (checked inside the harness)."""
+    batch, cfg, ref, _ = golden_runs()[name]
+    if cfg.gpu_count > 32:
+        pytest.skip("the IO kernel is the warp engine's (G <= 32)")
+    monkeypatch.setenv("MSG_EMU_IO", "1")
+    got = emu_run_batch_results(batch, [cfg])[0]
+    ref.events = ref.frag_timeline = None  # summary + rows only in the IO kernel
+    got.events = got.frag_timeline = None
+    assert diff_results(ref, got) == ""
+
+
+@pytest.mark.skipif(not rb.port_available(), reason="oracle port not built")
+def test_emulated_io_kernel_long_traces(monkeypatch):
+    """Traces long enough for several zero-copy blocks and row flushes."""
+    from paper_2512_16099_b200.engine import generate
+
+    monkeypatch.setenv("MSG_EMU_IO", "1")
+    for n, G, seed in ((7, 8, 1), (33, 4, 2), (150, 8, 3), (400, 16, 4)):
+        sp = WorkloadSpec(mean_interarrival_s=3.0, job_count=n, seed=seed)
+        cfg = SimConfig(gpu_count=G, migration_overlap_s=1.0)
+        b = TraceBatch.from_traces([generate(sp)])
+        want = rb.port_run_batch_results(b, [cfg])[0]
+        got = emu_run_batch_results(b, [cfg])[0]
+        want.events = want.frag_timeline = None
+        got.events = got.frag_timeline = None
+        assert diff_results(want, got) == "", (n, G)
