@@ -1275,14 +1275,18 @@ msg_status reserve_workspace(msg_engine* eng, msg_staged* s, uint64_t J, uint64_
     CK(s->d_traces.ensure(T * sizeof(DevTrace)));
     CK(s->d_summary.ensure(T * sizeof(DevSummary)));
     pt.mark("warm: device buffers");
-    RowBuf rows = take_rows(J);
-    msg_job_row* r = rows.p.get();
-    const uint64_t per_page = 4096 / sizeof(msg_job_row);  // a row in every 4 KiB page
-    parallel_for((uint32_t)((J + 8191) / 8192), 1, [&](uint32_t i) {  // first touch, in parallel
-        const uint64_t hi = std::min<uint64_t>(J, (uint64_t)(i + 1) * 8192);
-        for (uint64_t j = (uint64_t)i * 8192; j < hi; j += per_page) r[j].id = 0;
-    });
-    give_rows(std::move(rows));
+    // two row buffers: a caller that keeps the previous result while it
+    // makes the next call needs both in rotation
+    RowBuf rows[2] = {take_rows(J), take_rows(J)};
+    for (RowBuf& rb : rows) {
+        msg_job_row* r = rb.p.get();
+        const uint64_t per_page = 4096 / sizeof(msg_job_row);  // a row in every 4 KiB page
+        parallel_for((uint32_t)((J + 8191) / 8192), 1, [&](uint32_t i) {  // first touch, in parallel
+            const uint64_t hi = std::min<uint64_t>(J, (uint64_t)(i + 1) * 8192);
+            for (uint64_t j = (uint64_t)i * 8192; j < hi; j += per_page) r[j].id = 0;
+        });
+    }
+    for (RowBuf& rb : rows) give_rows(std::move(rb));
     pt.mark("warm: row buffer");
     return MSG_OK;
 }
