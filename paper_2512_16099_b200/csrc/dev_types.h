@@ -181,7 +181,7 @@ struct SimArgs {
     // optional (with jobs_host and done_host): progressive row publication.
     // prog_host[t] = done_epoch << 32 | n once the records of the trace's
     // first n jobs (all completed) are in jobs_host; the warp flushes the
-    // completed prefix every 32 arrivals, so the host decodes rows while the
+    // completed prefix every 64 arrivals (prog_mask), so the host decodes rows while the
     // trace still runs.
     uint64_t* prog_host;
     uint32_t prog_mask;  // flush when the arrival index is a multiple of prog_mask + 1 (a power of two >= 32)

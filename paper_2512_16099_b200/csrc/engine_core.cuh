@@ -191,6 +191,9 @@ MSG_DI void rows_flush_block(WS* sm, const JobOut* jobs, uint32_t N) {
     }
     if (q - p < 32u) return;  // amortise the system-scope fence
     for (uint32_t j = p + L; j < q; j += 32) store_row_host(sm, j, jobs[j]);
+    // The system-scope fence is this path's cost (~0.1 ms of the C2 IO
+    // kernel; a lane-0 release store compiles to the same MEMBAR): hence a
+    // flush every 64 arrivals (SimArgs::prog_mask), not every block.
     wp::gfence_sys();
     wp::sync();
     if (L == 0) {

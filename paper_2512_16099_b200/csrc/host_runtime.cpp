@@ -879,7 +879,7 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     }
     volatile uint64_t* hprog = prog ? s->h_prog.as<uint64_t>() : nullptr;
     // flush cadence in arrivals (MSG_PROG_EVERY, a power of two >= 32; tuning)
-    uint32_t prog_mask = 31;
+    uint32_t prog_mask = 63;  // r02 sweep (tools/zc_kernel_variants.py): 32 / 64 / 128 / 256 -> 1.71 / 1.60 / 1.71 / 1.69 ms
     if (const char* e = std::getenv("MSG_PROG_EVERY")) {
         const unsigned long v = std::strtoul(e, nullptr, 10);
         if (v >= 32 && (v & (v - 1)) == 0) prog_mask = (uint32_t)v - 1;
