@@ -14,7 +14,8 @@ for flags in (abi.OUT_JOBS, 0, abi.OUT_JOBS, 0):
     for i in range(6):
         r = eng.run_batch(b, cfg, flags); del r
 '''
-runs = [(lib, {}) for lib in sorted(glob.glob(os.path.join(root, "build/variants/lib_*.so")))]
+runs = [(lib, {"MSG_PROG_EVERY": v}) for lib in sorted(glob.glob(os.path.join(root, "build/variants/lib_*.so")))
+        for v in sys.argv[1:] or ["64"]]
 runs += [(os.path.join(root, "paper_2512_16099_b200/libmigsched_b200.so"), {"MSG_PROG_EVERY": v})
          for v in sys.argv[1:] or ["32"]]
 for lib, extra in runs:
