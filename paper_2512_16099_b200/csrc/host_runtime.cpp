@@ -63,6 +63,7 @@ struct msg_staged {
     uint32_t large_min_g = 0;
     const PeerBinding* peer = nullptr;  // set by msg_run_peer for one launch
     bool no_rerun = false;              // multi-GPU run: an output overflow cannot be re-run alone
+    bool htr_ready = false;             // h_traces already holds the layout (stage_impl's fast path)
     // pinned host mirrors (rank order)
     HostBuf h_arrival, h_service, h_profile, h_perm, h_ids;
     HostBuf h_jobs, h_events, h_timeline, h_summary;
@@ -218,8 +219,12 @@ inline void put_rows(msg_job_row* rows, uint32_t n, const int64_t* ids, const do
 // True when [p, p + bytes) is page-locked host memory this process has
 // registered with CUDA (cudaHostAlloc / msg_host_alloc / cudaHostRegister):
 // the copy engines can read it directly.
-bool host_pinned(const void* p, size_t bytes) {
+// *dev (optional): the device view of p (mapped page-locked memory: with
+// unified addressing the address itself), null if not mapped.
+bool host_pinned(const void* p, size_t bytes, const void** dev = nullptr) {
+    if (dev) *dev = nullptr;
     if (!p || !bytes) return false;
+    bool first = true;
     for (const void* q : {p, static_cast<const void*>(static_cast<const char*>(p) + bytes - 1)}) {
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
@@ -227,21 +232,12 @@ bool host_pinned(const void* p, size_t bytes) {
             return false;
         }
         if (at.type != cudaMemoryTypeHost) return false;
+        if (first && dev) *dev = at.devicePointer;
+        first = false;
     }
     return true;
 }
 
-// Device view of page-locked host memory (mapped: with unified addressing
-// the host address itself), or null when `p` is not CUDA-registered.
-template <class T>
-const T* dev_view(const T* p) {
-    cudaPointerAttributes at{};
-    if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    return at.type == cudaMemoryTypeHost ? static_cast<const T*>(at.devicePointer) : nullptr;
-}
 
 // stage_impl's second half: pinned staging (unless deferred), device
 // buffers, the H2D copies of configs / init / traces, and the ordering event.
@@ -347,11 +343,9 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     s->message.resize(s->n_in);
     s->dev_index.assign(s->n_in, -1);
     s->gpu_count.assign(s->n_in, 0);
-    s->src_of.clear();
-    s->traces.clear();
     s->configs.clear();
     s->init.clear();
-    s->overlap.clear();
+    s->htr_ready = false;
     s->handler_events = 0;
 
     // Configs referenced by the batch.
@@ -368,22 +362,29 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
     // small-cluster config and no event log / timeline: every trace on the
     // device in input order, so the layout is the batch's own offsets and is
     // filled in parallel.
-    if (defer_arrays && n_cfgs == 1 && cs[0].status == MSG_OK && cfgs[0].gpu_count <= (int)kMaxGpusEnsemble &&
+    bool one_cfg = n_cfgs == 1;
+    if (one_cfg && b->config_index)
+        for (uint32_t t = 0; t < s->n_in && one_cfg; ++t) one_cfg = b->config_index[t] == 0;
+    if (defer_arrays && one_cfg && cs[0].status == MSG_OK && cfgs[0].gpu_count <= (int)kMaxGpusEnsemble &&
         !(flags & (MSG_OUT_EVENTS | MSG_OUT_TIMELINE))) {
         const uint32_t n = s->n_in;
         const uint64_t j0 = n ? b->offsets[0] : 0;
-        s->traces.resize(n);
+        s->traces.resize(n);  // every entry is rewritten below (no clear: no zero-fill pass)
         s->src_of.resize(n);
         s->overlap.assign(n, cfgs[0].migration_overlap_s);
         std::fill(s->gpu_count.begin(), s->gpu_count.end(), cfgs[0].gpu_count);
+        CK(s->h_traces.ensure(std::max<uint32_t>(n, 1) * sizeof(DevTrace)));
+        DevTrace* htr = s->h_traces.as<DevTrace>();  // the pinned copy for the H2D, written alongside
         parallel_for(n, 512, [&](uint32_t t) {
             DevTrace tr{};
             tr.job_off = b->offsets[t] - j0;
             tr.n_jobs = (uint32_t)(b->offsets[t + 1] - b->offsets[t]);
             s->traces[t] = tr;  // cfg 0, identity order until the checks say otherwise
+            htr[t] = tr;
             s->src_of[t] = t;
             s->dev_index[t] = (int32_t)t;
         });
+        s->htr_ready = true;
         s->large_idx.clear();
         s->large_gpus = 0;
         s->large_max_g = s->large_min_g = 0;
@@ -396,6 +397,9 @@ msg_status stage_impl(msg_engine* eng, const msg_trace_batch* b, const msg_confi
         pt.mark("  layout (parallel)");
         return stage_buffers(eng, s, b, true);
     }
+    s->src_of.clear();
+    s->traces.clear();
+    s->overlap.clear();
     // Per-trace validation (parallel), in input order.
     std::vector<TraceCheck> checks(s->n_in);
     for (uint32_t t = 0; t < s->n_in; ++t) {
@@ -846,10 +850,11 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     // ids are not increasing (rank order differs from input order) is
     // staged as usual.  MSG_NO_DIRECT=1 disables it.
     const uint64_t jbase = T ? b->offsets[0] : 0, jall = T ? b->offsets[b->n_traces] - jbase : 0;
+    const void *dv_a = nullptr, *dv_s = nullptr, *dv_p = nullptr;  // device views (zero copy)
     const bool direct = T && jall && s->traces.size() == s->n_in && std::getenv("MSG_NO_DIRECT") == nullptr &&
-                        host_pinned(b->arrival_s + jbase, jall * sizeof(double)) &&
-                        host_pinned(b->service_s + jbase, jall * sizeof(double)) &&
-                        host_pinned(b->profile + jbase, jall * sizeof(int32_t));
+                        host_pinned(b->arrival_s + jbase, jall * sizeof(double), &dv_a) &&
+                        host_pinned(b->service_s + jbase, jall * sizeof(double), &dv_s) &&
+                        host_pinned(b->profile + jbase, jall * sizeof(int32_t), &dv_p);
     if (direct) CK(s->d_prof32.ensure(N * sizeof(int32_t)));
     CK(s->h_traces.ensure(std::max<uint32_t>(T, 1) * sizeof(DevTrace)));
     uint8_t chunk_direct[kMaxPipeChunks] = {};
@@ -860,9 +865,10 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
     // under the kernel.  A trace failing its check is reported as such (its
     // device results are ignored); a valid trace whose ids are not increasing
     // needs the rank permutation, so then the batch re-runs staged.
-    const double* zc_a = direct && allow_zc && !std::getenv("MSG_NO_ZC") ? dev_view(b->arrival_s + jbase) : nullptr;
-    const double* zc_s = zc_a ? dev_view(b->service_s + jbase) : nullptr;
-    const int32_t* zc_p = zc_s ? dev_view(b->profile + jbase) : nullptr;
+    const bool zc = direct && allow_zc && !std::getenv("MSG_NO_ZC") && dv_a && dv_s && dv_p;
+    const double* zc_a = zc ? static_cast<const double*>(dv_a) : nullptr;
+    const double* zc_s = zc ? static_cast<const double*>(dv_s) : nullptr;
+    const int32_t* zc_p = zc ? static_cast<const int32_t*>(dv_p) : nullptr;
     // Progressive rows (default with zero copy; MSG_PIPE_PROG=0 / 1 forces
     // off / on): each warp also publishes the completed prefix of its
     // trace's records as it goes, so the host decodes rows while the kernel
@@ -884,13 +890,13 @@ msg_status run_pipelined(msg_engine* eng, const msg_trace_batch* b, msg_staged* 
         const unsigned long v = std::strtoul(e, nullptr, 10);
         if (v >= 32 && (v & (v - 1)) == 0) prog_mask = (uint32_t)v - 1;
     }
-    for (int k = 0; k < n_chunks; ++k) CK(cudaStreamWaitEvent(eng->pstream[k], eng->staged, 0));
+    for (int k = 0; k < (zc_p ? 1 : n_chunks); ++k) CK(cudaStreamWaitEvent(eng->pstream[k], eng->staged, 0));
     if (zc_p) {
         cudaStream_t st = eng->pstream[0];
         n_chunks = 1;
         d0s[1] = T;
         DevTrace* htr = s->h_traces.as<DevTrace>();
-        std::memcpy(htr, s->traces.data(), T * sizeof(DevTrace));
+        if (!s->htr_ready) std::memcpy(htr, s->traces.data(), T * sizeof(DevTrace));  // (the fast layout wrote it)
         CK(cudaMemcpyAsync(s->d_traces.as<DevTrace>(), htr, T * sizeof(DevTrace), cudaMemcpyHostToDevice, st));
         SimArgs c = a;
         c.perm = nullptr;
