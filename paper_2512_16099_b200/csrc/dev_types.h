@@ -191,6 +191,7 @@ struct SimArgs {
     uint64_t rows_soa;
     uint32_t n_traces;
     uint32_t out_flags;
+    uint32_t no_delay;  // every config: reconfig latency 0 and migration overlap 0 (the ND kernels)
     // block engine (G > 32): cluster arena, indexed by GPU (cl_goff + g) or
     // slot (8 * (cl_goff + g) + s), and the list of large traces
     const uint32_t* large_idx;

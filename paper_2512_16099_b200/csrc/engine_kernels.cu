@@ -27,7 +27,7 @@ __device__ unsigned long long g_ttimes[4 * kTraceTimesCap];
 __device__ unsigned g_tt_n;
 #endif
 
-template <int SPL, bool DETAIL, bool IO>
+template <int SPL, bool DETAIL, bool IO, bool ND>
 #ifndef MSG_SIM_MINB
 #define MSG_SIM_MINB 7
 #endif
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MSG_SIM_MINB) sim_kernel(
 #ifdef MSG_TRACE_TIMES
     const uint64_t t0 = wp::gtime_ns();
 #endif
-    simulate_trace<SPL, DETAIL, IO>(a, tb, ws, t);
+    simulate_trace<SPL, DETAIL, IO, ND>(a, tb, ws, t);
 #ifdef MSG_TRACE_TIMES
     if (wp::lane() == 0) {
         const unsigned k = atomicAdd(&g_tt_n, 1u);
@@ -64,18 +64,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, MSG_SIM_MINB) sim_kernel(
 #endif
 }
 
-template <int SPL, bool DETAIL, bool IO = false>
+template <int SPL, bool DETAIL, bool IO, bool ND>
 static cudaError_t launch_sim_t(const SimArgs& a, cudaStream_t stream) {
     static_assert(sizeof(DevTables) % 16 == 0, "tables must be 16-byte sized");
     static_assert(sizeof(WarpSmem<SPL>) % 16 == 0, "warp state must be 16-byte sized");
     const size_t smem = sizeof(DevTables) + kWarpsPerBlock * sizeof(WarpSmem<SPL>);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(sim_kernel<SPL, DETAIL, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(sim_kernel<SPL, DETAIL, IO, ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     const unsigned blocks = (a.n_traces + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return cudaSuccess;
-    sim_kernel<SPL, DETAIL, IO><<<blocks, 32 * kWarpsPerBlock, smem, stream>>>(a);
+    sim_kernel<SPL, DETAIL, IO, ND><<<blocks, 32 * kWarpsPerBlock, smem, stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -186,38 +186,46 @@ cudaError_t launch_cluster(const SimArgs& a, cudaStream_t stream) {
     return detail ? launch_cluster_t<true, W>(a, stream) : launch_cluster_t<false, W>(a, stream);
 }
 
-cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream) {
+template <bool ND>
+static cudaError_t launch_sim_nd(int spl, const SimArgs& a, cudaStream_t stream) {
     const bool detail = (a.out_flags & (OF_EVENTS | OF_TIMELINE)) != 0;
     if (a.zc_arrival || a.prog_host) {  // the pipelined msg_run_batch's host-I/O kernel (summary / rows only)
         if (detail) return cudaErrorInvalidValue;
         switch (spl) {
-            case 1: return launch_sim_t<1, false, true>(a, stream);
-            case 2: return launch_sim_t<2, false, true>(a, stream);
-            case 4: return launch_sim_t<4, false, true>(a, stream);
-            case 8: return launch_sim_t<8, false, true>(a, stream);
+            case 1: return launch_sim_t<1, false, true, ND>(a, stream);
+            case 2: return launch_sim_t<2, false, true, ND>(a, stream);
+            case 4: return launch_sim_t<4, false, true, ND>(a, stream);
+            case 8: return launch_sim_t<8, false, true, ND>(a, stream);
             default: return cudaErrorInvalidValue;
         }
     }
     switch (spl) {
-        case 1: return detail ? launch_sim_t<1, true>(a, stream) : launch_sim_t<1, false>(a, stream);
-        case 2: return detail ? launch_sim_t<2, true>(a, stream) : launch_sim_t<2, false>(a, stream);
-        case 4: return detail ? launch_sim_t<4, true>(a, stream) : launch_sim_t<4, false>(a, stream);
-        case 8: return detail ? launch_sim_t<8, true>(a, stream) : launch_sim_t<8, false>(a, stream);
+        case 1: return detail ? launch_sim_t<1, true, false, ND>(a, stream) : launch_sim_t<1, false, false, ND>(a, stream);
+        case 2: return detail ? launch_sim_t<2, true, false, ND>(a, stream) : launch_sim_t<2, false, false, ND>(a, stream);
+        case 4: return detail ? launch_sim_t<4, true, false, ND>(a, stream) : launch_sim_t<4, false, false, ND>(a, stream);
+        case 8: return detail ? launch_sim_t<8, true, false, ND>(a, stream) : launch_sim_t<8, false, false, ND>(a, stream);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_sim(int spl, const SimArgs& a, cudaStream_t stream) {
+    return a.no_delay ? launch_sim_nd<true>(spl, a, stream) : launch_sim_nd<false>(spl, a, stream);
 }
 
 // Load every event-loop and block-engine kernel now (the runtime otherwise
 // loads a kernel lazily at its first launch, ~10 ms on the first call).
 cudaError_t preload_engine_kernels() {
     cudaFuncAttributes fa;
+#define MSG_SIM_FNS(ND)                                                                                   \
+    (const void*)sim_kernel<1, false, false, ND>, (const void*)sim_kernel<1, true, false, ND>,             \
+        (const void*)sim_kernel<2, false, false, ND>, (const void*)sim_kernel<2, true, false, ND>,         \
+        (const void*)sim_kernel<4, false, false, ND>, (const void*)sim_kernel<4, true, false, ND>,         \
+        (const void*)sim_kernel<8, false, false, ND>, (const void*)sim_kernel<8, true, false, ND>,         \
+        (const void*)sim_kernel<1, false, true, ND>, (const void*)sim_kernel<2, false, true, ND>,           \
+        (const void*)sim_kernel<4, false, true, ND>, (const void*)sim_kernel<8, false, true, ND>
     const void* fns[] = {
-        (const void*)sim_kernel<1, false, false>, (const void*)sim_kernel<1, true, false>,
-        (const void*)sim_kernel<2, false, false>, (const void*)sim_kernel<2, true, false>,
-        (const void*)sim_kernel<4, false, false>, (const void*)sim_kernel<4, true, false>,
-        (const void*)sim_kernel<8, false, false>, (const void*)sim_kernel<8, true, false>,
-        (const void*)sim_kernel<1, false, true>,  (const void*)sim_kernel<2, false, true>,
-        (const void*)sim_kernel<4, false, true>,  (const void*)sim_kernel<8, false, true>,
+        MSG_SIM_FNS(false), MSG_SIM_FNS(true),
+#undef MSG_SIM_FNS
         (const void*)cluster_kernel<false, MSG_CLUSTER_THREADS_WIDE>,
         (const void*)cluster_kernel<true, MSG_CLUSTER_THREADS_WIDE>,
         (const void*)cluster_kernel<false, MSG_CLUSTER_THREADS_NARROW>,

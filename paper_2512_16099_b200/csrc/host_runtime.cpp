@@ -524,6 +524,11 @@ SimArgs make_args(msg_engine* eng, msg_staged* s) {
     a.summary = s->d_summary.as<DevSummary>();
     a.n_traces = (uint32_t)s->traces.size();
     a.out_flags = s->out_flags;
+    // the no-delay kernels (engine_core.cuh, ND): reconfiguration latency
+    // exactly +0 and no migration overlap in every config of the batch
+    a.no_delay = 1;
+    for (const DevConfig& c : s->configs)
+        if (!(c.latency == 0.0 && !std::signbit(c.latency) && c.overlap <= 0.0)) a.no_delay = 0;
     a.n_large = (uint32_t)s->large_idx.size();
     if (a.n_large) {
         a.large_idx = s->d_large_idx.as<uint32_t>();

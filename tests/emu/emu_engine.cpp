@@ -2,6 +2,7 @@
 // (paper_2512_16099_b200/csrc/engine_core.cuh) on 32 host threads per trace,
 // with the product's own staging/decoding (staging.h), and returns results
 // in the ABI record formats so tests can diff them against the reference.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
@@ -26,8 +27,8 @@ struct EmuResult {
     std::vector<msg_timeline_point> timeline;
 };
 
-template <int SPL>
-void run_warp(const SimArgs& a, const DevTables* tb) {
+template <int SPL, bool ND = false>
+void run_warp_t(const SimArgs& a, const DevTables* tb) {
     auto ws = std::make_unique<WarpSmem<SPL>>();
     std::memset(ws.get(), 0xA5, sizeof(WarpSmem<SPL>));  // garbage, like real smem
     wp::EmuWarp warp;
@@ -37,10 +38,17 @@ void run_warp(const SimArgs& a, const DevTables* tb) {
             wp::g_warp = &warp;
             wp::g_lane = l;
             wp::g_phase = 0;
-            simulate_trace<SPL>(a, tb, ws.get(), 0);
+            simulate_trace<SPL, true, false, ND>(a, tb, ws.get(), 0);
         });
     }
     for (auto& t : lanes) t.join();
+}
+// MSG_EMU_ND=1: the no-delay instantiation, as the library picks it (reconfig
+// latency +0 and no migration overlap)
+template <int SPL>
+void run_warp(const SimArgs& a, const DevTables* tb) {
+    if (a.no_delay) run_warp_t<SPL, true>(a, tb);
+    else run_warp_t<SPL, false>(a, tb);
 }
 
 // The pipelined msg_run_batch's IO instantiation (zero-copy inputs,
@@ -176,6 +184,8 @@ void* emu_run(const msg_trace_batch* b, uint32_t t, const msg_config* c) {
     a.summary = &sum;
     a.n_traces = 1;
     a.out_flags = OF_JOBS | OF_EVENTS | OF_TIMELINE;
+    a.no_delay = std::getenv("MSG_EMU_ND") && cs.dev.latency == 0.0 && !std::signbit(cs.dev.latency) &&
+                 cs.dev.overlap <= 0.0;
     const int G = c->gpu_count;
     // block-engine arena (used when G > 32, or when MSG_EMU_FORCE_BLOCK is set)
     const size_t ns = 8 * (size_t)G;

@@ -78,3 +78,34 @@ def test_emulated_io_kernel_long_traces(monkeypatch):
         want.events = want.frag_timeline = None
         got.events = got.frag_timeline = None
         assert diff_results(want, got) == "", (n, G)
+
+
+@pytest.mark.parametrize("name", sorted(golden_runs().keys()))
+def test_emulated_no_delay_kernel_matches_golden(name, monkeypatch):
+    """The no-delay instantiation (chosen when every config has reconfig
+    latency +0 and no migration overlap: no slot is ever WaitingStart or
+    Draining) reproduces the golden runs it applies to, event log included;
+    the others run the general kernel."""
+    batch, cfg, ref, _ = golden_runs()[name]
+    monkeypatch.setenv("MSG_EMU_ND", "1")
+    got = emu_run_batch_results(batch, [cfg])[0]
+    assert diff_results(ref, got) == ""
+
+
+@pytest.mark.skipif(not rb.port_available(), reason="oracle port not built")
+def test_emulated_no_delay_kernel_vs_port(monkeypatch):
+    from paper_2512_16099_b200.engine import generate
+
+    monkeypatch.setenv("MSG_EMU_ND", "1")
+    rng = np.random.default_rng(5)
+    for _ in range(8):
+        G = int(rng.choice([2, 4, 8, 16]))
+        feats = FeatureFlags(bool(rng.integers(0, 2)), True, bool(rng.integers(0, 2)))
+        sp = WorkloadSpec(mean_interarrival_s=float(rng.choice([0.5, 2.0, 10.0])), job_count=80,
+                          seed=int(rng.integers(0, 1 << 30)))
+        cfg = SimConfig(gpu_count=G, sched=SchedulerConfig(threshold=float(rng.choice([0.0, 0.4, 1.0])),
+                                                           features=feats))
+        b = TraceBatch.from_traces([generate(sp)])
+        want = rb.port_run_batch_results(b, [cfg])[0]
+        got = emu_run_batch_results(b, [cfg])[0]
+        assert diff_results(want, got) == "", (G, feats)
