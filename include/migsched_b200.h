@@ -276,6 +276,10 @@ msg_status msg_engine_sync(msg_engine* engine);
 msg_status msg_time_launch(msg_engine* engine, msg_staged* staged, float* ms);
 /* Write a buffer larger than L2 (256 MiB) so the next launch starts cold. */
 msg_status msg_engine_flush_l2(msg_engine* engine);
+/* The same write enqueued on the engine stream without waiting for it: the
+ * launch that follows is queued behind it, so a kernel timed next starts on
+ * a busy device (its host launch latency is not inside the events). */
+msg_status msg_engine_flush_l2_async(msg_engine* engine);
 
 /* ---- multi-GPU: one large trace split over the B200s of one NVLink /
  * NVSwitch domain, one process per GPU (configuration C4) ------

@@ -1480,12 +1480,18 @@ msg_status msg_time_launch(msg_engine* eng, msg_staged* s, float* ms) {
 }
 
 msg_status msg_engine_flush_l2(msg_engine* eng) {
+    msg_status st = msg_engine_flush_l2_async(eng);
+    if (st != MSG_OK) return st;
+    CK(cudaStreamSynchronize(eng->stream));
+    return MSG_OK;
+}
+
+msg_status msg_engine_flush_l2_async(msg_engine* eng) {
     if (!eng) return MSG_ERR_INVALID_ARGUMENT;
     cudaSetDevice(eng->device);
     const size_t bytes = 256ull << 20;
     CK(eng->flush.ensure(bytes));
     CK(cudaMemsetAsync(eng->flush.p, eng->launches & 0xFF, bytes, eng->stream));
-    CK(cudaStreamSynchronize(eng->stream));
     return MSG_OK;
 }
 

@@ -33,6 +33,11 @@
 // the !dyn / first-fit variants, take the per-start path (tables in shared
 // memory, or in global memory for the rare draining word).
 //
+// The TMA kernel's default path keeps key-only item keys [pass|rank|
+// !reused|word] (MSG_SCORE_KF): the start is recovered once per snapshot
+// from the winning word (with_start), and a snapshot that is one item is
+// finished by the block that scored it (no merge kernel).
+//
 // Bound: HBM bandwidth — 8 B per scored GPU.
 #include <cuda_runtime.h>
 
@@ -55,6 +60,9 @@ constexpr int kScoreThreads = MSG_SCORE_THREADS;
 #endif
 #ifndef MSG_SCORE_MINB
 #define MSG_SCORE_MINB 2
+#endif
+#ifndef MSG_SCORE_KF
+#define MSG_SCORE_KF 1  // key-only per-word keys, the start recovered per snapshot by the merge
 #endif
 #ifndef MSG_SCORE_ITEM
 #define MSG_SCORE_ITEM 4
@@ -300,6 +308,78 @@ __device__ __forceinline__ bool score_word_fast32(const uint32_t* T, uint64_t w,
     return plain;
 }
 
+#if MSG_SCORE_KF
+// The key-only form (MSG_SCORE_KF, default): the start is not carried in the
+// key — the item keys hold [pass|rank|!reused|word] and score_reduce_kernel
+// recovers the winning word's start once per snapshot (word_start) — so a
+// word costs fewer ALU ops: no start field, no per-word draining test (the
+// busy/blocked XORs are ORed per thread and a thread that saw a draining
+// word rescores its chunk), counts summed unmasked.  Entry bits: 31 pass
+// (Busy), 30..26 cost rank, 25 !reused (the key, less the word index);
+// 18..12 the minimum-rank starts (reuse check against the word's idle-exact
+// bits shifted to 12); 11..6 / 5..0 the candidate count when the row is Lazy
+// / Busy (a thread sums at most 8 words x 7 starts = 56 per field, so the
+// fields never carry; the bits above them are don't-care in the sum).
+constexpr unsigned kNoCandKf = 0xFE000000u;  // key >= kNoCandKey, no counts, no starts
+
+__device__ __forceinline__ void fast_tabkf_init(uint32_t* t, const uint16_t* g, unsigned lazymask) {
+    for (unsigned i = threadIdx.x; i < (unsigned)kScoreTabEntries; i += blockDim.x) {
+        const unsigned e = __ldg(g + i);
+        const unsigned pc = (i >> 8) & 7u;
+        const unsigned cnt = e & 7u, mm = (e >> 3) & 0x7Fu, rank = (e >> 10) & 0x1Fu;
+        const unsigned busy = ((lazymask >> pc) & 1u) ^ 1u;
+        t[i] = cnt ? (busy << 31) | (rank << 26) | (1u << 25) | (mm << 12) | (cnt << (busy ? 0 : 6)) : kNoCandKf;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void score_word_kf(const uint32_t* T, uint64_t w, unsigned l, unsigned& best,
+                                              unsigned& cnt, unsigned& dr) {
+    using Q = Prof<P>;
+    const unsigned lo = (unsigned)w;
+    dr |= lo ^ (lo >> 8);  // bits 15..8: busy memory ^ blocked memory (a draining instance)
+    const unsigned e = T[(unsigned)__popc(lo & 0x7Fu) * 256u + ((lo >> 8) & 0xFFu)];
+    // a minimum-rank start with an idle-exact instance: reuse it (!reused
+    // cleared; scheduler.cpp:62-66)
+    const bool reuse = (e & (unsigned)(w >> (12 + Q::pbase)) & 0x7F000u) != 0;
+    best = min(best, (e & (reuse ? 0xFC000000u : 0xFE000000u)) | l);
+    cnt += e;
+}
+
+template <int P, int NW2>
+__device__ __forceinline__ void score_words_fast32(const uint32_t* T, const DevTables* tb, const ulonglong2 (&x)[NW2],
+                                                   unsigned l0, unsigned lazymask, ItemAcc& acc) {
+    const unsigned best0 = acc.best;
+    unsigned cnt = 0, dr = 0;
+#pragma unroll
+    for (int k = 0; k < NW2; ++k) {
+        const unsigned l = l0 + (unsigned)k * 2 * kScoreThreads;
+        score_word_kf<P>(T, x[k].x, l, acc.best, cnt, dr);
+        score_word_kf<P>(T, x[k].y, l + 1u, acc.best, cnt, dr);
+    }
+    if (__builtin_expect(__any_sync(0xffffffffu, (dr & 0xFF00u) != 0), 0)) {
+        if (dr & 0xFF00u) {  // this thread saw a draining word: rescore its words
+            unsigned best = best0, c2 = 0, d2 = 0;
+#pragma unroll
+            for (int k = 0; k < 2 * NW2; ++k) {  // static indices: the words stay in registers
+                const uint64_t w = (k & 1) ? x[k >> 1].y : x[k >> 1].x;
+                const unsigned l = l0 + (unsigned)(k >> 1) * 2 * kScoreThreads + (unsigned)(k & 1);
+                const unsigned lo = (unsigned)w;
+                if (((lo ^ (lo >> 8)) & 0xFF00u) == 0) {
+                    score_word_kf<P>(T, w, l, best, c2, d2);
+                } else {
+                    const uint2 g = score_word_generic<P>(tb, w, l, lazymask);
+                    best = min(best, (g.x & 0xFE000000u) | l);
+                    acc.cnt += g.y;
+                }
+            }
+            acc.best = best;
+            cnt = c2;
+        }
+    }
+    acc.cnt += (((cnt >> 6) & 63u) << 16) + (cnt & 63u);  // Lazy in the high half
+}
+#else
 template <int P, int NW2>
 __device__ __forceinline__ void score_words_fast32(const uint32_t* T, const DevTables* tb, const ulonglong2 (&x)[NW2],
                                                    unsigned l0, unsigned lazymask, ItemAcc& acc) {
@@ -324,6 +404,7 @@ __device__ __forceinline__ void score_words_fast32(const uint32_t* T, const DevT
         }
     }
 }
+#endif
 
 // The thread's words of one chunk (x[k].x at local index l_k, x[k].y at
 // l_k + 1), all through the table, then the draining ones (if any in the
@@ -693,6 +774,41 @@ __device__ __forceinline__ void consume_fast(const ScoreArgs& a, const TmaSmem& 
     }
 }
 
+// With key-only item keys (MSG_SCORE_KF) the winning word's start is
+// recovered here, once per snapshot: the lowest start among the word's
+// available starts with the key's cost rank and reuse flag
+// (candidate_starts + Candidate::better_than, scheduler.cpp:19-43).
+__device__ __forceinline__ unsigned word_start(const DevTables* tb, uint64_t w, unsigned p, unsigned key7) {
+    const unsigned lo = (unsigned)w;
+    const unsigned cs = (kCsPack >> (4 * p)) & 0xFu, ms = (kMsPack >> (4 * p)) & 0xFu;
+    const unsigned n = (kCountPack >> (4 * p)) & 0xFu, st = (kStridePack >> (4 * p)) & 0xFu;
+    const unsigned pbase = (0x00B74210u >> (4 * p)) & 0xFu;
+    const unsigned pc = (unsigned)__popc(lo & 0x7Fu), bm = (lo >> 8) & 0xFFu, km = (lo >> 16) & 0xFFu;
+    const unsigned row = min(pc + cs, 7u);
+    const unsigned ex = (unsigned)(w >> (24 + pbase));
+    for (unsigned j = 0; j < n; ++j) {
+        const unsigned fm = ((1u << ms) - 1u) << (j * st);
+        if (fm & km) continue;
+        const unsigned r = tb->cost2rank[row * 256 + (bm | fm)];
+        if (((r << 1) | (((ex >> j) & 1u) ^ 1u)) == (key7 & 0x3Fu)) return j * st;
+    }
+    return 0;
+}
+
+// The snapshot's merged key with its start filled in (key-only item keys).
+__device__ __forceinline__ uint64_t with_start(const ScoreArgs& a, uint32_t s, uint64_t best) {
+    const uint64_t gpu = (best >> 3) & 0xFFFFFFFFull;
+    const uint64_t w = a.words[(uint64_t)s * a.G + gpu];
+    const unsigned p = a.profile[s], lo = (unsigned)w;
+    if (((lo ^ (lo >> 8)) & 0xFF00u) == 0) {  // no draining instance: the per-word table's starts
+        const unsigned e = a.stab[p * 2048u + (unsigned)__popc(lo & 0x7Fu) * 256u + ((lo >> 8) & 0xFFu)];
+        const unsigned mm = (e >> 3) & 0x7Fu, pbase = (0x00B74210u >> (4 * p)) & 0xFu;
+        const unsigned sel = ((best >> 35) & 1u) ? mm : mm & (unsigned)(w >> (24 + pbase));
+        return best | (uint64_t)(((unsigned)__ffs(sel) - 1u) * ((kStridePack >> (4 * p)) & 0xFu));
+    }
+    return best | word_start(a.tables, w, p, (unsigned)(best >> 35));
+}
+
 template <bool LB, bool DYN>
 __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kernel(ScoreArgs a) {
     constexpr bool kFast = LB && DYN;
@@ -708,7 +824,11 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
     asm volatile("griddepcontrol.launch_dependents;");
     if constexpr (kT32) {
         uint32_t* t32 = reinterpret_cast<uint32_t*>(dyn_smem);
+#if MSG_SCORE_KF
+        fast_tabkf_init(t32, a.stab, a.lazymask);
+#else
         fast_tab32_init(t32, a.stab, a.lazymask);
+#endif
         sm.ft32 = t32;
     } else if constexpr (kFast) {
         fast_tab_init(tabs, a.stab, a.lazymask);
@@ -767,8 +887,13 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
                 }
                 uint64_t g64 = ~0ull;
                 if (best != 0xFFFFFFFFu) {
-                    const uint64_t gpu = (uint64_t)m.first * kChunk + ((best >> 3) & ((1u << 22) - 1u));
-                    g64 = ((uint64_t)(best >> 25) << 35) | (gpu << 3) | (best & 7u);
+                    if constexpr (kT32 && MSG_SCORE_KF) {  // [pass|rank|!reused|word]; the start: the merge
+                        const uint64_t gpu = (uint64_t)m.first * kChunk + (best & ((1u << 22) - 1u));
+                        g64 = ((uint64_t)(best >> 25) << 35) | (gpu << 3);
+                    } else {
+                        const uint64_t gpu = (uint64_t)m.first * kChunk + ((best >> 3) & ((1u << 22) - 1u));
+                        g64 = ((uint64_t)(best >> 25) << 35) | (gpu << 3) | (best & 7u);
+                    }
                 }
                 uint64_t* it = a.items + 2 * ((uint64_t)m.snap * items_per + m.first / kItemChunks);
                 it[0] = g64;
@@ -776,11 +901,25 @@ __global__ void __launch_bounds__(kScoreThreads, MSG_SCORE_MINB) score_tma_kerne
             }
         }
     }
+    if (items_per == 1) {
+        // every snapshot is one item (G <= one item's words): the block
+        // finishes the snapshots it scored — no merge kernel; the key-only
+        // keys get their start here, one dependent lookup per snapshot,
+        // all of the block's snapshots in parallel
+        __syncthreads();  // thread 0's item results are visible to the block
+        for (uint64_t it = blockIdx.x + (uint64_t)threadIdx.x * gridDim.x; it < n_items;
+             it += (uint64_t)blockDim.x * gridDim.x) {
+            uint64_t best = a.items[2 * it];
+            if (kT32 && MSG_SCORE_KF && best != ~0ull) best = with_start(a, (uint32_t)it, best);
+            a.out[2 * it] = best;
+            a.out[2 * it + 1] = a.items[2 * it + 1];
+        }
+    }
 }
 
 // After the scoring grid (TMA path): each snapshot's items merge into its
 // output — minimum key, summed Lazy/Busy candidate counts.
-__global__ void score_reduce_kernel(ScoreArgs a, uint32_t items_per) {
+__global__ void score_reduce_kernel(ScoreArgs a, uint32_t items_per, uint32_t kf) {
     asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the scoring grid
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -791,6 +930,7 @@ __global__ void score_reduce_kernel(ScoreArgs a, uint32_t items_per) {
         best = it[2 * i] < best ? it[2 * i] : best;
         cnt += it[2 * i + 1];
     }
+    if (kf && best != ~0ull) best = with_start(a, s, best);
     a.out[2 * s] = best;
     a.out[2 * s + 1] = cnt;
 }
@@ -852,7 +992,7 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
         case 6: score_tma_kernel<true, false><<<grid, block, kTmaDynBytes, stream>>>(a); break;
         default: score_tma_kernel<true, true><<<grid, block, kTmaDynBytesFast, stream>>>(a); break;
     }
-    if (!tma) return cudaGetLastError();
+    if (!tma || items / a.n == 1) return cudaGetLastError();  // one item per snapshot: merged in the grid
     // The merge launches as a programmatic dependent: its launch overlaps
     // the scoring grid's tail; griddepcontrol.wait holds its reads until the
     // scoring grid has completed.
@@ -865,7 +1005,8 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t stream) {
     lc.numAttrs = 1;
     lc.gridDim = dim3((a.n + 255) / 256);
     lc.blockDim = dim3(256);
-    cudaError_t e = cudaLaunchKernelEx(&lc, score_reduce_kernel, a, (uint32_t)(items / a.n));
+    const uint32_t kf = (MSG_SCORE_T32 && MSG_SCORE_KF && a.lb && a.dyn) ? 1u : 0u;
+    cudaError_t e = cudaLaunchKernelEx(&lc, score_reduce_kernel, a, (uint32_t)(items / a.n), kf);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

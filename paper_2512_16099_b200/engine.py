@@ -49,6 +49,7 @@ def lib():
         "msg_engine_sync": (C.c_int, [vp]),
         "msg_time_launch": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
         "msg_engine_flush_l2": (C.c_int, [vp]),
+        "msg_engine_flush_l2_async": (C.c_int, [vp]),
         "msg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
         "msg_host_free": (None, [vp]),
         "msg_result_n_traces": (u32, [vp]),
@@ -164,8 +165,10 @@ class Engine:
     def sync(self):
         _check(lib().msg_engine_sync(self._h), self)
 
-    def flush_l2(self):
-        _check(lib().msg_engine_flush_l2(self._h), self)
+    def flush_l2(self, sync: bool = True):
+        """Write 256 MiB (more than L2) on the engine stream; sync=False
+        leaves it queued so the next timed launch starts on a busy device."""
+        _check((lib().msg_engine_flush_l2 if sync else lib().msg_engine_flush_l2_async)(self._h), self)
 
     def run_batch(self, batch: TraceBatch, cfgs: Sequence[SimConfig], out_flags: int = abi.OUT_JOBS) -> "BatchResult":
         """migsched::run over every trace of the batch (sim.cpp:504-507)."""
