@@ -222,11 +222,12 @@ def test_schedule_random_clusters(d, G):
             assert got.tobytes() == want.tobytes(), (op, thr, lb, dyn)
 
 
-@pytest.mark.parametrize("G", [9000, 16386])
+@pytest.mark.parametrize("G", [9000, 16384, 16386])
 def test_schedule_multi_item_snapshots(d, G):
-    """Snapshots longer than one scorer item (4 chunks of 2048 GPUs): 9000
-    GPUs = 2 items, 16386 = 3 items with a 2-GPU tail; the snapshot's last
-    item to finish merges them.  Configs alternate so consecutive launches
+    """Snapshots around one scorer item (4 chunks of 4096 GPUs): 9000 GPUs =
+    one item with a ragged last chunk, 16384 = exactly one item (finished
+    in the scoring grid, no merge kernel), 16386 = 2 items with a 2-GPU
+    tail (merge kernel).  Configs alternate so consecutive launches
     exercise both pass-2 list counters, and the register path (an odd
     count, G + 1) runs between them."""
     rng = np.random.default_rng(G)

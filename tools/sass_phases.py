@@ -18,7 +18,7 @@ from collections import Counter
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "paper_2512_16099_b200", "csrc", "engine_core.cuh")
 LIB = os.path.join(ROOT, "paper_2512_16099_b200", "libmigsched_b200.so")
-KERNEL = "_ZN4msgk10sim_kernelILi2ELb0ELb0EEEvNS_7SimArgsE"
+KERNEL = os.environ.get("SIM_KERNEL", "_ZN4msgk10sim_kernelILi2ELb0ELb0ELb1EEEvNS_7SimArgsE")
 
 
 def main():
