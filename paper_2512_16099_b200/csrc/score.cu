@@ -62,7 +62,7 @@ constexpr int kScoreThreads = MSG_SCORE_THREADS;
 #define MSG_SCORE_MINB 2
 #endif
 #ifndef MSG_SCORE_KF
-#define MSG_SCORE_KF 1  // key-only per-word keys, the start recovered per snapshot by the merge
+#define MSG_SCORE_KF 1  // key-only per-word keys, the start recovered once per snapshot (with_start)
 #endif
 #ifndef MSG_SCORE_ITEM
 #define MSG_SCORE_ITEM 4
@@ -310,8 +310,9 @@ __device__ __forceinline__ bool score_word_fast32(const uint32_t* T, uint64_t w,
 
 #if MSG_SCORE_KF
 // The key-only form (MSG_SCORE_KF, default): the start is not carried in the
-// key — the item keys hold [pass|rank|!reused|word] and score_reduce_kernel
-// recovers the winning word's start once per snapshot (word_start) — so a
+// key — the item keys hold [pass|rank|!reused|word] and the winning word's
+// start is recovered once per snapshot (with_start: in the scoring grid when
+// the snapshot is one item, else in score_reduce_kernel) — so a
 // word costs fewer ALU ops: no start field, no per-word draining test (the
 // busy/blocked XORs are ORed per thread and a thread that saw a draining
 // word rescores its chunk), counts summed unmasked.  Entry bits: 31 pass
