@@ -320,3 +320,44 @@ def test_frag_cost_known_answers_and_random_gpus(d):
                 bm |= mm
         n_, den = rb.ref_frag_cost(bc, bm, kc, km)
         assert cost[i] == n_ / den and num[i] * den == n_ * 25200, i
+
+
+def test_scorer_full_size_tma_vs_register_path(d):
+    """bench.py's scorer sweep size (4096 snapshots x 16384 GPUs, 512 MiB),
+    with idle-exact bits and a few draining words: the TMA kernel (key-only
+    keys, merged in the grid) and the independent register-streaming kernel
+    (odd G: the same snapshots less their last word, which is a full GPU
+    with no candidate) agree bit for bit at every threshold.  Both are
+    checked against the reference library at smaller sizes above."""
+    import ctypes as C
+
+    import torch
+
+    L = d._bind()
+    from paper_2512_16099_b200.engine import default_engine
+
+    eng = default_engine(0)
+    B, G = 4096, 16384
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    rnd = torch.randint(0, 1 << 62, (B, G), device="cuda", dtype=torch.int64, generator=gen)
+    bm = rnd & 0x7F
+    idle = ((rnd >> 8) & 0x3FFFF) * (((rnd >> 30) & 3) == 0)
+    drain = ((rnd >> 40) & 0x7F) * (((rnd >> 50) & 4095) == 0)
+    words = bm | (bm << 8) | ((bm | drain) << 16) | (idle << 24)
+    del rnd, bm, idle, drain
+    words[:, G - 1] = 0xFFFF7F  # a full GPU: no candidate
+    words = words.contiguous()
+    odd = words[:, : G - 1].contiguous()
+    prof = torch.randint(0, 6, (B,), device="cuda", dtype=torch.uint8, generator=gen)
+    out_a = torch.empty(B * 2, device="cuda", dtype=torch.int64)
+    out_b = torch.empty(B * 2, device="cuda", dtype=torch.int64)
+    torch.cuda.synchronize()  # the engine launches on its own stream
+    for thr in (0.4, 0.0, 1.0):
+        cfg = d._sched_cfg(SchedulerConfig(threshold=thr))
+        assert L.msg_score_device(eng._h, B, G, words.data_ptr(), prof.data_ptr(), C.byref(cfg),
+                                  out_a.data_ptr()) == 0
+        assert L.msg_score_device(eng._h, B, G - 1, odd.data_ptr(), prof.data_ptr(), C.byref(cfg),
+                                  out_b.data_ptr()) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(out_a, out_b), thr
+        assert int((out_a[0::2] != -1).sum()) > B // 2  # most snapshots have a candidate
