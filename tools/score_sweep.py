@@ -18,7 +18,7 @@ from paper_2512_16099_b200.model import SchedulerConfig  # noqa: E402
 eng = Engine(0)
 peaks, kind = bench.measured_peaks()
 print(json.dumps(bench.scorer_sweep(eng, peaks, kind)["by_threshold"]))
-del_ = torch.cuda.empty_cache()
+torch.cuda.empty_cache()
 L = decisions._bind()
 B, G = 4096, 16384
 gen = torch.Generator(device="cuda").manual_seed(2)
